@@ -1,0 +1,149 @@
+"""Host-side surrogate-tree construction (the narrow phase's input format).
+
+Restates `ltsdem.surrogate.build_surrogate_tree` (surrogate.py:71-119) with
+`_fit_parent_triangle` (surrogate.py:49-68) and `kernels.morton_order`
+(kernels.py:118-135), vectorised over the groups of a level so that the
+20k-particle synthetic scenes build in seconds instead of minutes.  Tree
+construction is input setup and sits outside the hot path (SURVEY.md
+§8(f) item 3 lists a GPU builder as a later row).
+
+The arithmetic matches the reference op for op (centroids by sequential
+row sums, the 3x3 `dgemv` order ``fma(r2,u2, fma(r0,u0, r1*u1))`` for
+``rel @ u``, batched LAPACK SVD which equals the per-group call), so on the
+build container the trees are bit-identical to the reference's
+(`tests/test_host_inputs.py` checks this against reference-built goldens).
+On another host, LAPACK may differ in the last bits; that only changes the
+synthetic input, never the GPU-vs-oracle comparison, which always runs on
+one shared set of trees.
+"""
+
+from __future__ import annotations
+
+import numpy as np
+
+from .bodies import SurrogateLevel, SurrogateTree
+
+_EPS_PAD = 1e-12
+_TINY = 1e-300
+
+
+def morton_order(points: np.ndarray, bits: int = 10) -> np.ndarray:
+    pts = np.atleast_2d(np.asarray(points, dtype=np.float64))
+    lo = pts.min(axis=0)
+    span = pts.max(axis=0) - lo
+    span[span <= 0.0] = 1.0
+    q = ((pts - lo) * ((2 ** bits - 1) / span)).astype(np.uint64)
+    code = np.zeros(len(pts), dtype=np.uint64)
+    for i in range(bits):
+        for axis in range(3):
+            code |= ((q[:, axis] >> np.uint64(i)) & np.uint64(1)) << np.uint64(3 * i + axis)
+    return np.argsort(code, kind="stable")
+
+
+def _fma(a, b, c):
+    # exact FMA for the 3-term dgemv order; see oracle-independent note above
+    from ._fma import fma
+    return fma(a, b, c)
+
+
+def _dgemv_rows(rel: np.ndarray, u: np.ndarray) -> np.ndarray:
+    """(G, m, 3) @ (G, 3) per group, in OpenBLAS dgemv order."""
+    u = u[:, None, :]
+    return _fma(rel[..., 2], u[..., 2], _fma(rel[..., 0], u[..., 0], rel[..., 1] * u[..., 1]))
+
+
+def _row_mean(pts: np.ndarray, axis: int) -> np.ndarray:
+    """numpy mean over a short strided axis: sequential sum, then divide."""
+    n = pts.shape[axis]
+    acc = np.take(pts, 0, axis=axis).copy()
+    for i in range(1, n):
+        acc = acc + np.take(pts, i, axis=axis)
+    return acc / n
+
+
+def _fit_parents(points: np.ndarray) -> np.ndarray:
+    """Parent triangle per group of points (G, m, 3) -> (G, 3, 3)."""
+    centroid = _row_mean(points, 1)
+    rel = points - centroid[:, None, :]
+    _, _, vt = np.linalg.svd(rel, full_matrices=False)
+    u, v = vt[:, 0], vt[:, 1]
+    su = _dgemv_rows(rel, u)
+    sv = _dgemv_rows(rel, v)
+    spread = np.abs(rel).max(axis=(1, 2))
+    spread = np.where(spread == 0.0, 1.0, spread)
+    pad = np.maximum(1e-9, 1e-6 * spread)
+    lo_u = su.min(axis=1) - pad
+    hi_u = su.max(axis=1) + pad
+    lo_v = sv.min(axis=1) - pad
+    hi_v = sv.max(axis=1) + pad
+    w = hi_u - lo_u
+    h = hi_v - lo_v
+    p0 = (centroid + lo_u[:, None] * u) + lo_v[:, None] * v
+    return np.stack([p0, p0 + (2.0 * w)[:, None] * u, p0 + (2.0 * h)[:, None] * v], axis=1)
+
+
+def _point_triangle_dist(p, a, b, c):
+    """kernels.point_triangle_closest distance only (kernels.py:23-75)."""
+    def dot(x, y):
+        return (x[..., 0] * y[..., 0] + x[..., 2] * y[..., 2]) + x[..., 1] * y[..., 1]
+
+    def sdiv(n, d):
+        return n / np.where(np.abs(d) > _TINY, d, 1.0)
+
+    ab, ac, ap, bp, cp = b - a, c - a, p - a, p - b, p - c
+    d1, d2, d3, d4, d5, d6 = dot(ab, ap), dot(ac, ap), dot(ab, bp), dot(ac, bp), dot(ab, cp), dot(ac, cp)
+    vc = d1 * d4 - d3 * d2
+    vb = d5 * d2 - d1 * d6
+    va = d3 * d6 - d5 * d4
+    denom = (va + vb) + vc
+    out = (a + ab * sdiv(vb, denom)[..., None]) + ac * sdiv(vc, denom)[..., None]
+    m = (va <= 0) & (d4 - d3 >= 0) & (d5 - d6 >= 0)
+    out = np.where(m[..., None], b + sdiv(d4 - d3, (d4 - d3) + (d5 - d6))[..., None] * (c - b), out)
+    m = (vb <= 0) & (d2 >= 0) & (d6 <= 0)
+    out = np.where(m[..., None], a + sdiv(d2, d2 - d6)[..., None] * ac, out)
+    m = (vc <= 0) & (d1 >= 0) & (d3 <= 0)
+    out = np.where(m[..., None], a + sdiv(d1, d1 - d3)[..., None] * ab, out)
+    out = np.where(((d6 >= 0) & (d5 <= d6))[..., None], c, out)
+    out = np.where(((d3 >= 0) & (d4 <= d3))[..., None], b, out)
+    out = np.where(((d1 <= 0) & (d2 <= 0))[..., None], a, out)
+    w = p - out
+    return np.sqrt((w[..., 0] * w[..., 0] + w[..., 1] * w[..., 1]) + w[..., 2] * w[..., 2])
+
+
+def build_surrogate_tree(corners, epsilon: float, fanout: int = 4,
+                         max_levels: int = 8) -> SurrogateTree:
+    """Morton-grouped coarsening hierarchy (surrogate.py:71-119)."""
+    if epsilon <= 0.0:
+        raise ValueError(f"epsilon must be positive, got {epsilon}")
+    if fanout < 2:
+        raise ValueError(f"fanout must be at least 2, got {fanout}")
+    corners = np.ascontiguousarray(np.asarray(corners, dtype=np.float64).reshape(-1, 3, 3))
+    levels = [SurrogateLevel(corners=corners, epsilon=np.full(len(corners), float(epsilon)),
+                             children=None)]
+    while levels[-1].size > 1 and len(levels) < max_levels:
+        fine = levels[-1]
+        order = morton_order(_row_mean(fine.corners, 1))
+        n_full = len(order) // fanout
+        groups = [order[i:i + fanout] for i in range(0, len(order), fanout)]
+        parents = np.empty((len(groups), 3, 3))
+        peps = np.empty(len(groups))
+        spans = []
+        if n_full:
+            spans.append((0, n_full, order[:n_full * fanout].reshape(n_full, fanout)))
+        if len(order) % fanout:
+            spans.append((n_full, n_full + 1, order[n_full * fanout:].reshape(1, -1)))
+        for g0, g1, idx in spans:
+            pts = fine.corners[idx].reshape(g1 - g0, -1, 3)
+            tri = _fit_parents(pts)
+            m = pts.shape[1]
+            dist = _point_triangle_dist(
+                pts,
+                np.broadcast_to(tri[:, None, 0], (g1 - g0, m, 3)),
+                np.broadcast_to(tri[:, None, 1], (g1 - g0, m, 3)),
+                np.broadcast_to(tri[:, None, 2], (g1 - g0, m, 3)))
+            child_eps = np.repeat(fine.epsilon[idx], 3, axis=1)
+            parents[g0:g1] = tri
+            peps[g0:g1] = (dist + child_eps).max(axis=1) + _EPS_PAD
+        children = [np.sort(g) for g in groups]
+        levels.append(SurrogateLevel(corners=parents, epsilon=peps, children=children))
+    return SurrogateTree(levels=levels)

@@ -1,0 +1,88 @@
+"""The CPU oracle against the reference's own outputs (golden fixtures).
+
+Every fixture was produced by running the reference (`ltsdem`) itself
+(tests/golden/make_golden.py).  The oracle must reproduce it bit for bit:
+the same floating-point operations in the same order.  This pins the
+oracle before anything is checked against it.
+"""
+
+import numpy as np
+import pytest
+
+from helpers import compare_contacts, compare_result, golden, run_case
+from oracle import narrow_oracle as O
+
+
+def test_point_triangle_rows_bit_exact():
+    g = golden("kernels")["pt"]
+    d, c, _ = O.point_triangle(g["p"], g["a"], g["b"], g["c"])
+    np.testing.assert_array_equal(d, g["dist"])
+    np.testing.assert_array_equal(c, g["closest"])
+
+
+def test_segment_segment_rows_bit_exact():
+    g = golden("kernels")["ss"]
+    d, c1, c2 = O.segment_segment(g["p1"], g["q1"], g["p2"], g["q2"])
+    np.testing.assert_array_equal(d, g["dist"])
+    np.testing.assert_array_equal(c1, g["c1"])
+    np.testing.assert_array_equal(c2, g["c2"])
+
+
+def test_feature_distance_rows_bit_exact():
+    g = golden("kernels")["feat"]
+    np.testing.assert_array_equal(O.tri_pair_distance(g["ta"], g["tb"]), g["dist"])
+
+
+def test_witness_points_and_normals_bit_exact():
+    g = golden("witness")
+    for i in range(len(g["ta"])):
+        d, pa, pb = O.tri_pair_witness(g["ta"][i], g["tb"][i])
+        assert d == g["dist"][i]
+        np.testing.assert_array_equal(pa, g["pa"][i])
+        np.testing.assert_array_equal(pb, g["pb"][i])
+        np.testing.assert_array_equal(O.unit_face_normal(g["ta"][i]), g["na"][i])
+        np.testing.assert_array_equal(O.unit_face_normal(g["tb"][i]), g["nb"][i])
+
+
+def test_overlap_centroid_bit_exact():
+    g = golden("witness")
+    for i in range(len(g["ov_a"])):
+        n = O.unit_face_normal(g["ov_a"][i])
+        out = O.overlap_centroid(g["ov_a"][i], g["ov_b"][i], n)
+        assert (out is not None) == g["ov_has"][i]
+        if out is not None:
+            np.testing.assert_array_equal(out, g["ov_centroid"][i])
+
+
+def _contacts(soa):
+    return [O.Contact(int(soa["body_a"][i]), int(soa["body_b"][i]), soa["position"][i].copy(),
+                      soa["normal"][i].copy(), float(soa["depth"][i]), float(soa["t"][i]),
+                      int(soa["tri_a"][i]), int(soa["tri_b"][i]), float(soa["threshold"][i]))
+            for i in range(len(soa["t"]))]
+
+
+def test_fusion_bit_exact():
+    for k, case in enumerate(golden("fusion")["cases"]):
+        compare_contacts(O.fuse(_contacts(case["raw"])), case["fused"], label=f"fusion {k}")
+
+
+def _scene_ids(name):
+    return [c["name"] for c in golden(name)["cases"]]
+
+
+@pytest.mark.parametrize("idx", range(len(golden("scenes_ccd")["cases"])),
+                         ids=_scene_ids("scenes_ccd"))
+def test_reference_test_scenes_bit_exact(idx):
+    case = golden("scenes_ccd")["cases"][idx]
+    res = run_case(O, case)
+    compare_result(res, case["result"], raw=res.raw, label=case["name"])
+    assert sum(res.stats.values()) == case["rows"]
+
+
+@pytest.mark.parametrize("idx", range(len(golden("scenes_configs")["cases"])),
+                         ids=_scene_ids("scenes_configs"))
+def test_config_shaped_scenes_bit_exact(idx):
+    case = golden("scenes_configs")["cases"][idx]
+    res = run_case(O, case)
+    compare_result(res, case["result"], raw=res.raw, label=case["name"])
+    assert sum(res.stats.values()) == case["rows"]
