@@ -1,0 +1,405 @@
+"""Benchmark of the B200 narrow phase.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+                    [--config c1] [--pairs P]
+
+One step = one batched narrow-phase pass (ltsg_search) over the whole
+workload of the configuration: for c1, 1024 static pairs of 1280-triangle
+noisy icospheres (BASELINE.json configs[0]).  Inputs are seeded synthetic
+scenes (no dataset exists for this path).  Rank 0 prints ONE JSON line.
+
+  value    reference-equivalent triangle-pair tests per second (the rows the
+           reference's _feature_distances evaluates for the same search:
+           screen + zoom + bisection), inputs resident in HBM, device time
+  e2e      the same metric through the public batched API
+           (`ccd.earliest_contacts`) from host bodies: packing, H2D copies,
+           the search and the D2H copy of every result inside the timed region
+  roofline the dominant kernel (k_screen): 984 FP64 flops per test over its
+           CUDA-event time, against the FP64 DFMA peak measured in this run
+  cpu_baseline  the CPU oracle (numpy restatement of the reference) on a
+           bounded sample of the same workload, on this host's cores
+
+`--impl reference` times the CPU oracle alone (the reference is pure
+Python/numpy and cannot travel to the GPU box; the oracle is bit-identical
+to it on the golden fixtures) and prints the same line with "impl".
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+REPO = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, REPO)
+
+FLOPS_PER_TEST = 984  # 6 x 62 point-triangle + 9 x 68 segment-segment
+METRIC = "triangle-pair distance tests/sec"
+CONFIG_DOC = {
+    "c1": "1024 static pairs of 1280-tri noisy icospheres, centre distance U(1.9,2.1), eps 0.01, dt 0",
+    "c2": "4096 domino boxes (12 tris), neighbour pairs within bounding-sphere overlap, eps 1e-3, dt 0",
+    "c3": "20k convex rocks (~124 tris) packed at phi~0.55, bounding-sphere pairs, eps 0.005, dt 0",
+    "c4": "8192 moving pairs of 1280-tri icospheres, v~N(0,1), w~N(0,2), gap U(0,0.5), eps 1e-3, dt 0.1",
+    "c5": "2000 polydisperse mixed meshes, clusters of the swept-sphere graph, eps 1e-3, dt 0.1",
+}
+
+
+def _env_rank():
+    return int(os.environ.get("RANK", 0)), int(os.environ.get("WORLD_SIZE", 1)), \
+        int(os.environ.get("LOCAL_RANK", 0))
+
+
+def build_scene(config: str, rank: int, pairs: int | None):
+    from paper_2309_15417_b200 import scenes
+
+    fn = scenes.CONFIGS[config]
+    kw = {"seed_offset": 100 * rank + int(config[1])}
+    if pairs is not None:
+        key = {"c1": "n_pairs", "c2": "n_boxes", "c3": "n_rocks", "c4": "n_pairs", "c5": "n_particles"}[config]
+        kw[key] = pairs
+    return fn(**kw)
+
+
+def scene_problems(scene):
+    """(pairs of body objects, dt, t_base) per problem, as the public API packs them."""
+    import numpy as np
+
+    if scene.mode == "pair":
+        return [([(scene.body(a), scene.body(b))], float(scene.dt[k]), 0.0)
+                for k, (a, b) in enumerate(scene.pairs)]
+    probs = []
+    for p in range(scene.n_problems):
+        sel = np.flatnonzero(scene.problem == p)
+        probs.append(([(scene.body(scene.pairs[i][0]), scene.body(scene.pairs[i][1])) for i in sel],
+                      float(scene.dt[p]), float(scene.t_base[p])))
+    return probs
+
+
+# ------------------------------------------------------------------ clocks
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+        self.lines = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "200"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+        except (OSError, FileNotFoundError):
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *exc):
+        if self.proc is not None:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], [], set()
+        names = ("hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap")
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 8:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx.append(float(parts[1]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[4:8]):
+                if v.lower().startswith("active"):
+                    reasons.add(nm)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"],
+                    "samples": 0}
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": max(mx), "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+# ------------------------------------------------------------------ CPU arms
+
+def _oracle_job(args):
+    os.environ.setdefault("OMP_NUM_THREADS", "1")
+    os.environ.setdefault("OPENBLAS_NUM_THREADS", "1")
+    from oracle import narrow_oracle as O
+
+    idx = args
+    pairs, dt, tb = _CPU_PROBLEMS[idx]
+    t0 = time.perf_counter()
+    if len(pairs) == 1 and tb == 0.0:
+        res = O.pair_earliest_contact(pairs[0][0], pairs[0][1], dt)
+    else:
+        from types import SimpleNamespace
+
+        parts, stats, plist = {}, {}, []
+        for a, b in pairs:
+            for x in (a, b):
+                (parts if hasattr(x, "timeline") else stats)[_bid(x)] = x
+            plist.append((_bid(a), _bid(b)))
+        res = O.compute_effective_dt(SimpleNamespace(dt=dt, t_current=tb), parts, stats, plist)
+    rows = res.stats.get("rows", 0) + res.stats.get("zoom_rows", 0) + res.stats.get("bisect_rows", 0)
+    return rows, len(res.raw), time.perf_counter() - t0
+
+
+def _bid(b):
+    return int(b.pid) if hasattr(b, "timeline") else int(b.sid)
+
+
+_CPU_PROBLEMS = []
+
+
+def cpu_sample(problems, n_items: int, workers: int):
+    """Run the oracle over the first n_items problems on `workers` processes."""
+    import multiprocessing as mp
+
+    global _CPU_PROBLEMS
+    _CPU_PROBLEMS = problems
+    idx = list(range(min(n_items, len(problems))))
+    t0 = time.perf_counter()
+    if workers <= 1:
+        out = [_oracle_job(i) for i in idx]
+    else:
+        with mp.get_context("fork").Pool(workers) as pool:
+            out = pool.map(_oracle_job, idx, chunksize=1)
+    wall = time.perf_counter() - t0
+    rows = sum(o[0] for o in out)
+    contacts = sum(o[1] for o in out)
+    return rows, contacts, wall, len(idx)
+
+
+def cpu_cores():
+    try:
+        return len(os.sched_getaffinity(0))
+    except AttributeError:
+        return os.cpu_count() or 1
+
+
+def run_reference(args, rank, world):
+    """--impl reference: the CPU oracle on this host's cores."""
+    if rank != 0:
+        return 0
+    scene = build_scene(args.config, 0, args.pairs)
+    problems = scene_problems(scene)
+    workers = max(1, min(cpu_cores(), args.cpu_workers or cpu_cores()))
+    per_step = max(workers, 1)
+    for _ in range(args.warmup if args.warmup < 1 else 1):
+        cpu_sample(problems, min(per_step, 2), min(workers, 2))
+    rows = contacts = 0
+    wall = 0.0
+    for s in range(args.steps):
+        r, c, w, _ = cpu_sample(problems[s * per_step % max(len(problems), 1):] or problems,
+                                per_step, workers)
+        rows += r
+        contacts += c
+        wall += w
+    value = rows / wall if wall > 0 else 0.0
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": "tests/s",
+        "n_gpus": 0, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": 1e3 * wall / max(args.steps, 1), "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (seeded, BASELINE.json shapes)",
+        "config": {"workload": args.config, "description": CONFIG_DOC[args.config],
+                   "sample_problems_per_step": per_step},
+        "cpu_baseline": {"value": value, "unit": "tests/s", "cores": workers, "kind": "port",
+                         "sample": f"{per_step} {args.config} problems per step x {args.steps} steps"},
+        "e2e": {"value": value, "unit": "tests/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "contacts_per_s": contacts / wall if wall > 0 else 0.0,
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+# ------------------------------------------------------------------ GPU arm
+
+def run_ours(args, rank, world, local_rank):
+    import ctypes as C
+
+    import numpy as np
+    import torch
+
+    from paper_2309_15417_b200 import _lib, ccd, packing
+
+    torch.cuda.set_device(local_rank)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+
+    t_build = time.perf_counter()
+    scene = build_scene(args.config, rank, args.pairs)
+    problems = scene_problems(scene)
+    hs = packing.pack(problems)
+    t_build = time.perf_counter() - t_build
+    ds = ccd.DeviceScene(hs)
+    torch.cuda.synchronize()
+
+    peak_tflops = C.c_double(0.0)
+    peak_ms = C.c_double(0.0)
+    _lib.check(_lib.lib().ltsg_fp64_peak(C.byref(peak_tflops), C.byref(peak_ms),
+                                         C.c_void_p(torch.cuda.current_stream().cuda_stream)),
+               "ltsg_fp64_peak")
+
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")  # > 126 MB L2
+
+    def barrier():
+        torch.cuda.synchronize()
+        if dist is not None:
+            dist.barrier()
+
+    # ---- device-resident steps
+    for _ in range(args.warmup):
+        res = ccd.run_scene(ds)
+    stats = []
+    step_ms = []
+    barrier()
+    with ClockSampler(local_rank) as clocks:
+        for _ in range(args.steps):
+            flush.fill_(1)
+            ev0 = torch.cuda.Event(enable_timing=True)
+            ev1 = torch.cuda.Event(enable_timing=True)
+            ev0.record()
+            res = ccd.run_scene(ds)
+            ev1.record()
+            ev1.synchronize()
+            step_ms.append(ev0.elapsed_time(ev1))
+            stats.append(res.stats)
+        barrier()
+    total_ms = sum(step_ms)
+    tests = sum(s["rows_screen"] + s["rows_zoom"] + s["rows_bisect"] for s in stats)
+    contacts = sum(s["n_raw"] for s in stats)
+    # per-kernel device time of the screen from the library's own events
+    screen_ms = sum(s.get("ms_screen", 0.0) for s in stats)
+    screen_rows = sum(s["rows_screen"] for s in stats)
+    launches = sum(s.get("launches", 0) for s in stats)
+
+    # ---- end to end through the public API from host bodies
+    pairs_obj = [pr[0][0] for pr in problems] if scene.mode == "pair" else None
+    e2e_ms = []
+    h2d = d2h = 0
+    for i in range(args.warmup + args.steps):
+        flush.fill_(1)
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        if scene.mode == "pair":
+            out = ccd.earliest_contacts(pairs_obj, scene.dt)
+        else:
+            out = ccd._run_problems(problems, widen=1e-3)
+        t1 = time.perf_counter()
+        if i >= args.warmup:
+            e2e_ms.append(1e3 * (t1 - t0))
+    h2d = hs.nbytes
+    d2h = sum(v.nbytes for v in out.contacts.values()) + out.dt.nbytes + out.collision.nbytes \
+        + out.first_contact.nbytes + out.fused_offset.nbytes
+
+    # ---- reduce over ranks (max time, sum work)
+    vals = torch.tensor([total_ms, sum(e2e_ms), float(tests), float(contacts)], dtype=torch.float64,
+                        device="cuda")
+    if dist is not None:
+        t_max = vals[:2].clone()
+        dist.all_reduce(t_max, op=dist.ReduceOp.MAX)
+        w_sum = vals[2:].clone()
+        dist.all_reduce(w_sum, op=dist.ReduceOp.SUM)
+        total_ms, e2e_total = float(t_max[0]), float(t_max[1])
+        tests_all, contacts_all = float(w_sum[0]), float(w_sum[1])
+    else:
+        e2e_total = sum(e2e_ms)
+        tests_all, contacts_all = float(tests), float(contacts)
+
+    cpu = None
+    if rank == 0 and not args.no_cpu:
+        workers = max(1, min(cpu_cores(), 64))
+        r, c, w, n = cpu_sample(problems, min(len(problems), 2 * workers), workers)
+        cpu = {"value": r / w if w > 0 else 0.0, "unit": "tests/s", "cores": workers, "kind": "port",
+               "sample": f"{n} {args.config} problems (of {len(problems)}) through the numpy oracle, "
+                         f"{workers} processes, {w:.1f} s wall"}
+
+    if rank == 0:
+        value = tests_all / (total_ms * 1e-3)
+        achieved = screen_rows * FLOPS_PER_TEST / (screen_ms * 1e-3) / 1e12 if screen_ms > 0 else 0.0
+        line = {
+            "metric": METRIC, "value": value, "unit": "tests/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": total_ms / args.steps,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (seeded, BASELINE.json shapes)",
+            "config": {"workload": args.config, "description": CONFIG_DOC[args.config],
+                       "problems_per_gpu": len(problems), "pairs_per_gpu": len(hs.pair_problem),
+                       "triangle_records_per_gpu": int(len(hs.tris)),
+                       "l2": "flushed (256 MiB write) before every timed step",
+                       "parallelism": f"weak: {world} independent shards"},
+            "contacts_per_s": contacts_all / (total_ms * 1e-3),
+            "tests_per_step": tests_all / args.steps,
+            "raw_contacts_per_step": contacts_all / args.steps,
+            "e2e": {"value": tests_all / (e2e_total * 1e-3), "unit": "tests/s",
+                    "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
+                    "ms_per_step": e2e_total / args.steps,
+                    "path": "ccd.earliest_contacts(host bodies) -> pack -> H2D -> ltsg_search -> D2H"},
+            "roofline": {"bound": "fp64", "kernel": "k_screen", "achieved": achieved,
+                         "peak": peak_tflops.value, "unit": "TFLOP/s",
+                         "frac": achieved / peak_tflops.value if peak_tflops.value else None,
+                         "traffic": None,
+                         "peak_source": "in-run DFMA microbenchmark (ltsg_fp64_peak); "
+                                        "MEASURED_PEAKS.json has no FP64 entry",
+                         "flops_per_test": FLOPS_PER_TEST,
+                         "screen_ms_per_step": screen_ms / args.steps},
+            "gpu_launches": launches,
+            "breakdown_ms_per_step": {
+                "screen": screen_ms / args.steps,
+                "refine": sum(s.get("ms_refine", 0.0) for s in stats) / args.steps,
+                "contacts_fusion": sum(s.get("ms_contacts", 0.0) for s in stats) / args.steps,
+                "generations": stats[-1].get("generations"),
+                "candidates": stats[-1].get("candidates")},
+            "clocks": clocks.summary(),
+            "cpu_baseline": cpu,
+            "setup_s": t_build,
+        }
+        print(json.dumps(line), flush=True)
+    if dist is not None:
+        dist.destroy_process_group()
+    return 0
+
+
+def main(argv=None) -> int:
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=("ours", "reference"), default="ours")
+    ap.add_argument("--config", choices=tuple(CONFIG_DOC), default="c1")
+    ap.add_argument("--pairs", type=int, default=None, help="override the workload size")
+    ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
+    ap.add_argument("--cpu-workers", type=int, default=0)
+    args = ap.parse_args(argv)
+    rank, world, local_rank = _env_rank()
+    if args.impl == "reference":
+        return run_reference(args, rank, world)
+    return run_ours(args, rank, world, local_rank)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

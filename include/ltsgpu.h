@@ -1,0 +1,194 @@
+/* ltsgpu -- B200 (sm_100a) narrow phase for the optimistic local-time-stepping
+ * DEM method (arXiv 2309.15417), C ABI.
+ *
+ * The reference (ltsdem) is pure Python/numpy and has no FFI; its "operator
+ * API" for this path is the module `ltsdem.ccd` plus the row kernels in
+ * `ltsdem.kernels`.  Each entry point below replaces one of those functions
+ * (file:line under /root/reference/pkg/src/ltsdem).  The Python host
+ * (`paper_2309_15417_b200/ccd.py`, `kernels.py`) binds them with ctypes and
+ * keeps the reference's call surface; INTEGRATION.md shows the binding.
+ *
+ * Conventions
+ *  - Every pointer argument is DEVICE memory owned by the caller unless the
+ *    name ends in `_host`.  The library never frees caller memory.
+ *  - Every call is ordered on `stream` (a cudaStream_t, NULL = legacy default)
+ *    and re-entrant; all scratch lives in an explicit workspace handle.
+ *  - Arrays of 3-vectors are row-major (n, 3) float64; triangles are
+ *    (n, 3, 3) float64 (corner-major), exactly numpy's C layout.
+ *  - Return value: LTSG_OK or an error code; ltsg_last_error() gives a
+ *    thread-local message.  On LTSG_ECAPACITY the caller grows its output
+ *    buffers (sizes reported in the out struct) and calls again.
+ *  - All arithmetic is IEEE float64 with the reference's rounding order, so
+ *    static (dt = 0) results are bit-identical to the reference.
+ */
+#ifndef LTSGPU_H
+#define LTSGPU_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define LTSG_OK 0
+#define LTSG_EINVAL 1
+#define LTSG_ECUDA 2
+#define LTSG_ECAPACITY 3
+
+const char* ltsg_last_error(void);
+int ltsg_version(void);
+
+/* kernels.point_triangle_closest (kernels.py:23-75): per row, the closest
+ * point on triangle (a, b, c) to p and its distance.  `closest` may be NULL. */
+int ltsg_point_triangle_closest(const double* p, const double* a, const double* b,
+                                const double* c, int64_t n, double* dist, double* closest,
+                                void* stream);
+
+/* kernels.segment_segment_closest (kernels.py:78-115).  c1/c2 may be NULL. */
+int ltsg_segment_segment_closest(const double* p1, const double* q1, const double* p2,
+                                 const double* q2, int64_t n, double* dist, double* c1,
+                                 double* c2, void* stream);
+
+/* ccd._feature_distances (ccd.py:135-153): row-wise 15-feature distance of
+ * triangle pairs tri_a[i], tri_b[i], each (n, 3, 3). */
+int ltsg_feature_distances(const double* tri_a, const double* tri_b, int64_t n, double* dist,
+                           void* stream);
+
+/* ccd._closest_feature (ccd.py:156-174) per row: distance and witness points
+ * pa (on tri_a) and pb (on tri_b), (n, 3) each. */
+int ltsg_closest_feature(const double* tri_a, const double* tri_b, int64_t n, double* dist,
+                         double* pa, double* pb, void* stream);
+
+/* kernels.triangle_overlap_centroid (kernels.py:138-201) per row; has[i] = 0
+ * where the reference returns None. */
+int ltsg_overlap_centroid(const double* tri_a, const double* tri_b, const double* normal,
+                          int64_t n, double* centroid, int32_t* has, void* stream);
+
+/* ---------------------------------------------------------------- search
+ *
+ * One call runs ccd._search (ccd.py:373-487) for a batch of independent
+ * problems: a problem is one `pair_earliest_contact` call (one body pair,
+ * ccd.py:490-502) or one `compute_effective_dt` cluster (several pairs
+ * sharing one bound, ccd.py:505-524).  It also builds the contact records
+ * (_make_contact, ccd.py:183-213) and fuses them (filter_contacts,
+ * ccd.py:527-577).
+ *
+ * Packed scene (device, built by the host packer):
+ *  tris       n_tris x 12 float64 triangle records: 9 body-frame corners,
+ *             epsilon, arm (max corner norm), and (int32 first child,
+ *             int32 child count) packed into the 12th slot.  Each tree level
+ *             is stored so that a parent's children form a contiguous range
+ *             of the next finer level.
+ *  tri_orig   n_tris int32: the triangle's index in the reference tree level
+ *             (reported as tri_a / tri_b).
+ *  body_state n_bodies x 16 float64: position[3], velocity[3], rotation
+ *             quaternion [w,x,y,z], angular_velocity[3], static flag, 2 pad.
+ *  body_levels n_bodies x 18 int64: n_levels, id, then 8 level record
+ *             offsets and 8 level sizes.
+ *  pair_body  n_pairs x 2 int32 body slots; pair_problem n_pairs int32;
+ *  pair_group n_pairs int32: rank of (body_a id, body_b id) among the distinct
+ *             id pairs of the pair's problem (fusion groups, ccd.py:535-539).
+ *  problem_dt / problem_tbase  n_problems float64.
+ */
+typedef struct {
+  const double* tris;
+  const int32_t* tri_orig;
+  int64_t n_tris;
+  const double* body_state;
+  const int64_t* body_levels;
+  int32_t n_bodies;
+  int32_t n_problems;
+  const int32_t* pair_body;
+  const int32_t* pair_problem;
+  const int32_t* pair_group;
+  int64_t n_pairs;
+  const double* problem_dt;
+  const double* problem_tbase;
+  double widen;
+  int32_t exhaustive;
+  int32_t max_children;  /* max children per surrogate triangle (fanout) */
+} ltsg_scene;
+
+/* Per-problem results and the contact lists (device buffers, caller-owned).
+ * Contacts are SoA; `fused_*` are the filter_contacts output grouped by
+ * problem (problem p's fused contacts are [fused_offset[p], fused_offset[p+1]));
+ * `raw_*` (optional, may be NULL) are the pre-fusion records. */
+typedef struct {
+  double* dt;             /* n_problems */
+  double* first_contact;  /* n_problems; valid where collision */
+  int32_t* collision;     /* n_problems */
+  int64_t* fused_offset;  /* n_problems + 1 */
+  int64_t capacity;       /* contact capacity of each list below */
+  int32_t* body_a;
+  int32_t* body_b;
+  double* position;       /* (capacity, 3) */
+  double* normal;         /* (capacity, 3) */
+  double* depth;
+  double* t;
+  int32_t* tri_a;
+  int32_t* tri_b;
+  double* threshold;
+  int32_t* problem;       /* problem of each fused contact */
+  /* optional raw (pre-fusion) records */
+  int32_t* raw_problem;
+  int32_t* raw_body_a;
+  int32_t* raw_body_b;
+  double* raw_position;
+  double* raw_normal;
+  double* raw_depth;
+  double* raw_t;
+  int32_t* raw_tri_a;
+  int32_t* raw_tri_b;
+  double* raw_threshold;
+  /* filled by the call (host-visible scalars) */
+  int64_t n_fused;
+  int64_t n_raw;
+  int64_t rows_screen;    /* 15-feature rows of the multiscale screen (= reference) */
+  int64_t rows_zoom;      /* zoom rows the reference would evaluate */
+  int64_t rows_bisect;    /* bisection rows */
+  int64_t rows_executed;  /* rows actually evaluated on the device */
+  int64_t candidates;     /* candidates screened over all levels */
+  int32_t generations;
+  int32_t launches;       /* kernels launched by the call */
+  double ms_screen;       /* device time of the screen kernels (CUDA events) */
+  double ms_refine;       /* zoom + bisection */
+  double ms_contacts;     /* records, contacts, fusion */
+} ltsg_result;
+
+typedef struct ltsg_workspace ltsg_workspace;
+
+/* Scratch owner for ltsg_search: grows on demand, reused across calls.  One
+ * workspace per concurrent stream.  `budget_bytes` caps its device memory
+ * (0 = 75% of free memory at creation). */
+ltsg_workspace* ltsg_workspace_create(int64_t budget_bytes);
+void ltsg_workspace_destroy(ltsg_workspace* ws);
+int64_t ltsg_workspace_bytes(const ltsg_workspace* ws);
+
+/* Run the batched search.  Blocks the calling thread until `stream` has
+ * finished the call (the traversal reads frontier sizes back each level). */
+int ltsg_search(const ltsg_scene* scene, ltsg_result* out, ltsg_workspace* ws, void* stream);
+
+/* ccd.filter_contacts (ccd.py:527-577) on caller-provided raw contacts: the
+ * raw_* arrays of `io` (n_raw entries) are the input, group_key[i] =
+ * (problem << 32) | rank of (body_a, body_b) within the problem; the fused
+ * outputs and fused_offset of `io` are written.  On entry io->n_raw must hold
+ * the number of problems. */
+int ltsg_fuse_contacts(ltsg_result* io, int64_t n_raw, const uint64_t* group_key,
+                       ltsg_workspace* ws, void* stream);
+
+/* Time one launch of the screen kernel over an implicit all-pairs frontier
+ * of `n_pairs` pairs (exhaustive fine x fine, every candidate one sample at
+ * tau = 0) -- the roofline microbenchmark of the 15-feature distance.
+ * Returns the number of rows evaluated in *rows and the contacts in *hits. */
+int ltsg_exhaustive_rows(const ltsg_scene* scene, int64_t* rows, int64_t* hits,
+                         ltsg_workspace* ws, void* stream);
+
+/* FP64 pipe microbenchmark: independent DFMA chains on every SM; reports
+ * the achieved FP64 FLOP/s (2 per DFMA) -- the roofline denominator. */
+int ltsg_fp64_peak(double* tflops, double* ms, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif

@@ -1,0 +1,369 @@
+"""Drop-in for `ltsdem.ccd` backed by the B200 narrow phase.
+
+Same names, arguments, result types and semantics as the reference module
+(/root/reference/pkg/src/ltsdem/ccd.py):
+
+* `pair_earliest_contact(body_a, body_b, dt, *, widen, exhaustive)`  ccd.py:490-502
+* `compute_effective_dt(cluster, particles, statics, pairs, *, widen)` ccd.py:505-524
+* `filter_contacts(contacts)`                                        ccd.py:527-577
+* `ContactPoint`, `NarrowResult`                                     ccd.py:43-79
+* `_feature_distances(tri_a, tri_b)`                                  ccd.py:135-153
+
+plus batched forms that a sweep driver uses to put many problems on the GPU
+in one call (`earliest_contacts`, `effective_dts`).  Every call runs the
+hand-written sm_100a kernels of libltsgpu.so through its C ABI; there is no
+CPU path, and a missing library or device raises.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from . import _lib
+from . import packing
+
+_WIDEN = 1e-3
+
+
+@dataclass
+class ContactPoint:
+    """A touching point between two halo surfaces (ccd.py:43-61).
+
+    `normal` points from body_b toward body_a; `depth` is how far inside
+    the touching threshold the pair sits at time `t`."""
+
+    body_a: int
+    body_b: int
+    position: np.ndarray
+    normal: np.ndarray
+    depth: float
+    t: float
+    tri_a: int = -1
+    tri_b: int = -1
+    threshold: float = 0.0
+
+
+@dataclass
+class NarrowResult:
+    """Outcome of one earliest-contact search (ccd.py:64-79)."""
+
+    dt: float
+    contacts: list
+    narrowing_iters: int
+    bound_history: list
+    collision: bool
+    first_contact: float | None = None
+
+
+_CONTACT_FIELDS = (
+    ("body_a", np.int32, ()), ("body_b", np.int32, ()), ("position", np.float64, (3,)),
+    ("normal", np.float64, (3,)), ("depth", np.float64, ()), ("t", np.float64, ()),
+    ("tri_a", np.int32, ()), ("tri_b", np.int32, ()), ("threshold", np.float64, ()),
+    ("problem", np.int32, ()),
+)
+
+
+@dataclass
+class BatchResult:
+    """Results of a batched call, as arrays (problem p's fused contacts are
+    rows fused_offset[p]:fused_offset[p+1] of `contacts`)."""
+
+    dt: np.ndarray
+    collision: np.ndarray
+    first_contact: np.ndarray
+    fused_offset: np.ndarray
+    contacts: dict
+    raw: dict | None
+    stats: dict = field(default_factory=dict)
+
+    def __len__(self):
+        return len(self.dt)
+
+    def result(self, p: int) -> NarrowResult:
+        coll = bool(self.collision[p])
+        first = float(self.first_contact[p]) if coll else None
+        lo, hi = int(self.fused_offset[p]), int(self.fused_offset[p + 1])
+        return NarrowResult(
+            dt=float(self.dt[p]), contacts=_contacts(self.contacts, lo, hi),
+            narrowing_iters=1 if coll else 0, bound_history=[first] if coll else [],
+            collision=coll, first_contact=first)
+
+    def results(self) -> list:
+        return [self.result(p) for p in range(len(self))]
+
+    def raw_contacts(self, p: int | None = None) -> list:
+        if self.raw is None:
+            raise ValueError("raw contacts were not requested")
+        n = len(self.raw["t"])
+        if p is None:
+            return _contacts(self.raw, 0, n)
+        sel = np.flatnonzero(self.raw["problem"] == p)
+        if len(sel) == 0:
+            return []
+        return _contacts(self.raw, int(sel[0]), int(sel[-1]) + 1)
+
+
+def _contacts(soa, lo, hi) -> list:
+    out = []
+    for i in range(lo, hi):
+        out.append(ContactPoint(
+            body_a=int(soa["body_a"][i]), body_b=int(soa["body_b"][i]),
+            position=soa["position"][i].copy(), normal=soa["normal"][i].copy(),
+            depth=float(soa["depth"][i]), t=float(soa["t"][i]),
+            tri_a=int(soa["tri_a"][i]), tri_b=int(soa["tri_b"][i]),
+            threshold=float(soa["threshold"][i])))
+    return out
+
+
+def _ptr(t) -> int:
+    return t.data_ptr() if t is not None and t.numel() > 0 else 0
+
+
+class DeviceScene:
+    """A packed scene resident in HBM (torch tensors as plain device buffers)."""
+
+    def __init__(self, hs: packing.HostScene, device=None, non_blocking: bool = True):
+        torch = _lib.require_cuda()
+        dev = torch.device("cuda", torch.cuda.current_device()) if device is None else device
+        self.host = hs
+        self.t = {}
+        for k, v in hs.arrays().items():
+            src = torch.from_numpy(np.ascontiguousarray(v))
+            self.t[k] = src.to(dev, non_blocking=non_blocking)
+        self.device = dev
+
+    def struct(self, widen: float, exhaustive: bool) -> _lib.Scene:
+        t = self.t
+        hs = self.host
+        return _lib.Scene(
+            tris=_ptr(t["tris"]), tri_orig=_ptr(t["tri_orig"]), n_tris=len(hs.tris),
+            body_state=_ptr(t["body_state"]), body_levels=_ptr(t["body_levels"]),
+            n_bodies=len(hs.body_state), n_problems=hs.n_problems,
+            pair_body=_ptr(t["pair_body"]), pair_problem=_ptr(t["pair_problem"]),
+            pair_group=_ptr(t["pair_group"]), n_pairs=len(hs.pair_problem),
+            problem_dt=_ptr(t["problem_dt"]), problem_tbase=_ptr(t["problem_tbase"]),
+            widen=float(widen), exhaustive=1 if exhaustive else 0,
+            max_children=int(hs.max_children))
+
+
+class DeviceResult:
+    """Caller-owned output buffers of ltsg_search."""
+
+    def __init__(self, n_problems: int, capacity: int, device, raw: bool):
+        import torch
+
+        self.capacity = int(max(capacity, 1))
+        self.n_problems = n_problems
+        self.f = {}
+        self.r = {}
+        self.dt = torch.empty(max(n_problems, 1), dtype=torch.float64, device=device)
+        self.first = torch.empty(max(n_problems, 1), dtype=torch.float64, device=device)
+        self.coll = torch.empty(max(n_problems, 1), dtype=torch.int32, device=device)
+        self.off = torch.empty(n_problems + 1, dtype=torch.int64, device=device)
+        tdt = {np.int32: torch.int32, np.float64: torch.float64}
+        for name, dt, shape in _CONTACT_FIELDS:
+            self.f[name] = torch.empty((self.capacity, *shape), dtype=tdt[dt], device=device)
+            if raw:
+                self.r[name] = torch.empty((self.capacity, *shape), dtype=tdt[dt], device=device)
+
+    def struct(self) -> _lib.Result:
+        f, r = self.f, self.r
+        res = _lib.Result(
+            dt=_ptr(self.dt), first_contact=_ptr(self.first), collision=_ptr(self.coll),
+            fused_offset=_ptr(self.off), capacity=self.capacity,
+            body_a=_ptr(f["body_a"]), body_b=_ptr(f["body_b"]), position=_ptr(f["position"]),
+            normal=_ptr(f["normal"]), depth=_ptr(f["depth"]), t=_ptr(f["t"]),
+            tri_a=_ptr(f["tri_a"]), tri_b=_ptr(f["tri_b"]), threshold=_ptr(f["threshold"]),
+            problem=_ptr(f["problem"]))
+        if r:
+            res.raw_problem = _ptr(r["problem"])
+            res.raw_body_a = _ptr(r["body_a"])
+            res.raw_body_b = _ptr(r["body_b"])
+            res.raw_position = _ptr(r["position"])
+            res.raw_normal = _ptr(r["normal"])
+            res.raw_depth = _ptr(r["depth"])
+            res.raw_t = _ptr(r["t"])
+            res.raw_tri_a = _ptr(r["tri_a"])
+            res.raw_tri_b = _ptr(r["tri_b"])
+            res.raw_threshold = _ptr(r["threshold"])
+        return res
+
+    def to_host(self, st: _lib.Result) -> BatchResult:
+        n = self.n_problems
+        nf, nr = int(st.n_fused), int(st.n_raw)
+        fused = {k: v[:nf].cpu().numpy() for k, v in self.f.items()}
+        raw = {k: v[:nr].cpu().numpy() for k, v in self.r.items()} if self.r else None
+        stats = {k: int(getattr(st, k)) for k in (
+            "rows_screen", "rows_zoom", "rows_bisect", "rows_executed", "candidates",
+            "generations", "n_raw", "n_fused", "launches")}
+        stats.update({k: float(getattr(st, k)) for k in ("ms_screen", "ms_refine", "ms_contacts")})
+        return BatchResult(dt=self.dt[:n].cpu().numpy(), collision=self.coll[:n].cpu().numpy() != 0,
+                           first_contact=self.first[:n].cpu().numpy(),
+                           fused_offset=self.off.cpu().numpy(), contacts=fused, raw=raw, stats=stats)
+
+
+_capacity_hint = [1 << 12]
+
+
+def run_scene(ds: DeviceScene, *, widen: float = _WIDEN, exhaustive: bool = False,
+              raw: bool = False, workspace=None, stream=None) -> BatchResult:
+    """ltsg_search on a device-resident scene; returns host arrays."""
+    torch = _lib.require_cuda()
+    ws = workspace or _lib.workspace()
+    st = stream if stream is not None else torch.cuda.current_stream()
+    scene = ds.struct(widen, exhaustive)
+    cap = _capacity_hint[0]
+    while True:
+        out = DeviceResult(ds.host.n_problems, cap, ds.device, raw)
+        res = out.struct()
+        rc = _lib.lib().ltsg_search(C.byref(scene), C.byref(res), ws.handle, C.c_void_p(st.cuda_stream))
+        if rc == _lib.LTSG_ECAPACITY and res.n_fused > out.capacity:
+            cap = int(res.n_fused * 1.25) + 16
+            _capacity_hint[0] = max(_capacity_hint[0], cap)
+            continue
+        _lib.check(rc, "ltsg_search")
+        return out.to_host(res)
+
+
+def _run_problems(problems, *, widen, exhaustive=False, raw=False) -> BatchResult:
+    hs = packing.pack(problems)
+    try:
+        return run_scene(DeviceScene(hs), widen=widen, exhaustive=exhaustive, raw=raw)
+    except _lib.CapacityError:
+        if len(problems) <= 1:
+            raise
+        half = len(problems) // 2
+        a = _run_problems(problems[:half], widen=widen, exhaustive=exhaustive, raw=raw)
+        b = _run_problems(problems[half:], widen=widen, exhaustive=exhaustive, raw=raw)
+        return _concat(a, b)
+
+
+def _concat(a: BatchResult, b: BatchResult) -> BatchResult:
+    na = len(a)
+    contacts = {k: np.concatenate([a.contacts[k], b.contacts[k]]) for k in a.contacts}
+    contacts["problem"] = np.concatenate([a.contacts["problem"], b.contacts["problem"] + na])
+    raw = None
+    if a.raw is not None:
+        raw = {k: np.concatenate([a.raw[k], b.raw[k]]) for k in a.raw}
+        raw["problem"] = np.concatenate([a.raw["problem"], b.raw["problem"] + na])
+    return BatchResult(
+        dt=np.concatenate([a.dt, b.dt]), collision=np.concatenate([a.collision, b.collision]),
+        first_contact=np.concatenate([a.first_contact, b.first_contact]),
+        fused_offset=np.concatenate([a.fused_offset[:-1], b.fused_offset + a.fused_offset[-1]]),
+        contacts=contacts, raw=raw,
+        stats={k: a.stats.get(k, 0) + b.stats.get(k, 0) for k in a.stats})
+
+
+def _bid(body) -> int:
+    return packing.body_id(body)
+
+
+def _pair_problem(body_a, body_b, dt):
+    # the reference keys motions by body id (ccd.py:501): equal ids collapse to body_b
+    motions = {_bid(body_a): body_a, _bid(body_b): body_b}
+    return ([(motions[_bid(body_a)], motions[_bid(body_b)])], float(dt), 0.0)
+
+
+def _cluster_problem(cluster, particles, statics, pairs):
+    motions = {}
+    obj_pairs = []
+    for a, b in pairs:
+        for bid in (a, b):
+            if bid not in motions:
+                motions[bid] = particles[bid] if bid >= 0 else statics[bid]
+        obj_pairs.append((motions[a], motions[b]))
+    return (obj_pairs, float(cluster.dt), float(cluster.t_current))
+
+
+# ------------------------------------------------------------------ public API
+
+def pair_earliest_contact(body_a, body_b, dt: float, *, widen: float = _WIDEN,
+                          exhaustive: bool = False) -> NarrowResult:
+    """Earliest-contact search for one body pair over [0, dt] (ccd.py:490-502)."""
+    return _run_problems([_pair_problem(body_a, body_b, dt)], widen=widen,
+                         exhaustive=exhaustive).result(0)
+
+
+def compute_effective_dt(cluster, particles, statics, pairs, *,
+                         widen: float = _WIDEN) -> NarrowResult:
+    """Size one cluster's step against its contact pairs (ccd.py:505-524)."""
+    pairs = list(pairs)
+    if not pairs:
+        return NarrowResult(dt=cluster.dt, contacts=[], narrowing_iters=0, bound_history=[],
+                            collision=False)
+    return _run_problems([_cluster_problem(cluster, particles, statics, pairs)],
+                         widen=widen).result(0)
+
+
+def earliest_contacts(pairs, dt, *, widen: float = _WIDEN, exhaustive: bool = False,
+                      raw: bool = False) -> BatchResult:
+    """Batched `pair_earliest_contact` over many independent body pairs."""
+    pairs = list(pairs)
+    dts = np.broadcast_to(np.asarray(dt, dtype=np.float64), (len(pairs),))
+    return _run_problems([_pair_problem(a, b, d) for (a, b), d in zip(pairs, dts)],
+                         widen=widen, exhaustive=exhaustive, raw=raw)
+
+
+def effective_dts(clusters, particles, statics, pairs_per_cluster, *, widen: float = _WIDEN,
+                  raw: bool = False):
+    """Batched `compute_effective_dt` over the clusters of one sweep.  Clusters
+    without pairs keep their own dt (ccd.py:515-517) and launch nothing."""
+    clusters = list(clusters)
+    pairs_per_cluster = [list(p) for p in pairs_per_cluster]
+    live = [i for i, p in enumerate(pairs_per_cluster) if p]
+    out = [None] * len(clusters)
+    batch = None
+    if live:
+        batch = _run_problems([_cluster_problem(clusters[i], particles, statics, pairs_per_cluster[i])
+                               for i in live], widen=widen, raw=raw)
+        for j, i in enumerate(live):
+            out[i] = batch.result(j)
+    for i, c in enumerate(clusters):
+        if out[i] is None:
+            out[i] = NarrowResult(dt=c.dt, contacts=[], narrowing_iters=0, bound_history=[],
+                                  collision=False)
+    return out, batch
+
+
+def filter_contacts(contacts) -> list:
+    """Fuse near-coincident points per body pair, canonically (ccd.py:527-577)."""
+    contacts = list(contacts)
+    if not contacts:
+        return []
+    torch = _lib.require_cuda()
+    n = len(contacts)
+    ids = [(int(c.body_a), int(c.body_b)) for c in contacts]
+    rank = {u: r for r, u in enumerate(sorted(set(ids)))}
+    dev = torch.device("cuda", torch.cuda.current_device())
+    out = DeviceResult(1, n, dev, raw=True)
+    host = {
+        "body_a": np.array([c.body_a for c in contacts], dtype=np.int32),
+        "body_b": np.array([c.body_b for c in contacts], dtype=np.int32),
+        "position": np.array([np.asarray(c.position, dtype=np.float64) for c in contacts]).reshape(n, 3),
+        "normal": np.array([np.asarray(c.normal, dtype=np.float64) for c in contacts]).reshape(n, 3),
+        "depth": np.array([c.depth for c in contacts], dtype=np.float64),
+        "t": np.array([c.t for c in contacts], dtype=np.float64),
+        "tri_a": np.array([c.tri_a for c in contacts], dtype=np.int32),
+        "tri_b": np.array([c.tri_b for c in contacts], dtype=np.int32),
+        "threshold": np.array([c.threshold for c in contacts], dtype=np.float64),
+        "problem": np.zeros(n, dtype=np.int32),
+    }
+    for k, v in host.items():
+        out.r[k].copy_(torch.from_numpy(v))
+    keys = torch.from_numpy(np.array([rank[i] for i in ids], dtype=np.uint64).view(np.int64)).to(dev)
+    res = out.struct()
+    res.n_raw = 1  # number of problems on entry
+    st = torch.cuda.current_stream()
+    rc = _lib.lib().ltsg_fuse_contacts(C.byref(res), n, C.c_void_p(keys.data_ptr()),
+                                       _lib.workspace().handle, C.c_void_p(st.cuda_stream))
+    _lib.check(rc, "ltsg_fuse_contacts")
+    return out.to_host(res).result(0).contacts
+
+
+def _feature_distances(tri_a, tri_b) -> np.ndarray:
+    """Row-wise 15-feature triangle-pair distance (ccd.py:135-153)."""
+    from .kernels import feature_distances
+    return feature_distances(tri_a, tri_b)

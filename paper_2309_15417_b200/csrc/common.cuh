@@ -1,0 +1,63 @@
+// Error reporting and the growable device workspace shared by the ABI files.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdarg>
+#include <cstdint>
+#include <cstdio>
+#include <string>
+#include <unordered_map>
+
+#include "../../include/ltsgpu.h"
+
+namespace ltsg {
+
+void set_error(const char* fmt, ...);
+
+struct Status {
+  int code = LTSG_OK;
+};
+
+#define LTSG_CUDA(expr)                                                                     \
+  do {                                                                                      \
+    cudaError_t err_ = (expr);                                                              \
+    if (err_ != cudaSuccess) {                                                              \
+      ::ltsg::set_error("%s:%d %s: %s", __FILE__, __LINE__, #expr, cudaGetErrorString(err_)); \
+      return LTSG_ECUDA;                                                                    \
+    }                                                                                       \
+  } while (0)
+
+#define LTSG_CHECK_LAUNCH() LTSG_CUDA(cudaGetLastError())
+
+#define LTSG_TRY(expr)          \
+  do {                          \
+    int rc_ = (expr);           \
+    if (rc_ != LTSG_OK) return rc_; \
+  } while (0)
+
+inline int grid_for(int64_t n, int block) {
+  int64_t g = (n + block - 1) / block;
+  if (g < 1) g = 1;
+  if (g > 2147483647LL) g = 2147483647LL;
+  return (int)g;
+}
+
+}  // namespace ltsg
+
+// Named growable buffers.  Growing frees the old buffer (cudaFree
+// synchronises), so callers only grow between kernels whose inputs they do
+// not need to keep.
+struct ltsg_workspace {
+  struct Buf {
+    void* ptr = nullptr;
+    size_t bytes = 0;
+  };
+  std::unordered_map<std::string, Buf> bufs;
+  size_t total = 0;
+  size_t budget = 0;
+  int device = 0;
+
+  int get(const char* name, size_t bytes, void** out, bool keep = false);
+  ~ltsg_workspace();
+};

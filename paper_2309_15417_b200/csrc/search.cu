@@ -1,0 +1,1525 @@
+// Batched multiscale earliest-contact search: ccd._search (ccd.py:373-487)
+// over many independent problems in one pass, plus contact records
+// (ccd.py:183-213) and fusion (ccd.py:527-577).
+//
+// Schedule.  In the reference the fine (0,0) bucket is processed last and
+// exactly once (bucket key max(la,lb) strictly decreases from parent to
+// child, ccd.py:394 / 418-427), so the shared bound equals dt for the whole
+// coarse traversal and the prune filters at ccd.py:396-397 / 448-449 never
+// fire.  Every candidate is therefore screened over [w0, dt] independently
+// of every other, and the traversal is an order-free frontier expansion.
+// We run it level-synchronously over all problems at once ("generations"):
+// the screen kernel evaluates every candidate of the frontier, expands the
+// flagged coarse ones into the next frontier and turns fine ones into
+// resting records, defensive crossings and refinement entries.  Zoom and
+// bisection then run per entry; the bound of a problem is the minimum
+// bisected tau (ccd.py:459-468), which is exactly what the reference's
+// sorted narrowing loop produces.
+#include "common.cuh"
+#include "geom.cuh"
+#include "dist_staged.cuh"
+
+#include <cub/cub.cuh>
+
+#include <algorithm>
+#include <vector>
+
+namespace ltsg {
+
+constexpr int kMaxLevels = 8;
+constexpr int kRecord = 12;  // doubles per triangle record
+
+struct BodyInfo {
+  Motion m;
+  int64_t level_off[kMaxLevels];
+  int32_t level_size[kMaxLevels];
+  int32_t n_levels;
+  int32_t id;
+};
+
+struct PairInfo {
+  int32_t ba, bb, problem, group;
+  double speed0;  // |v_a - v_b| (ddot norm)
+  double dt;
+};
+
+struct Cand {
+  int32_t pair;
+  int32_t ia;  // level-local record index (children contiguous)
+  int32_t ib;
+  int16_t la, lb;
+  double w0;
+};
+static_assert(sizeof(Cand) == 24, "Cand layout");
+
+struct RestRec {
+  int32_t pair, ia, ib, pad;
+  double h;
+};
+struct Entry {
+  int32_t pair, ia, ib, pad;
+  double lo, hi, h, speed;
+};
+struct Cross {
+  int32_t pair, ia, ib, pad;
+  double tau, h;
+};
+struct Bracket {
+  int32_t pair, ia, ib, pad;
+  double lo, hi, h;
+};
+
+struct Counters {
+  unsigned long long next;       // next-frontier size
+  unsigned long long resting;
+  unsigned long long entries;
+  unsigned long long cross;
+  unsigned long long rows;       // screen rows (reference-equivalent)
+  unsigned long long brackets;
+  unsigned long long zoom_rows;  // rows the reference would evaluate
+  unsigned long long zoom_exec;  // rows evaluated here
+  unsigned long long bisect_rows;
+  unsigned long long records;
+  unsigned long long overflow;   // zoom queue overflow flag
+};
+
+// ---------------------------------------------------------------- prep
+
+__global__ void k_prep_bodies(const double* state, const int64_t* levels, int n, BodyInfo* out) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const double* s = state + 16 * i;
+  const int64_t* L = levels + 18 * i;
+  BodyInfo b;
+  b.n_levels = (int32_t)L[0];
+  b.id = (int32_t)L[1];
+  for (int l = 0; l < kMaxLevels; ++l) {
+    b.level_off[l] = L[2 + l];
+    b.level_size[l] = (int32_t)L[10 + l];
+  }
+  Motion& m = b.m;
+  const bool is_static = s[13] != 0.0;
+  if (is_static) {  // ccd.py:106: zero motion, identity pose
+    for (int k = 0; k < 3; ++k) m.x0[k] = m.v[k] = 0.0;
+    for (int k = 0; k < 9; ++k) m.base[k] = (k % 4 == 0) ? 1.0 : 0.0;
+    m.omega = 0.0;
+    m.spinning = 0;
+  } else {
+    for (int k = 0; k < 3; ++k) {
+      m.x0[k] = s[k];
+      m.v[k] = s[3 + k];
+    }
+    const double w = s[6], x = s[7], y = s[8], z = s[9];  // quaternions.to_matrix
+    m.base[0] = sub(1.0, mul(2.0, add(mul(y, y), mul(z, z))));
+    m.base[1] = mul(2.0, sub(mul(x, y), mul(w, z)));
+    m.base[2] = mul(2.0, add(mul(x, z), mul(w, y)));
+    m.base[3] = mul(2.0, add(mul(x, y), mul(w, z)));
+    m.base[4] = sub(1.0, mul(2.0, add(mul(x, x), mul(z, z))));
+    m.base[5] = mul(2.0, sub(mul(y, z), mul(w, x)));
+    m.base[6] = mul(2.0, sub(mul(x, z), mul(w, y)));
+    m.base[7] = mul(2.0, add(mul(y, z), mul(w, x)));
+    m.base[8] = sub(1.0, mul(2.0, add(mul(x, x), mul(y, y))));
+    const V3 om{s[10], s[11], s[12]};
+    m.omega = norm_blas(om);
+    m.spinning = m.omega > 0.0;
+  }
+  for (int k = 0; k < 9; ++k) m.K[k] = m.KK[k] = 0.0;
+  if (m.spinning) {
+    const double k0 = dv(s[10], m.omega), k1 = dv(s[11], m.omega), k2 = dv(s[12], m.omega);
+    const double K[9] = {0.0, -k2, k1, k2, 0.0, -k0, -k1, k0, 0.0};
+    for (int r = 0; r < 3; ++r)
+      for (int c = 0; c < 3; ++c) {
+        m.K[3 * r + c] = K[3 * r + c];
+        m.KK[3 * r + c] = fma_(K[3 * r + 2], K[6 + c], fma_(K[3 * r + 1], K[3 + c], mul(K[3 * r], K[c])));
+      }
+  }
+  m.pad = 0;
+  out[i] = b;
+}
+
+__global__ void k_prep_pairs(const int32_t* pair_body, const int32_t* pair_problem,
+                             const int32_t* pair_group, int64_t n, const BodyInfo* bodies,
+                             const double* problem_dt, PairInfo* out) {
+  const int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (k >= n) return;
+  PairInfo p;
+  p.ba = pair_body[2 * k];
+  p.bb = pair_body[2 * k + 1];
+  p.problem = pair_problem[k];
+  p.group = pair_group[k];
+  const Motion& a = bodies[p.ba].m;
+  const Motion& b = bodies[p.bb].m;
+  p.speed0 = norm_blas(V3{sub(a.v[0], b.v[0]), sub(a.v[1], b.v[1]), sub(a.v[2], b.v[2])});
+  p.dt = problem_dt[p.problem];
+  out[k] = p;
+}
+
+// ---------------------------------------------------------------- seeds
+
+__device__ __forceinline__ void seed_levels(const PairInfo& p, const BodyInfo* bodies, int exhaustive,
+                                            int* la, int* lb, int64_t* na, int64_t* nb) {
+  const BodyInfo& A = bodies[p.ba];
+  const BodyInfo& B = bodies[p.bb];
+  *la = exhaustive ? 0 : A.n_levels - 1;
+  *lb = exhaustive ? 0 : B.n_levels - 1;
+  *na = A.level_size[*la];
+  *nb = B.level_size[*lb];
+}
+
+__global__ void k_seed_count(const PairInfo* pairs, int64_t n, const BodyInfo* bodies, int exhaustive,
+                             int64_t* count) {
+  const int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (k >= n) return;
+  int la, lb;
+  int64_t na, nb;
+  seed_levels(pairs[k], bodies, exhaustive, &la, &lb, &na, &nb);
+  count[k] = na * nb;
+}
+
+__global__ void k_seed_fill(const PairInfo* pairs, int64_t n, const BodyInfo* bodies, int exhaustive,
+                            const int64_t* offset, Cand* out) {
+  for (int64_t k = blockIdx.x; k < n; k += gridDim.x) {
+    int la, lb;
+    int64_t na, nb;
+    seed_levels(pairs[k], bodies, exhaustive, &la, &lb, &na, &nb);
+    const int64_t base = offset[k];
+    for (int64_t j = threadIdx.x; j < na * nb; j += blockDim.x) {
+      Cand c;
+      c.pair = (int32_t)k;
+      c.ia = (int32_t)(j / nb);
+      c.ib = (int32_t)(j % nb);
+      c.la = (int16_t)la;
+      c.lb = (int16_t)lb;
+      c.w0 = 0.0;
+      out[base + j] = c;
+    }
+  }
+}
+
+// ---------------------------------------------------------------- rows
+
+__device__ __forceinline__ const double* rec(const double* tris, const BodyInfo& b, int level, int idx) {
+  return tris + (size_t)(b.level_off[level] + idx) * kRecord;
+}
+
+__device__ __forceinline__ void load_local(const double* r, double L[9]) {
+  const double2* q = reinterpret_cast<const double2*>(r);
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    const double2 t = __ldg(q + k);
+    L[2 * k] = t.x;
+    L[2 * k + 1] = t.y;
+  }
+  L[8] = __ldg(r + 8);
+}
+
+// World triangle of body record `r` at time tau.
+__device__ __forceinline__ Tri world_at(const Motion& m, const double* r, double tau) {
+  double L[9], R[9], pos[3];
+  load_local(r, L);
+  rotation_at(m, tau, R);
+  position_at(m, tau, pos);
+  return world_tri(R, pos, L);
+}
+
+__device__ __forceinline__ double row_distance(const Staged& st, const double* tris, const BodyInfo& A,
+                                               const BodyInfo& B, int la, int ia, int lb, int ib,
+                                               double tau) {
+  stage_pair(st, world_at(A.m, rec(tris, A, la, ia), tau), world_at(B.m, rec(tris, B, lb, ib), tau));
+  return __dsqrt_rn(staged_dist_sq(st));
+}
+
+// ---------------------------------------------------------------- screen
+
+struct CandInfo {
+  double w0, dt, h, speed, thr;
+  int32_t pair, ia, ib, la, lb, count, first, pad;
+};
+
+struct ChildInfo {
+  double w0;
+  int32_t first, count, pair, ia0, ib0, nb, la, lb;
+};
+
+struct ScreenOut {
+  Cand* next;
+  unsigned long long next_cap;
+  RestRec* resting;
+  unsigned long long rest_cap;
+  Entry* entries;
+  unsigned long long entry_cap;
+  Cross* cross;
+  unsigned long long cross_cap;
+  Counters* ctr;
+};
+
+constexpr int kScreenWarps = 2;
+constexpr int kRowsPerWarp = 32 * kMaxSamples;
+
+__device__ __forceinline__ int sample_count(double span, double speed, double h) {
+  // ccd.py:347-352
+  if (span == 0.0) return 1;
+  if (speed == 0.0) return kMinSamples;
+  const double q = ceil(dv(mul(span, speed), mul(0.5, h)));
+  long long need;
+  if (!(q < 9.2233720368547758e18))  // numpy astype(int) of nan / out of range -> INT64_MIN
+    need = (long long)0x8000000000000000ULL;
+  else
+    need = (long long)q;
+  need += 1;
+  if (need < kMinSamples) need = kMinSamples;
+  if (need > kMaxSamples) need = kMaxSamples;
+  return (int)need;
+}
+
+__device__ __forceinline__ int warp_incl_scan(int v, int lane) {
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int t = __shfl_up_sync(0xffffffffu, v, o);
+    if (lane >= o) v += t;
+  }
+  return v;
+}
+
+// Screen one frontier (one generation): every candidate is sampled over
+// [w0, dt] (ccd.py:321-370) and decided (ccd.py:404-446).  A warp owns 32
+// consecutive candidates; their 1..33 samples are flattened into rows and
+// spread over the 32 lanes, so lanes stay busy whatever the sample counts.
+__global__ void __launch_bounds__(32 * kScreenWarps)
+k_screen(const Cand* __restrict__ front, int64_t n, const PairInfo* __restrict__ pairs,
+         const BodyInfo* __restrict__ bodies, const double* __restrict__ tris, ScreenOut out) {
+  __shared__ union {  // per warp: candidate info, later reused for child descriptors
+    CandInfo cand[32];
+    ChildInfo child[32];
+  } s_u[kScreenWarps];
+  __shared__ uint8_t s_bits[kScreenWarps][kRowsPerWarp];
+  extern __shared__ double s_stage[];  // kStaged x (32 * kScreenWarps), dynamic
+  const Staged st{s_stage + threadIdx.x, 32 * kScreenWarps};
+  const int warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
+  const int64_t n_warps = (n + 31) / 32;
+  CandInfo* info = s_u[warp].cand;
+  ChildInfo* kid = s_u[warp].child;
+  uint8_t* bits = s_bits[warp];
+
+  for (int64_t wi = blockIdx.x * (int64_t)kScreenWarps + warp; wi < n_warps;
+       wi += (int64_t)gridDim.x * kScreenWarps) {
+    const int64_t ci = wi * 32 + lane;
+    const bool valid = ci < n;
+    CandInfo me{};
+    if (valid) {
+      const Cand c = front[ci];
+      const PairInfo p = pairs[c.pair];
+      const BodyInfo& A = bodies[p.ba];
+      const BodyInfo& B = bodies[p.bb];
+      const double* ra = rec(tris, A, c.la, c.ia);
+      const double* rb = rec(tris, B, c.lb, c.ib);
+      me.h = add(__ldg(ra + 9), __ldg(rb + 9));  // ccd.py:339
+      double sp = p.speed0;                      // ccd.py:340-345
+      if (A.m.omega > 0.0) sp = add(sp, mul(A.m.omega, __ldg(ra + 10)));
+      if (B.m.omega > 0.0) sp = add(sp, mul(B.m.omega, __ldg(rb + 10)));
+      me.speed = sp;
+      me.w0 = c.w0;
+      me.dt = p.dt;
+      const double span = fmax(sub(p.dt, c.w0), 0.0);
+      me.count = sample_count(span, sp, me.h);
+      const double step = me.count > 1
+          ? sub(linspace_at(c.w0, p.dt, me.count, 1), linspace_at(c.w0, p.dt, me.count, 0)) : 0.0;
+      me.thr = add(me.h, mul(mul(0.5, sp), step));  // ccd.py:410-411
+      me.pair = c.pair;
+      me.ia = c.ia;
+      me.ib = c.ib;
+      me.la = c.la;
+      me.lb = c.lb;
+    }
+    const int incl = warp_incl_scan(me.count, lane);
+    const int total = __shfl_sync(0xffffffffu, incl, 31);
+    me.first = incl - me.count;
+    info[lane] = me;
+    __syncwarp();
+
+    for (int r = lane; r < total; r += 32) {
+      int o = 0;  // owner: last lane with first <= r (valid lanes have count >= 1)
+#pragma unroll
+      for (int step = 16; step > 0; step >>= 1)
+        if (info[o + step].first <= r) o += step;
+      const CandInfo& c = info[o];
+      const double tau = linspace_at(c.w0, c.dt, c.count, r - c.first);
+      const PairInfo p = pairs[c.pair];
+      const double d = row_distance(st, tris, bodies[p.ba], bodies[p.bb], c.la, c.ia, c.lb, c.ib, tau);
+      uint8_t b = 0;
+      if (d <= c.thr) b |= 1;                  // screen flag
+      if (d <= c.h) b |= 2;                    // at or below touching distance
+      if (d <= add(c.h, kRestSlop)) b |= 4;    // resting test (ccd.py:407)
+      bits[r] = b;
+    }
+    __syncwarp();
+
+    // per-candidate decisions
+    ChildInfo ch{};
+    if (valid) {
+      const uint8_t* cb = bits + me.first;
+      const bool fine = me.la == 0 && me.lb == 0;
+      if (fine && me.w0 == 0.0 && (cb[0] & 4)) {
+        const unsigned long long slot = atomicAdd(&out.ctr->resting, 1ULL);
+        if (slot < out.rest_cap) out.resting[slot] = RestRec{me.pair, me.ia, me.ib, 0, me.h};
+      } else {
+        int k0 = -1;
+        for (int k = 0; k < me.count; ++k)
+          if (cb[k] & 1) { k0 = k; break; }
+        if (k0 >= 0 && !fine) {  // ccd.py:414-428
+          const PairInfo p = pairs[me.pair];
+          ch.w0 = linspace_at(me.w0, me.dt, me.count, k0 > 0 ? k0 - 1 : 0);
+          ch.pair = me.pair;
+          int na = 1, nb = 1;
+          ch.ia0 = me.ia;
+          ch.ib0 = me.ib;
+          if (me.la > 0) {
+            const int2 cr = *reinterpret_cast<const int2*>(rec(tris, bodies[p.ba], me.la, me.ia) + 11);
+            ch.ia0 = cr.x;
+            na = cr.y;
+          }
+          if (me.lb > 0) {
+            const int2 cr = *reinterpret_cast<const int2*>(rec(tris, bodies[p.bb], me.lb, me.ib) + 11);
+            ch.ib0 = cr.x;
+            nb = cr.y;
+          }
+          ch.nb = nb;
+          ch.count = na * nb;
+          ch.la = me.la > 0 ? me.la - 1 : 0;
+          ch.lb = me.lb > 0 ? me.lb - 1 : 0;
+        } else if (k0 >= 0) {  // fine: flagged runs (ccd.py:429-446)
+          int k = k0;
+          while (k < me.count) {
+            if (!(cb[k] & 1)) { ++k; continue; }
+            int ke = k;
+            while (ke + 1 < me.count && (cb[ke + 1] & 1)) ++ke;
+            const int lo_i = k > 0 ? k - 1 : 0;
+            const int hi_i = ke + 1 < me.count - 1 ? ke + 1 : me.count - 1;
+            if (cb[lo_i] & 2) {
+              const unsigned long long slot = atomicAdd(&out.ctr->cross, 1ULL);
+              if (slot < out.cross_cap)
+                out.cross[slot] = Cross{me.pair, me.ia, me.ib, 0,
+                                        linspace_at(me.w0, me.dt, me.count, lo_i), me.h};
+            } else if (hi_i > lo_i) {
+              const unsigned long long slot = atomicAdd(&out.ctr->entries, 1ULL);
+              if (slot < out.entry_cap)
+                out.entries[slot] = Entry{me.pair, me.ia, me.ib, 0,
+                                          linspace_at(me.w0, me.dt, me.count, lo_i),
+                                          linspace_at(me.w0, me.dt, me.count, hi_i), me.h, me.speed};
+            }
+            k = ke + 1;
+          }
+        }
+      }
+    }
+    // cooperative, coalesced child emission
+    const int cincl = warp_incl_scan(ch.count, lane);
+    const int ctotal = __shfl_sync(0xffffffffu, cincl, 31);
+    unsigned long long cbase = 0;
+    if (lane == 0) {
+      atomicAdd(&out.ctr->rows, (unsigned long long)total);
+      if (ctotal) cbase = atomicAdd(&out.ctr->next, (unsigned long long)ctotal);
+    }
+    cbase = __shfl_sync(0xffffffffu, cbase, 0);
+    if (ctotal) {
+      ch.first = cincl - ch.count;
+      __syncwarp();  // cand and child info share storage
+      kid[lane] = ch;
+      __syncwarp();
+      for (int s = lane; s < ctotal; s += 32) {
+        int o = 0;
+#pragma unroll
+        for (int step = 16; step > 0; step >>= 1)
+          if (kid[o + step].first <= s) o += step;
+        const ChildInfo& c = kid[o];
+        const int j = s - c.first;
+        const unsigned long long dst = cbase + s;
+        if (dst < out.next_cap) {
+          Cand nc;
+          nc.pair = c.pair;
+          nc.ia = c.ia0 + j / c.nb;
+          nc.ib = c.ib0 + j % c.nb;
+          nc.la = (int16_t)c.la;
+          nc.lb = (int16_t)c.lb;
+          nc.w0 = c.w0;
+          out.next[dst] = nc;
+        }
+      }
+    }
+    __syncwarp();
+  }
+}
+
+// ---------------------------------------------------------------- zoom
+
+constexpr int kZoomQueue = 512;
+constexpr int kZoomWarps = 4;
+
+struct Interval {
+  double a, b;
+};
+
+// ccd._isolate_crossings (ccd.py:242-308), one warp per entry.  The
+// intervals of a round are processed in order, each sampled at 17 points by
+// lanes 0..16; once a bracket exists, intervals starting at or after its lo
+// are skipped (ccd.py:278-279), exactly as the reference's sequential loop.
+__global__ void __launch_bounds__(32 * kZoomWarps)
+k_zoom(const Entry* __restrict__ entries, int64_t n, const PairInfo* __restrict__ pairs,
+       const BodyInfo* __restrict__ bodies, const double* __restrict__ tris,
+       Interval* __restrict__ queue, Bracket* brackets, Counters* ctr) {
+  __shared__ double s_grid[kZoomWarps][kZoomSamples + 1];
+  __shared__ double s_stage[kStaged * 32 * kZoomWarps];
+  const Staged st{s_stage + threadIdx.x, 32 * kZoomWarps};
+  const int warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
+  const int64_t gw = blockIdx.x * (int64_t)kZoomWarps + warp;
+  Interval* q0 = queue + gw * 2 * kZoomQueue;
+  Interval* q1 = q0 + kZoomQueue;
+  double* grid = s_grid[warp];
+  for (int64_t e = gw; e < n; e += (int64_t)gridDim.x * kZoomWarps) {
+    const Entry en = entries[e];
+    const PairInfo p = pairs[en.pair];
+    const BodyInfo& A = bodies[p.ba];
+    const BodyInfo& B = bodies[p.bb];
+    Interval* cur = q0;
+    Interval* nxt = q1;
+    int n_cur = 1;
+    if (lane == 0) cur[0] = Interval{en.lo, en.hi};
+    __syncwarp();
+    bool have = false;
+    double blo = 0.0, bhi = 0.0;
+    unsigned long long ref_rows = 0, exec_rows = 0;
+    bool overflow = false;
+    for (int round = 0; round < 64 && n_cur > 0; ++round) {
+      ref_rows += (unsigned long long)n_cur * kZoomSamples;
+      int n_nxt = 0;
+      for (int iv = 0; iv < n_cur; ++iv) {
+        const Interval I = cur[iv];
+        if (lane < kZoomSamples) grid[lane] = linspace_at(I.a, I.b, kZoomSamples, lane);
+        __syncwarp();
+        const bool skip = have && grid[0] >= blo;
+        if (!skip) {
+          double d = 0.0;
+          if (lane < kZoomSamples) d = row_distance(st, tris, A, B, 0, en.ia, 0, en.ib, grid[lane]);
+          exec_rows += kZoomSamples;
+          const double slack = mul(mul(0.5, en.speed), sub(grid[1], grid[0]));
+          const unsigned below = __ballot_sync(0xffffffffu, lane < kZoomSamples && d <= en.h);
+          int cut = kZoomSamples;
+          if (below) {
+            const int j = __ffs(below) - 1;
+            blo = j > 0 ? grid[j - 1] : grid[0];
+            bhi = grid[j];
+            have = true;
+            cut = j;
+          }
+          if (slack > kGrazeTol) {
+            const unsigned flags = __ballot_sync(0xffffffffu, lane < cut && d <= add(en.h, slack));
+            if (lane == 0) {
+              int k = 0;
+              while (k < cut) {
+                if (!((flags >> k) & 1u)) { ++k; continue; }
+                int ke = k;
+                while (ke + 1 < cut && ((flags >> (ke + 1)) & 1u)) ++ke;
+                const double sa = grid[k > 0 ? k - 1 : 0];
+                const double sb = grid[ke + 1 < cut - 1 ? ke + 1 : cut - 1];
+                if (sb > sa) {
+                  if (n_nxt < kZoomQueue) nxt[n_nxt] = Interval{sa, sb}; else overflow = true;
+                  ++n_nxt;
+                }
+                k = ke + 1;
+              }
+            }
+            n_nxt = __shfl_sync(0xffffffffu, n_nxt, 0);
+          }
+        }
+        __syncwarp();
+      }
+      Interval* t = cur;
+      cur = nxt;
+      nxt = t;
+      n_cur = n_nxt < kZoomQueue ? n_nxt : kZoomQueue;
+    }
+    if (lane == 0) {
+      atomicAdd(&ctr->zoom_rows, ref_rows);
+      atomicAdd(&ctr->zoom_exec, exec_rows);
+      if (overflow) atomicExch(&ctr->overflow, 1ULL);
+      if (have) {
+        const unsigned long long slot = atomicAdd(&ctr->brackets, 1ULL);
+        brackets[slot] = Bracket{en.pair, en.ia, en.ib, 0, blo, bhi, en.h};
+      }
+    }
+    __syncwarp();
+  }
+}
+
+// ccd._batched_bisect (ccd.py:311-318): 52 halvings, returns hi.
+__global__ void k_bisect(const Bracket* __restrict__ br, int64_t n, const PairInfo* __restrict__ pairs,
+                         const BodyInfo* __restrict__ bodies, const double* __restrict__ tris,
+                         Cross* cross, unsigned long long cross_base, unsigned long long* tau_min_bits) {
+  __shared__ double s_stage[kStaged * 64];
+  const Staged st{s_stage + threadIdx.x, 64};
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const Bracket b = br[i];
+  const PairInfo p = pairs[b.pair];
+  const BodyInfo& A = bodies[p.ba];
+  const BodyInfo& B = bodies[p.bb];
+  double lo = b.lo, hi = b.hi;
+  for (int it = 0; it < kBisectIters; ++it) {
+    const double mid = mul(0.5, add(lo, hi));
+    if (row_distance(st, tris, A, B, 0, b.ia, 0, b.ib, mid) <= b.h) hi = mid; else lo = mid;
+  }
+  cross[cross_base + i] = Cross{b.pair, b.ia, b.ib, 1, hi, b.h};
+  // tau >= 0, so the IEEE bit pattern orders like the value
+  atomicMin(tau_min_bits + p.problem, (unsigned long long)__double_as_longlong(hi));
+}
+
+// ---------------------------------------------------------------- finalize
+
+__global__ void k_init_problems(unsigned long long* tau_min_bits, int n) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) tau_min_bits[i] = 0x7ff0000000000000ULL;  // +inf
+}
+
+// Shared bound, effective step, collision (ccd.py:459-471).  Crossings are
+// visited in ascending tau by the reference, so its bound is min(dt, min tau).
+__global__ void k_finalize(const unsigned long long* tau_min_bits, const double* problem_dt, int n,
+                           double widen, double* dt_out, double* first_out, int32_t* coll_out) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const double dt = problem_dt[i];
+  const double tmin = __longlong_as_double((long long)tau_min_bits[i]);
+  const double bound = tmin < dt ? tmin : dt;
+  const bool collision = bound < dt;
+  double eff = dt;
+  if (collision) {
+    const double w = mul(bound, add(1.0, widen));
+    eff = dt < w ? dt : w;
+  }
+  dt_out[i] = eff;
+  first_out[i] = collision ? bound : 0.0;
+  coll_out[i] = collision ? 1 : 0;
+}
+
+struct Record {
+  int32_t pair, ia, ib, rest;
+  double tau, h;
+};
+
+// Resting contacts at tau = 0 and crossings with tau <= dt_eff (ccd.py:473-479).
+__global__ void k_collect(const RestRec* rest, int64_t n_rest, const Cross* cross, int64_t n_cross,
+                          const PairInfo* pairs, const double* dt_eff, Record* out, Counters* ctr) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i < n_rest) {
+    const RestRec r = rest[i];
+    out[atomicAdd(&ctr->records, 1ULL)] = Record{r.pair, r.ia, r.ib, 1, 0.0, r.h};
+  } else if (i < n_rest + n_cross) {
+    const Cross c = cross[i - n_rest];
+    if (c.tau <= dt_eff[pairs[c.pair].problem])
+      out[atomicAdd(&ctr->records, 1ULL)] = Record{c.pair, c.ia, c.ib, 0, c.tau, c.h};
+  }
+}
+
+// ---------------------------------------------------------------- contacts
+
+struct Soa {
+  int32_t* problem;
+  int32_t* body_a;
+  int32_t* body_b;
+  double* position;
+  double* normal;
+  double* depth;
+  double* t;
+  int32_t* tri_a;
+  int32_t* tri_b;
+  double* threshold;
+};
+
+__device__ __forceinline__ void soa_copy(const Soa& s, int64_t i, const Soa& d, int64_t j) {
+  d.problem[j] = s.problem[i];
+  d.body_a[j] = s.body_a[i];
+  d.body_b[j] = s.body_b[i];
+#pragma unroll
+  for (int c = 0; c < 3; ++c) {
+    d.position[3 * j + c] = s.position[3 * i + c];
+    d.normal[3 * j + c] = s.normal[3 * i + c];
+  }
+  d.depth[j] = s.depth[i];
+  d.t[j] = s.t[i];
+  d.tri_a[j] = s.tri_a[i];
+  d.tri_b[j] = s.tri_b[i];
+  d.threshold[j] = s.threshold[i];
+}
+
+// ccd._make_contact (ccd.py:183-213), one thread per record.
+__global__ void k_contacts(const Record* recs, int64_t n, const PairInfo* pairs, const BodyInfo* bodies,
+                           const double* tris, const int32_t* tri_orig, const double* tbase, Soa o,
+                           unsigned long long* key) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const Record r = recs[i];
+  const PairInfo p = pairs[r.pair];
+  const BodyInfo& A = bodies[p.ba];
+  const BodyInfo& B = bodies[p.bb];
+  const Tri ta = world_at(A.m, rec(tris, A, 0, r.ia), r.tau);
+  const Tri tb = world_at(B.m, rec(tris, B, 0, r.ib), r.tau);
+  V3 pa, pb;
+  const double dist = closest_feature(ta, tb, &pa, &pb);
+  V3 pos = scale(pa + pb, 0.5);
+  const V3 na = face_normal(ta);
+  const V3 nb = face_normal(tb);
+  if (fabs(dot_blas(na, nb)) >= kParallelCos) {
+    V3 mid;
+    if (overlap_centroid(ta, tb, na, &mid)) pos = mid;
+  }
+  V3 nrm;
+  if (dist > 1e-9) {
+    const V3 d = pa - pb;
+    nrm = V3{dv(d.x, dist), dv(d.y, dist), dv(d.z, dist)};
+  } else {
+    nrm = nb;
+    if (dot_blas(nrm, mean3(ta) - mean3(tb)) < 0.0) nrm = neg(nrm);
+  }
+  const double depth_raw = sub(r.h, dist);
+  const double t0 = tbase[p.problem];
+  o.problem[i] = p.problem;
+  o.body_a[i] = A.id;
+  o.body_b[i] = B.id;
+  o.position[3 * i] = pos.x;
+  o.position[3 * i + 1] = pos.y;
+  o.position[3 * i + 2] = pos.z;
+  o.normal[3 * i] = nrm.x;
+  o.normal[3 * i + 1] = nrm.y;
+  o.normal[3 * i + 2] = nrm.z;
+  o.depth[i] = depth_raw > 0.0 ? depth_raw : 0.0;  // max(0.0, h - dist)
+  o.t[i] = r.rest ? t0 : add(t0, r.tau);
+  o.tri_a[i] = tri_orig[A.level_off[0] + r.ia];
+  o.tri_b[i] = tri_orig[B.level_off[0] + r.ib];
+  o.threshold[i] = r.h;
+  key[i] = ((unsigned long long)(uint32_t)p.problem << 32) | (uint32_t)p.group;
+}
+
+// ---------------------------------------------------------------- fusion
+
+__device__ __forceinline__ double round9(double x) {  // round(np.float64, 9) = rint(x*1e9)/1e9
+  return dv(rint(mul(x, 1e9)), 1e9);
+}
+
+// Sort key of ccd.py:541-542: (t, round9(x), round9(y), round9(z), tri_a, tri_b).
+__device__ __forceinline__ bool key_less(const Soa& o, int64_t a, int64_t b) {
+  if (o.t[a] != o.t[b]) return o.t[a] < o.t[b];
+#pragma unroll
+  for (int k = 0; k < 3; ++k) {
+    const double ra = round9(o.position[3 * a + k]), rb = round9(o.position[3 * b + k]);
+    if (ra != rb) return ra < rb;
+  }
+  if (o.tri_a[a] != o.tri_a[b]) return o.tri_a[a] < o.tri_a[b];
+  return o.tri_b[a] < o.tri_b[b];
+}
+
+// filter_contacts for one (problem, body pair) group per thread: canonical
+// stable sort, union-find over points within max(threshold), merge
+// (ccd.py:540-576).  Fused results land in the group's own slot range.
+__global__ void k_fuse_big(Soa o, int64_t* idx, const int64_t* g_off, int64_t n_groups, int64_t n_total,
+                           int32_t* parent, Soa f, int64_t* g_fused, int32_t* prob_count,
+                           const int32_t* big_list, const int32_t* big_count) {
+  const int64_t bi = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (bi >= *big_count) return;
+  const int64_t g = big_list[bi];
+  const int64_t off = g_off[g];
+  const int64_t n = (g + 1 < n_groups ? g_off[g + 1] : n_total) - off;
+  int64_t* ix = idx + off;
+  int32_t* par = parent + off;
+  for (int64_t i = 1; i < n; ++i) {
+    const int64_t v = ix[i];
+    int64_t j = i - 1;
+    while (j >= 0 && key_less(o, v, ix[j])) {
+      ix[j + 1] = ix[j];
+      --j;
+    }
+    ix[j + 1] = v;
+  }
+  for (int64_t i = 0; i < n; ++i) par[i] = (int32_t)i;
+  auto find = [&](int32_t i) {
+    while (par[i] != i) i = par[i];
+    return i;
+  };
+  for (int64_t i = 0; i < n; ++i) {
+    const int64_t a = ix[i];
+    const V3 pa{o.position[3 * a], o.position[3 * a + 1], o.position[3 * a + 2]};
+    for (int64_t j = i + 1; j < n; ++j) {
+      const int64_t b = ix[j];
+      const double rad = fmax(o.threshold[a], o.threshold[b]);
+      const V3 pb{o.position[3 * b], o.position[3 * b + 1], o.position[3 * b + 2]};
+      if (norm_blas(pa - pb) <= rad) par[find((int32_t)j)] = find((int32_t)i);
+    }
+  }
+  for (int64_t i = 0; i < n; ++i) par[i] = find((int32_t)i);
+  int64_t nf = 0;
+  for (int64_t r = 0; r < n; ++r) {
+    if (par[r] != r) continue;
+    V3 ps{0, 0, 0}, ns{0, 0, 0};
+    int64_t cnt = 0, rep = -1, first = -1;
+    double dmax = 0.0, tmin = 0.0, thr = 0.0;
+    // members in ascending sorted index; a root need not be its smallest member
+    for (int64_t i = 0; i < n; ++i) {
+      if (par[i] != r) continue;
+      const int64_t a = ix[i];
+      const V3 pp{o.position[3 * a], o.position[3 * a + 1], o.position[3 * a + 2]};
+      const V3 nn{o.normal[3 * a], o.normal[3 * a + 1], o.normal[3 * a + 2]};
+      if (cnt == 0) {
+        first = a;
+        ps = pp;
+        ns = nn;
+        dmax = o.depth[a];
+        tmin = o.t[a];
+        thr = o.threshold[a];
+        rep = a;
+      } else {
+        ps = ps + pp;  // np.mean / np.sum over axis 0: sequential
+        ns = ns + nn;
+        if (o.depth[a] > dmax) dmax = o.depth[a];
+        if (o.t[a] < tmin) tmin = o.t[a];
+        if (o.threshold[a] > thr) thr = o.threshold[a];
+        if (o.t[a] < o.t[rep] || (o.t[a] == o.t[rep] && -o.depth[a] < -o.depth[rep])) rep = a;
+      }
+      ++cnt;
+    }
+    const double c = (double)cnt;
+    const V3 pos{dv(ps.x, c), dv(ps.y, c), dv(ps.z, c)};
+    const double ln = norm_blas(ns);
+    V3 nrm;
+    if (ln > 1e-12) {
+      nrm = V3{dv(ns.x, ln), dv(ns.y, ln), dv(ns.z, ln)};
+    } else {
+      nrm = V3{o.normal[3 * first], o.normal[3 * first + 1], o.normal[3 * first + 2]};
+    }
+    const int64_t dst = off + nf;
+    f.problem[dst] = o.problem[rep];
+    f.body_a[dst] = o.body_a[rep];
+    f.body_b[dst] = o.body_b[rep];
+    f.position[3 * dst] = pos.x;
+    f.position[3 * dst + 1] = pos.y;
+    f.position[3 * dst + 2] = pos.z;
+    f.normal[3 * dst] = nrm.x;
+    f.normal[3 * dst + 1] = nrm.y;
+    f.normal[3 * dst + 2] = nrm.z;
+    f.depth[dst] = dmax;
+    f.t[dst] = tmin;
+    f.tri_a[dst] = o.tri_a[rep];
+    f.tri_b[dst] = o.tri_b[rep];
+    f.threshold[dst] = thr;
+    ++nf;
+  }
+  g_fused[g] = nf;
+  if (n > 0) atomicAdd(prob_count + o.problem[ix[0]], (int32_t)nf);
+}
+
+
+// filter_contacts, one block per (problem, body pair) group of at most
+// kFuseCap records, staged in shared memory: keys and positions are loaded
+// once, the stable sort is a parallel rank sort, the "within max(threshold)"
+// adjacency is a bit matrix built by all threads, and one thread replays the
+// reference's union-find over it (ccd.py:543-555) so roots -- and therefore
+// the output order -- are identical.  Larger groups go to k_fuse_big.
+constexpr int kFuseCap = 256;
+constexpr int kFuseWords = kFuseCap / 32;
+constexpr int kFuseThreads = 128;
+
+struct FuseKey {
+  double t, r0, r1, r2;
+  int32_t ta, tb;
+};
+
+__device__ __forceinline__ bool fkey_less(const FuseKey& a, const FuseKey& b) {
+  if (a.t != b.t) return a.t < b.t;
+  if (a.r0 != b.r0) return a.r0 < b.r0;
+  if (a.r1 != b.r1) return a.r1 < b.r1;
+  if (a.r2 != b.r2) return a.r2 < b.r2;
+  if (a.ta != b.ta) return a.ta < b.ta;
+  return a.tb < b.tb;
+}
+
+__global__ void __launch_bounds__(kFuseThreads)
+k_fuse_block(Soa o, int64_t* __restrict__ idx, const int64_t* __restrict__ g_off, int64_t n_groups,
+             int64_t n_total, Soa f, int64_t* g_fused, int32_t* prob_count, int32_t* big_list,
+             int32_t* big_count) {
+  __shared__ FuseKey s_key[kFuseCap];
+  __shared__ int64_t s_gi[kFuseCap];
+  __shared__ double s_p[3][kFuseCap];
+  __shared__ double s_thr[kFuseCap];
+  __shared__ int32_t s_par[kFuseCap];
+  __shared__ int32_t s_slot[kFuseCap];
+  __shared__ uint32_t s_adj[kFuseCap * kFuseWords];
+  __shared__ int32_t s_nroots;
+  const int tid = threadIdx.x;
+  for (int64_t g = blockIdx.x; g < n_groups; g += gridDim.x) {
+    const int64_t off = g_off[g];
+    const int n = (int)((g + 1 < n_groups ? g_off[g + 1] : n_total) - off);
+    if (n > kFuseCap) {
+      if (tid == 0) big_list[atomicAdd(big_count, 1)] = (int32_t)g;
+      continue;
+    }
+    int64_t* ix = idx + off;
+    __syncthreads();
+    for (int i = tid; i < n; i += kFuseThreads) {
+      const int64_t a = ix[i];
+      FuseKey k;
+      k.t = o.t[a];
+      k.r0 = round9(o.position[3 * a]);
+      k.r1 = round9(o.position[3 * a + 1]);
+      k.r2 = round9(o.position[3 * a + 2]);
+      k.ta = o.tri_a[a];
+      k.tb = o.tri_b[a];
+      s_key[i] = k;
+    }
+    __syncthreads();
+    // stable rank sort (ccd.py:541-542): equal keys keep their input order
+    for (int i = tid; i < n; i += kFuseThreads) {
+      const FuseKey ki = s_key[i];
+      int rank = 0;
+      for (int j = 0; j < n; ++j) {
+        const FuseKey kj = s_key[j];
+        rank += (fkey_less(kj, ki) || (j < i && !fkey_less(ki, kj))) ? 1 : 0;
+      }
+      const int64_t a = ix[i];
+      s_gi[rank] = a;
+      s_p[0][rank] = o.position[3 * a];
+      s_p[1][rank] = o.position[3 * a + 1];
+      s_p[2][rank] = o.position[3 * a + 2];
+      s_thr[rank] = o.threshold[a];
+    }
+    __syncthreads();
+    for (int r = tid; r < n; r += kFuseThreads) ix[r] = s_gi[r];  // canonical raw order
+    // adjacency bit matrix, upper triangle: |p_i - p_j| <= max(thr_i, thr_j) (ccd.py:551-555)
+    const int words = (n + 31) / 32;
+    for (int w = tid; w < n * words; w += kFuseThreads) {
+      const int row = w / words, word = w % words;
+      const V3 pi{s_p[0][row], s_p[1][row], s_p[2][row]};
+      const double ti = s_thr[row];
+      uint32_t bits = 0;
+      for (int b = 0; b < 32; ++b) {
+        const int j = word * 32 + b;
+        if (j <= row || j >= n) continue;
+        const V3 pj{s_p[0][j], s_p[1][j], s_p[2][j]};
+        if (norm_blas(pi - pj) <= fmax(ti, s_thr[j])) bits |= 1u << b;
+      }
+      s_adj[row * kFuseWords + word] = bits;
+    }
+    __syncthreads();
+    if (tid == 0) {
+      for (int i = 0; i < n; ++i) s_par[i] = i;
+      for (int i = 0; i < n; ++i) {
+        int ri = i;
+        while (s_par[ri] != ri) ri = s_par[ri];
+        for (int word = i / 32; word < words; ++word) {
+          uint32_t bits = s_adj[i * kFuseWords + word];
+          while (bits) {
+            const int j = word * 32 + __ffs(bits) - 1;
+            bits &= bits - 1;
+            int rj = j;
+            while (s_par[rj] != rj) rj = s_par[rj];
+            s_par[rj] = ri;  // parent[find(j)] = find(i)
+          }
+        }
+      }
+      int nr = 0;
+      for (int i = 0; i < n; ++i) {
+        int r = i;
+        while (s_par[r] != r) r = s_par[r];
+        s_par[i] = r;
+      }
+      for (int i = 0; i < n; ++i)
+        if (s_par[i] == i) s_slot[i] = nr++;
+      s_nroots = nr;
+    }
+    __syncthreads();
+    for (int r = tid; r < n; r += kFuseThreads) {
+      if (s_par[r] != r) continue;
+      V3 ps{0, 0, 0}, ns{0, 0, 0};
+      int cnt = 0;
+      int64_t rep = -1, first = -1;
+      double dmax = 0.0, tmin = 0.0, thr = 0.0;
+      for (int i = 0; i < n; ++i) {  // members in ascending sorted order (ccd.py:557-558)
+        if (s_par[i] != r) continue;
+        const int64_t a = s_gi[i];
+        const V3 pp{s_p[0][i], s_p[1][i], s_p[2][i]};
+        const V3 nn{o.normal[3 * a], o.normal[3 * a + 1], o.normal[3 * a + 2]};
+        const double da = o.depth[a], ta = o.t[a], tha = o.threshold[a];
+        if (cnt == 0) {
+          first = a;
+          rep = a;
+          ps = pp;
+          ns = nn;
+          dmax = da;
+          tmin = ta;
+          thr = tha;
+        } else {
+          ps = ps + pp;
+          ns = ns + nn;
+          if (da > dmax) dmax = da;
+          if (ta < tmin) tmin = ta;
+          if (tha > thr) thr = tha;
+          if (ta < o.t[rep] || (ta == o.t[rep] && -da < -o.depth[rep])) rep = a;
+        }
+        ++cnt;
+      }
+      const double c = (double)cnt;
+      const V3 pos{dv(ps.x, c), dv(ps.y, c), dv(ps.z, c)};
+      const double ln = norm_blas(ns);
+      V3 nrm;
+      if (ln > 1e-12) {
+        nrm = V3{dv(ns.x, ln), dv(ns.y, ln), dv(ns.z, ln)};
+      } else {
+        nrm = V3{o.normal[3 * first], o.normal[3 * first + 1], o.normal[3 * first + 2]};
+      }
+      const int64_t dst = off + s_slot[r];
+      f.problem[dst] = o.problem[rep];
+      f.body_a[dst] = o.body_a[rep];
+      f.body_b[dst] = o.body_b[rep];
+      f.position[3 * dst] = pos.x;
+      f.position[3 * dst + 1] = pos.y;
+      f.position[3 * dst + 2] = pos.z;
+      f.normal[3 * dst] = nrm.x;
+      f.normal[3 * dst + 1] = nrm.y;
+      f.normal[3 * dst + 2] = nrm.z;
+      f.depth[dst] = dmax;
+      f.t[dst] = tmin;
+      f.tri_a[dst] = o.tri_a[rep];
+      f.tri_b[dst] = o.tri_b[rep];
+      f.threshold[dst] = thr;
+    }
+    if (tid == 0) {
+      g_fused[g] = s_nroots;
+      if (n > 0) atomicAdd(prob_count + o.problem[ix[0]], s_nroots);
+    }
+  }
+}
+
+__global__ void k_compact(Soa f, const int64_t* g_off, const int64_t* g_fused, const int64_t* g_dst,
+                          int64_t n_groups, Soa o) {
+  for (int64_t g = blockIdx.x; g < n_groups; g += gridDim.x) {
+    const int64_t src = g_off[g], dst = g_dst[g], n = g_fused[g];
+    for (int64_t k = threadIdx.x; k < n; k += blockDim.x) soa_copy(f, src + k, o, dst + k);
+  }
+}
+
+__global__ void k_gather(Soa s, const int64_t* idx, int64_t n, Soa d) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i < n) soa_copy(s, idx[i], d, i);
+}
+
+__global__ void k_heads(const unsigned long long* keys, int64_t n, int64_t* head) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i < n) head[i] = (i == 0 || keys[i] != keys[i - 1]) ? 1 : 0;
+  if (i == n) head[n] = 0;
+}
+
+__global__ void k_group_table(const int64_t* head, const int64_t* head_scan, int64_t n, int64_t* g_off) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i < n && head[i]) g_off[head_scan[i]] = i;
+}
+
+__global__ void k_iota(int64_t* x, int64_t n) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i < n) x[i] = i;
+}
+
+__global__ void k_widen(const int32_t* a, int64_t* b, int64_t n) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i < n) b[i] = a[i];
+}
+
+// Exhaustive fine x fine screen of pair `k` at tau = 0 over an implicit
+// frontier (no candidate records): the roofline microbenchmark.
+__global__ void __launch_bounds__(128)
+k_allpairs(const PairInfo* __restrict__ pairs, int64_t n_pairs, const BodyInfo* __restrict__ bodies,
+           const double* __restrict__ tris, unsigned long long* hits) {
+  __shared__ double s_stage[kStaged * 128];
+  const Staged st{s_stage + threadIdx.x, 128};
+  unsigned long long local = 0;
+  for (int64_t k = blockIdx.y; k < n_pairs; k += gridDim.y) {
+    const PairInfo p = pairs[k];
+    const BodyInfo& A = bodies[p.ba];
+    const BodyInfo& B = bodies[p.bb];
+    const int64_t na = A.level_size[0], nb = B.level_size[0];
+    const int64_t total = na * nb;
+    for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < total;
+         j += (int64_t)gridDim.x * blockDim.x) {
+      const int ia = (int)(j / nb), ib = (int)(j % nb);
+      const double* ra = rec(tris, A, 0, ia);
+      const double* rb = rec(tris, B, 0, ib);
+      const double h = add(__ldg(ra + 9), __ldg(rb + 9));
+      const double d = row_distance(st, tris, A, B, 0, ia, 0, ib, 0.0);
+      if (d <= add(h, kRestSlop)) ++local;
+    }
+  }
+  for (int o = 16; o > 0; o >>= 1) local += __shfl_down_sync(0xffffffffu, local, o);
+  if ((threadIdx.x & 31) == 0 && local) atomicAdd(hits, local);
+}
+
+// ---------------------------------------------------------------- host side
+
+template <typename T>
+static int ws_get(ltsg_workspace* ws, const char* name, size_t count, T** out, bool keep = false) {
+  void* p = nullptr;
+  LTSG_TRY(ws->get(name, std::max<size_t>(count, 1) * sizeof(T), &p, keep));
+  *out = static_cast<T*>(p);
+  return LTSG_OK;
+}
+
+static int read_ctr(Counters* d, Counters* h, cudaStream_t st) {
+  LTSG_CUDA(cudaMemcpyAsync(h, d, sizeof(Counters), cudaMemcpyDeviceToHost, st));
+  LTSG_CUDA(cudaStreamSynchronize(st));
+  return LTSG_OK;
+}
+
+static int scan_exclusive(ltsg_workspace* ws, const int64_t* in, int64_t* out, int64_t n, cudaStream_t st) {
+  size_t tmp = 0;
+  LTSG_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, tmp, in, out, n, st));
+  void* t = nullptr;
+  LTSG_TRY(ws->get("cub_tmp", tmp, &t));
+  LTSG_CUDA(cub::DeviceScan::ExclusiveSum(t, tmp, in, out, n, st));
+  return LTSG_OK;
+}
+
+constexpr int kScreenStageBytes = kStaged * 32 * kScreenWarps * sizeof(double);
+
+static int configure_kernels() {
+  static int done = 0;
+  if (!done) {
+    LTSG_CUDA(cudaFuncSetAttribute(k_screen, cudaFuncAttributeMaxDynamicSharedMemorySize, kScreenStageBytes));
+    done = 1;
+  }
+  return LTSG_OK;
+}
+
+static int screen_grid(int64_t n) {
+  const int64_t warps = (n + 31) / 32;
+  const int64_t blocks = (warps + kScreenWarps - 1) / kScreenWarps;
+  return (int)std::max<int64_t>(1, std::min<int64_t>(blocks, 148LL * 32));
+}
+
+struct Prepared {
+  BodyInfo* bodies;
+  PairInfo* pairs;
+};
+
+static int validate(const ltsg_scene* sc) {
+  if (!sc || sc->n_bodies < 0 || sc->n_pairs < 0 || sc->n_problems < 0 || sc->max_children < 1 ||
+      (sc->n_pairs > 0 && (!sc->tris || !sc->body_state || !sc->body_levels || !sc->pair_body ||
+                           !sc->pair_problem || !sc->pair_group || !sc->problem_dt ||
+                           !sc->problem_tbase || !sc->tri_orig))) {
+    set_error("ltsg_search: invalid scene");
+    return LTSG_EINVAL;
+  }
+  return LTSG_OK;
+}
+
+static int prepare(const ltsg_scene* sc, ltsg_workspace* ws, cudaStream_t st, Prepared* pr) {
+  LTSG_TRY(ws_get(ws, "bodies", (size_t)sc->n_bodies, &pr->bodies));
+  LTSG_TRY(ws_get(ws, "pairs", (size_t)sc->n_pairs, &pr->pairs));
+  if (sc->n_bodies > 0) {
+    k_prep_bodies<<<grid_for(sc->n_bodies, 128), 128, 0, st>>>(sc->body_state, sc->body_levels,
+                                                               sc->n_bodies, pr->bodies);
+    LTSG_CHECK_LAUNCH();
+  }
+  if (sc->n_pairs > 0) {
+    k_prep_pairs<<<grid_for(sc->n_pairs, 128), 128, 0, st>>>(sc->pair_body, sc->pair_problem,
+                                                             sc->pair_group, sc->n_pairs, pr->bodies,
+                                                             sc->problem_dt, pr->pairs);
+    LTSG_CHECK_LAUNCH();
+  }
+  return LTSG_OK;
+}
+
+static int fuse_stage(ltsg_workspace* ws, cudaStream_t st, Soa ro, unsigned long long* key, int64_t n_rec,
+                      int np, int32_t* prob_count, int64_t* prob_count64, ltsg_result* out);
+
+// Device-time accounting of one call: CUDA events on the call's stream.
+struct Timer {
+  cudaEvent_t a = nullptr, b = nullptr;
+  Timer() {
+    cudaEventCreate(&a);
+    cudaEventCreate(&b);
+  }
+  ~Timer() {
+    if (a) cudaEventDestroy(a);
+    if (b) cudaEventDestroy(b);
+  }
+  void start(cudaStream_t st) { cudaEventRecord(a, st); }
+  void stop(cudaStream_t st) { cudaEventRecord(b, st); }
+  double ms() {  // call after the stream has passed `b`
+    float m = 0.f;
+    cudaEventSynchronize(b);
+    cudaEventElapsedTime(&m, a, b);
+    return (double)m;
+  }
+};
+
+#define LTSG_LAUNCHED() \
+  do {                  \
+    LTSG_CHECK_LAUNCH(); \
+    ++out->launches;    \
+  } while (0)
+
+static int run_search(const ltsg_scene* sc, ltsg_result* out, ltsg_workspace* ws, cudaStream_t st) {
+  LTSG_TRY(validate(sc));
+  LTSG_TRY(configure_kernels());
+  const int np = sc->n_problems;
+  out->n_fused = out->n_raw = 0;
+  out->rows_screen = out->rows_zoom = out->rows_bisect = out->rows_executed = 0;
+  out->candidates = 0;
+  out->generations = 0;
+  out->launches = 0;
+  out->ms_screen = out->ms_refine = out->ms_contacts = 0.0;
+  if (np == 0) return LTSG_OK;
+
+  Prepared pr{};
+  LTSG_TRY(prepare(sc, ws, st, &pr));
+  out->launches += 2;
+  Timer t_screen, t_refine, t_contacts;
+  Counters* d_ctr;
+  LTSG_TRY(ws_get(ws, "ctr", 1, &d_ctr));
+  LTSG_CUDA(cudaMemsetAsync(d_ctr, 0, sizeof(Counters), st));
+  unsigned long long* tau_min;
+  LTSG_TRY(ws_get(ws, "tau_min", (size_t)np, &tau_min));
+  k_init_problems<<<grid_for(np, 128), 128, 0, st>>>(tau_min, np);
+  LTSG_LAUNCHED();
+
+  // ---- seeds: all root x root pairs (fine x fine when exhaustive), ccd.py:385-391
+  int64_t n_front = 0;
+  const char* fname[2] = {"front0", "front1"};
+  int fsel = 0;
+  Cand* front = nullptr;
+  if (sc->n_pairs > 0) {
+    int64_t *cnt, *off;
+    LTSG_TRY(ws_get(ws, "seed_cnt", (size_t)sc->n_pairs + 1, &cnt));
+    LTSG_TRY(ws_get(ws, "seed_off", (size_t)sc->n_pairs + 1, &off));
+    k_seed_count<<<grid_for(sc->n_pairs, 128), 128, 0, st>>>(pr.pairs, sc->n_pairs, pr.bodies,
+                                                             sc->exhaustive, cnt);
+    LTSG_LAUNCHED();
+    LTSG_CUDA(cudaMemsetAsync(cnt + sc->n_pairs, 0, sizeof(int64_t), st));
+    LTSG_TRY(scan_exclusive(ws, cnt, off, sc->n_pairs + 1, st));
+    LTSG_CUDA(cudaMemcpyAsync(&n_front, off + sc->n_pairs, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+    LTSG_CUDA(cudaStreamSynchronize(st));
+    LTSG_TRY(ws_get(ws, fname[fsel], (size_t)n_front, &front));
+    k_seed_fill<<<(int)std::min<int64_t>(sc->n_pairs, 148 * 16), 128, 0, st>>>(
+        pr.pairs, sc->n_pairs, pr.bodies, sc->exhaustive, off, front);
+    LTSG_LAUNCHED();
+  }
+
+  // ---- generations
+  size_t rest_cap = 1 << 16, entry_cap = 1 << 14, cross_cap = 1 << 14;
+  RestRec* resting;
+  Entry* entries;
+  Cross* cross;
+  LTSG_TRY(ws_get(ws, "resting", rest_cap, &resting));
+  LTSG_TRY(ws_get(ws, "entries", entry_cap, &entries));
+  LTSG_TRY(ws_get(ws, "cross", cross_cap, &cross));
+  Counters h{};
+  const int64_t fan = (int64_t)sc->max_children * sc->max_children;
+  while (n_front > 0) {
+    Cand* next;
+    LTSG_TRY(ws_get(ws, fname[fsel ^ 1], (size_t)(n_front * fan), &next));
+    Counters before;
+    LTSG_TRY(read_ctr(d_ctr, &before, st));
+    before.next = 0;
+    for (;;) {
+      LTSG_CUDA(cudaMemcpyAsync(d_ctr, &before, sizeof(Counters), cudaMemcpyHostToDevice, st));
+      ScreenOut so{next, (unsigned long long)(n_front * fan), resting, rest_cap, entries, entry_cap,
+                   cross, cross_cap, d_ctr};
+      t_screen.start(st);
+      k_screen<<<screen_grid(n_front), 32 * kScreenWarps, kScreenStageBytes, st>>>(
+          front, n_front, pr.pairs, pr.bodies, sc->tris, so);
+      LTSG_LAUNCHED();
+      t_screen.stop(st);
+      LTSG_TRY(read_ctr(d_ctr, &h, st));
+      out->ms_screen += t_screen.ms();
+      bool grow = false;
+      if (h.resting > rest_cap) {
+        rest_cap = (size_t)h.resting * 2;
+        LTSG_TRY(ws_get(ws, "resting", rest_cap, &resting, true));
+        grow = true;
+      }
+      if (h.entries > entry_cap) {
+        entry_cap = (size_t)h.entries * 2;
+        LTSG_TRY(ws_get(ws, "entries", entry_cap, &entries, true));
+        grow = true;
+      }
+      if (h.cross > cross_cap) {
+        cross_cap = (size_t)h.cross * 2;
+        LTSG_TRY(ws_get(ws, "cross", cross_cap, &cross, true));
+        grow = true;
+      }
+      if (!grow) break;
+    }
+    out->candidates += n_front;
+    out->generations += 1;
+    n_front = (int64_t)h.next;
+    fsel ^= 1;
+    front = next;
+  }
+
+  // ---- certified zoom + bisection
+  t_refine.start(st);
+  const int64_t n_entries = (int64_t)h.entries;
+  int64_t n_br = 0;
+  if (n_entries > 0) {
+    Bracket* br;
+    Interval* queue;
+    LTSG_TRY(ws_get(ws, "brackets", (size_t)n_entries, &br));
+    const int zblocks = (int)std::min<int64_t>((n_entries + kZoomWarps - 1) / kZoomWarps, 148 * 8);
+    LTSG_TRY(ws_get(ws, "zoomq", (size_t)zblocks * kZoomWarps * 2 * kZoomQueue, &queue));
+    k_zoom<<<zblocks, 32 * kZoomWarps, 0, st>>>(entries, n_entries, pr.pairs, pr.bodies, sc->tris, queue,
+                                                br, d_ctr);
+    LTSG_LAUNCHED();
+    LTSG_TRY(read_ctr(d_ctr, &h, st));
+    if (h.overflow) {
+      set_error("zoom interval queue overflow (more than %d pending intervals)", kZoomQueue);
+      return LTSG_ECAPACITY;
+    }
+    n_br = (int64_t)h.brackets;
+    if (n_br > 0) {
+      const size_t need = (size_t)(h.cross + n_br);
+      if (need > cross_cap) {
+        cross_cap = need;
+        LTSG_TRY(ws_get(ws, "cross", cross_cap, &cross, true));
+      }
+      k_bisect<<<grid_for(n_br, 64), 64, 0, st>>>(br, n_br, pr.pairs, pr.bodies, sc->tris, cross, h.cross,
+                                                 tau_min);
+      LTSG_LAUNCHED();
+    }
+  }
+  const int64_t n_cross = (int64_t)h.cross + n_br;
+  t_refine.stop(st);
+  t_contacts.start(st);
+  k_finalize<<<grid_for(np, 128), 128, 0, st>>>(tau_min, sc->problem_dt, np, sc->widen, out->dt,
+                                                out->first_contact, out->collision);
+  LTSG_LAUNCHED();
+
+  // ---- records
+  const int64_t n_rest = (int64_t)h.resting;
+  const int64_t n_cand_rec = n_rest + n_cross;
+  Record* recs;
+  LTSG_TRY(ws_get(ws, "records", (size_t)n_cand_rec, &recs));
+  if (n_cand_rec > 0) {
+    k_collect<<<grid_for(n_cand_rec, 128), 128, 0, st>>>(resting, n_rest, cross, n_cross, pr.pairs, out->dt,
+                                                        recs, d_ctr);
+    LTSG_LAUNCHED();
+  }
+  LTSG_TRY(read_ctr(d_ctr, &h, st));
+  const int64_t n_rec = (int64_t)h.records;
+  out->rows_screen = (int64_t)h.rows;
+  out->rows_zoom = (int64_t)h.zoom_rows;
+  out->rows_bisect = n_br * kBisectIters;
+  out->rows_executed = (int64_t)(h.rows + h.zoom_exec) + n_br * kBisectIters;
+  out->n_raw = n_rec;
+
+  int32_t* prob_count;
+  int64_t *prob_count64;
+  LTSG_TRY(ws_get(ws, "prob_count", (size_t)np + 1, &prob_count));
+  LTSG_TRY(ws_get(ws, "prob_count64", (size_t)np + 1, &prob_count64));
+  LTSG_CUDA(cudaMemsetAsync(prob_count, 0, sizeof(int32_t) * (np + 1), st));
+  if (n_rec == 0) {
+    LTSG_CUDA(cudaMemsetAsync(out->fused_offset, 0, sizeof(int64_t) * (np + 1), st));
+    out->n_fused = 0;
+    t_contacts.stop(st);
+    LTSG_CUDA(cudaStreamSynchronize(st));
+    out->ms_refine = t_refine.ms();
+    out->ms_contacts = t_contacts.ms();
+    return LTSG_OK;
+  }
+  if (n_rec > out->capacity) {
+    set_error("contact capacity %lld < %lld raw contacts", (long long)out->capacity, (long long)n_rec);
+    out->n_fused = n_rec;
+    return LTSG_ECAPACITY;
+  }
+
+  // ---- contact records (raw, record order)
+  Soa ro;
+  unsigned long long* key;
+  LTSG_TRY(ws_get(ws, "r_problem", n_rec, &ro.problem));
+  LTSG_TRY(ws_get(ws, "r_body_a", n_rec, &ro.body_a));
+  LTSG_TRY(ws_get(ws, "r_body_b", n_rec, &ro.body_b));
+  LTSG_TRY(ws_get(ws, "r_pos", 3 * n_rec, &ro.position));
+  LTSG_TRY(ws_get(ws, "r_nrm", 3 * n_rec, &ro.normal));
+  LTSG_TRY(ws_get(ws, "r_depth", n_rec, &ro.depth));
+  LTSG_TRY(ws_get(ws, "r_t", n_rec, &ro.t));
+  LTSG_TRY(ws_get(ws, "r_tri_a", n_rec, &ro.tri_a));
+  LTSG_TRY(ws_get(ws, "r_tri_b", n_rec, &ro.tri_b));
+  LTSG_TRY(ws_get(ws, "r_thr", n_rec, &ro.threshold));
+  LTSG_TRY(ws_get(ws, "r_key", n_rec, &key));
+  k_contacts<<<grid_for(n_rec, 64), 64, 0, st>>>(recs, n_rec, pr.pairs, pr.bodies, sc->tris, sc->tri_orig,
+                                                 sc->problem_tbase, ro, key);
+  LTSG_LAUNCHED();
+
+  LTSG_TRY(fuse_stage(ws, st, ro, key, n_rec, np, prob_count, prob_count64, out));
+  t_contacts.stop(st);
+  out->ms_refine = t_refine.ms();
+  out->ms_contacts = t_contacts.ms();
+  return LTSG_OK;
+}
+
+// Group raw records by (problem, body pair), fuse each group
+// (filter_contacts), write raw (canonical order) and fused outputs.
+static int fuse_stage(ltsg_workspace* ws, cudaStream_t st, Soa ro, unsigned long long* key, int64_t n_rec,
+                      int np, int32_t* prob_count, int64_t* prob_count64, ltsg_result* out) {
+  // group by (problem, body pair): radix sort of the group key
+  int64_t *idx_in, *idx, *head, *head_scan, *g_off, *g_fused, *g_dst;
+  unsigned long long* keys_sorted;
+  int32_t* parent;
+  LTSG_TRY(ws_get(ws, "idx_in", n_rec, &idx_in));
+  LTSG_TRY(ws_get(ws, "idx", n_rec, &idx));
+  LTSG_TRY(ws_get(ws, "keys_sorted", n_rec, &keys_sorted));
+  LTSG_TRY(ws_get(ws, "head", n_rec + 1, &head));
+  LTSG_TRY(ws_get(ws, "head_scan", n_rec + 1, &head_scan));
+  LTSG_TRY(ws_get(ws, "parent", n_rec, &parent));
+  k_iota<<<grid_for(n_rec, 256), 256, 0, st>>>(idx_in, n_rec);
+  LTSG_LAUNCHED();
+  {
+    size_t tmp = 0;
+    LTSG_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, tmp, key, keys_sorted, idx_in, idx, n_rec, 0, 64, st));
+    void* t;
+    LTSG_TRY(ws->get("cub_tmp", tmp, &t));
+    LTSG_CUDA(cub::DeviceRadixSort::SortPairs(t, tmp, key, keys_sorted, idx_in, idx, n_rec, 0, 64, st));
+  }
+  k_heads<<<grid_for(n_rec + 1, 256), 256, 0, st>>>(keys_sorted, n_rec, head);
+  LTSG_LAUNCHED();
+  LTSG_TRY(scan_exclusive(ws, head, head_scan, n_rec + 1, st));
+  int64_t n_groups = 0;
+  LTSG_CUDA(cudaMemcpyAsync(&n_groups, head_scan + n_rec, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+  LTSG_CUDA(cudaStreamSynchronize(st));
+  LTSG_TRY(ws_get(ws, "g_off", (size_t)n_groups + 1, &g_off));
+  LTSG_TRY(ws_get(ws, "g_fused", (size_t)n_groups + 1, &g_fused));
+  LTSG_TRY(ws_get(ws, "g_dst", (size_t)n_groups + 1, &g_dst));
+  k_group_table<<<grid_for(n_rec, 256), 256, 0, st>>>(head, head_scan, n_rec, g_off);
+  LTSG_LAUNCHED();
+
+  Soa fs;  // fused, group-slotted
+  LTSG_TRY(ws_get(ws, "f_problem", n_rec, &fs.problem));
+  LTSG_TRY(ws_get(ws, "f_body_a", n_rec, &fs.body_a));
+  LTSG_TRY(ws_get(ws, "f_body_b", n_rec, &fs.body_b));
+  LTSG_TRY(ws_get(ws, "f_pos", 3 * n_rec, &fs.position));
+  LTSG_TRY(ws_get(ws, "f_nrm", 3 * n_rec, &fs.normal));
+  LTSG_TRY(ws_get(ws, "f_depth", n_rec, &fs.depth));
+  LTSG_TRY(ws_get(ws, "f_t", n_rec, &fs.t));
+  LTSG_TRY(ws_get(ws, "f_tri_a", n_rec, &fs.tri_a));
+  LTSG_TRY(ws_get(ws, "f_tri_b", n_rec, &fs.tri_b));
+  LTSG_TRY(ws_get(ws, "f_thr", n_rec, &fs.threshold));
+  int32_t *big_list, *big_count;
+  LTSG_TRY(ws_get(ws, "big_list", (size_t)n_groups, &big_list));
+  LTSG_TRY(ws_get(ws, "big_count", 1, &big_count));
+  LTSG_CUDA(cudaMemsetAsync(big_count, 0, sizeof(int32_t), st));
+  k_fuse_block<<<(int)std::min<int64_t>(n_groups, 148 * 8), kFuseThreads, 0, st>>>(
+      ro, idx, g_off, n_groups, n_rec, fs, g_fused, prob_count, big_list, big_count);
+  LTSG_LAUNCHED();
+  k_fuse_big<<<grid_for(n_groups, 32), 32, 0, st>>>(ro, idx, g_off, n_groups, n_rec, parent, fs, g_fused,
+                                                    prob_count, big_list, big_count);
+  LTSG_LAUNCHED();
+
+  // raw output in canonical order (group, then fusion key)
+  if (out->raw_t) {
+    Soa rr{out->raw_problem, out->raw_body_a, out->raw_body_b, out->raw_position, out->raw_normal,
+           out->raw_depth, out->raw_t, out->raw_tri_a, out->raw_tri_b, out->raw_threshold};
+    k_gather<<<grid_for(n_rec, 128), 128, 0, st>>>(ro, idx, n_rec, rr);
+    LTSG_LAUNCHED();
+  }
+  // dense fused output
+  LTSG_CUDA(cudaMemsetAsync(g_fused + n_groups, 0, sizeof(int64_t), st));
+  LTSG_TRY(scan_exclusive(ws, g_fused, g_dst, n_groups + 1, st));
+  Soa fo{out->problem, out->body_a, out->body_b, out->position, out->normal, out->depth, out->t,
+         out->tri_a, out->tri_b, out->threshold};
+  k_compact<<<(int)std::min<int64_t>(n_groups, 148 * 16), 64, 0, st>>>(fs, g_off, g_fused, g_dst, n_groups, fo);
+  LTSG_LAUNCHED();
+  k_widen<<<grid_for(np + 1, 256), 256, 0, st>>>(prob_count, prob_count64, np + 1);
+  LTSG_LAUNCHED();
+  LTSG_TRY(scan_exclusive(ws, prob_count64, out->fused_offset, np + 1, st));
+  LTSG_CUDA(cudaMemcpyAsync(&out->n_fused, g_dst + n_groups, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+  LTSG_CUDA(cudaStreamSynchronize(st));
+  return LTSG_OK;
+}
+
+static int run_allpairs(const ltsg_scene* sc, int64_t* rows, int64_t* hits, ltsg_workspace* ws,
+                        cudaStream_t st) {
+  LTSG_TRY(validate(sc));
+  Prepared pr{};
+  LTSG_TRY(prepare(sc, ws, st, &pr));
+  unsigned long long* d_hits;
+  LTSG_TRY(ws_get(ws, "hits", 1, &d_hits));
+  LTSG_CUDA(cudaMemsetAsync(d_hits, 0, sizeof(unsigned long long), st));
+  if (sc->n_pairs > 0) {
+    dim3 grid(148 * 4, (unsigned)std::min<int64_t>(sc->n_pairs, 65535));
+    k_allpairs<<<grid, 128, 0, st>>>(pr.pairs, sc->n_pairs, pr.bodies, sc->tris, d_hits);
+    LTSG_CHECK_LAUNCH();
+  }
+  unsigned long long h = 0;
+  LTSG_CUDA(cudaMemcpyAsync(&h, d_hits, sizeof(h), cudaMemcpyDeviceToHost, st));
+  LTSG_CUDA(cudaStreamSynchronize(st));
+  *hits = (int64_t)h;
+  *rows = -1;  // computed by the caller from the tree sizes
+  return LTSG_OK;
+}
+
+}  // namespace ltsg
+
+extern "C" int ltsg_search(const ltsg_scene* scene, ltsg_result* out, ltsg_workspace* ws, void* stream) {
+  if (!scene || !out || !ws) {
+    ltsg::set_error("ltsg_search: null argument");
+    return LTSG_EINVAL;
+  }
+  return ltsg::run_search(scene, out, ws, (cudaStream_t)stream);
+}
+
+extern "C" int ltsg_fuse_contacts(ltsg_result* io, int64_t n_raw, const uint64_t* group_key,
+                                  ltsg_workspace* ws, void* stream) {
+  using namespace ltsg;
+  if (!io || !ws || n_raw < 0 || (n_raw > 0 && (!group_key || !io->raw_t || !io->raw_problem))) {
+    set_error("ltsg_fuse_contacts: invalid arguments");
+    return LTSG_EINVAL;
+  }
+  cudaStream_t st = (cudaStream_t)stream;
+  // n_problems = 1 + max problem id, passed through io->n_raw on entry
+  const int np = (int)io->n_raw;
+  if (np < 1) {
+    set_error("ltsg_fuse_contacts: io->n_raw must carry the problem count (>= 1)");
+    return LTSG_EINVAL;
+  }
+  io->n_fused = 0;
+  if (n_raw > io->capacity) {
+    set_error("ltsg_fuse_contacts: capacity %lld < %lld", (long long)io->capacity, (long long)n_raw);
+    return LTSG_ECAPACITY;
+  }
+  int32_t* prob_count;
+  int64_t* prob_count64;
+  LTSG_TRY(ws_get(ws, "prob_count", (size_t)np + 1, &prob_count));
+  LTSG_TRY(ws_get(ws, "prob_count64", (size_t)np + 1, &prob_count64));
+  LTSG_CUDA(cudaMemsetAsync(prob_count, 0, sizeof(int32_t) * (np + 1), st));
+  io->n_raw = n_raw;
+  if (n_raw == 0) {
+    LTSG_CUDA(cudaMemsetAsync(io->fused_offset, 0, sizeof(int64_t) * (np + 1), st));
+    LTSG_CUDA(cudaStreamSynchronize(st));
+    return LTSG_OK;
+  }
+  Soa ro{io->raw_problem, io->raw_body_a, io->raw_body_b, io->raw_position, io->raw_normal,
+         io->raw_depth, io->raw_t, io->raw_tri_a, io->raw_tri_b, io->raw_threshold};
+  unsigned long long* key;
+  LTSG_TRY(ws_get(ws, "r_key", (size_t)n_raw, &key));
+  LTSG_CUDA(cudaMemcpyAsync(key, group_key, sizeof(uint64_t) * n_raw, cudaMemcpyDeviceToDevice, st));
+  // the raw arrays are inputs here: do not overwrite them with the canonical order
+  double* saved_raw_t = io->raw_t;
+  io->raw_t = nullptr;
+  const int rc = fuse_stage(ws, st, ro, key, n_raw, np, prob_count, prob_count64, io);
+  io->raw_t = saved_raw_t;
+  return rc;
+}
+
+extern "C" int ltsg_exhaustive_rows(const ltsg_scene* scene, int64_t* rows, int64_t* hits,
+                                    ltsg_workspace* ws, void* stream) {
+  if (!scene || !rows || !hits || !ws) {
+    ltsg::set_error("ltsg_exhaustive_rows: null argument");
+    return LTSG_EINVAL;
+  }
+  return ltsg::run_allpairs(scene, rows, hits, ws, (cudaStream_t)stream);
+}

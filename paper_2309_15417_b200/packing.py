@@ -1,0 +1,239 @@
+"""Host packer: reference-shaped inputs -> the device scene of ltsg_search.
+
+Layout in HBM (DESIGN.md §"Data layout"):
+
+* one float64 record of 12 slots (96 B, three 32-B sectors) per surrogate
+  triangle of every body and level: the 9 body-frame corners (corner-major),
+  epsilon, arm (largest corner norm, ccd._Motion.arm, ccd.py:108-114) and the
+  (int32 first child, int32 child count) pair in slot 11.  Levels of a tree
+  are re-ordered top-down so that a parent's children (the Morton groups of
+  surrogate.py:99-116) are one contiguous range of the finer level: the
+  traversal expands children with coalesced, index-free loads.  `tri_orig`
+  maps a record back to its index in the reference tree (contacts report it).
+* per body: the raw kinematic snapshot (ccd.py:98-106 reads exactly these);
+  rotation matrices, spin axes and |omega| are derived on the device with the
+  reference's rounding.
+* per pair: body slots, problem index and fusion-group rank.
+
+Packed trees are cached per tree object (trees are immutable after
+construction), so repeated calls only re-pack states.
+"""
+
+from __future__ import annotations
+
+import threading
+import weakref
+from dataclasses import dataclass
+
+import numpy as np
+
+MAX_LEVELS = 8
+RECORD = 12
+
+
+@dataclass
+class PackedTree:
+    records: np.ndarray      # (n, 12) float64
+    orig: np.ndarray         # (n,) int32
+    level_off: np.ndarray    # (L,) int64, record offset of each level within the tree
+    level_size: np.ndarray   # (L,) int64
+    max_children: int
+
+
+_cache_lock = threading.Lock()
+_cache: dict = {}
+
+
+def _tree_key(tree):
+    return id(tree)
+
+
+def pack_tree(tree) -> PackedTree:
+    """Pack one SurrogateTree (cached by identity while the tree lives)."""
+    key = _tree_key(tree)
+    with _cache_lock:
+        hit = _cache.get(key)
+        if hit is not None and hit[0]() is tree:
+            return hit[1]
+    packed = _pack_tree(tree)
+    try:
+        ref = weakref.ref(tree, lambda _r, k=key: _cache.pop(k, None))
+    except TypeError:
+        return packed
+    with _cache_lock:
+        _cache[key] = (ref, packed)
+    return packed
+
+
+def _pack_tree(tree) -> PackedTree:
+    levels = tree.levels
+    n_levels = len(levels)
+    if n_levels < 1:
+        raise ValueError("tree has no levels")
+    if n_levels > MAX_LEVELS:
+        raise ValueError(f"trees deeper than {MAX_LEVELS} levels are not supported")
+    # top-down order: perm[l] lists original indices of level l in packed order
+    perm = [None] * n_levels
+    top = n_levels - 1
+    perm[top] = np.arange(levels[top].size, dtype=np.int64)
+    first = [None] * n_levels
+    count = [None] * n_levels
+    max_children = 1
+    for lvl in range(top, 0, -1):
+        kids = levels[lvl].children
+        if kids is None:
+            raise ValueError(f"level {lvl} has no children")
+        lists = [np.asarray(kids[i], dtype=np.int64) for i in perm[lvl]]
+        cnt = np.array([len(k) for k in lists], dtype=np.int64)
+        max_children = max(max_children, int(cnt.max()) if len(cnt) else 1)
+        order = np.concatenate(lists) if lists else np.zeros(0, dtype=np.int64)
+        seen = np.zeros(levels[lvl - 1].size, dtype=bool)
+        seen[order] = True
+        if not seen.all():  # unreferenced finer triangles: unreachable, keep them anyway
+            order = np.concatenate([order, np.flatnonzero(~seen)])
+        perm[lvl - 1] = order
+        first[lvl] = np.concatenate([[0], np.cumsum(cnt)[:-1]]).astype(np.int64)
+        count[lvl] = cnt
+    sizes = np.array([len(p) for p in perm], dtype=np.int64)
+    offs = np.concatenate([[0], np.cumsum(sizes)[:-1]]).astype(np.int64)
+    recs = np.zeros((int(sizes.sum()), RECORD), dtype=np.float64)
+    orig = np.empty(int(sizes.sum()), dtype=np.int32)
+    for lvl in range(n_levels):
+        p = perm[lvl]
+        lv = levels[lvl]
+        corners = np.asarray(lv.corners, dtype=np.float64)[p]
+        sl = slice(offs[lvl], offs[lvl] + sizes[lvl])
+        recs[sl, 0:9] = corners.reshape(-1, 9)
+        recs[sl, 9] = np.asarray(lv.epsilon, dtype=np.float64)[p]
+        # ccd._Motion.arm: np.linalg.norm(corners, axis=2).max(axis=1)
+        recs[sl, 10] = np.linalg.norm(corners, axis=2).max(axis=1)
+        if lvl > 0:
+            ch = np.zeros(len(p), dtype=np.int64)
+            ch[: len(first[lvl])] = first[lvl]
+            cn = np.zeros(len(p), dtype=np.int64)
+            cn[: len(count[lvl])] = count[lvl]
+            pair = (ch.astype(np.uint32).astype(np.uint64)
+                    | (cn.astype(np.uint32).astype(np.uint64) << np.uint64(32)))
+            recs[sl, 11] = pair.view(np.float64)
+        orig[sl] = p.astype(np.int32)
+    return PackedTree(records=recs, orig=orig, level_off=offs, level_size=sizes,
+                      max_children=max_children)
+
+
+def body_id(body) -> int:
+    return int(body.pid) if hasattr(body, "timeline") else int(body.sid)
+
+
+@dataclass
+class HostScene:
+    """Packed scene in host (optionally pinned) memory."""
+    tris: np.ndarray
+    tri_orig: np.ndarray
+    body_state: np.ndarray
+    body_levels: np.ndarray
+    pair_body: np.ndarray
+    pair_problem: np.ndarray
+    pair_group: np.ndarray
+    problem_dt: np.ndarray
+    problem_tbase: np.ndarray
+    max_children: int
+    n_problems: int
+    body_ids: np.ndarray
+
+    def arrays(self):
+        return {k: getattr(self, k) for k in (
+            "tris", "tri_orig", "body_state", "body_levels", "pair_body", "pair_problem",
+            "pair_group", "problem_dt", "problem_tbase")}
+
+    @property
+    def nbytes(self) -> int:
+        return sum(a.nbytes for a in self.arrays().values())
+
+
+def body_state_row(body) -> np.ndarray:
+    row = np.zeros(16)
+    if hasattr(body, "timeline"):
+        s = body.timeline.current
+        row[0:3] = np.asarray(s.position, dtype=np.float64)
+        row[3:6] = np.asarray(s.velocity, dtype=np.float64)
+        row[6:10] = np.asarray(s.rotation, dtype=np.float64)
+        row[10:13] = np.asarray(s.angular_velocity, dtype=np.float64)
+    else:
+        row[13] = 1.0
+    return row
+
+
+def pack(problems) -> HostScene:
+    """Pack a batch of problems.
+
+    `problems` is a list of (pairs, dt, t_base) where each pair is a tuple of
+    two body objects.  A body object shared by several pairs or problems is
+    packed once.
+    """
+    slot_of = {}
+    bodies = []
+    pair_body = []
+    pair_problem = []
+    pair_group = []
+    dts = np.empty(len(problems))
+    tbs = np.empty(len(problems))
+    for pi, (pairs, dt, tb) in enumerate(problems):
+        dts[pi] = float(dt)
+        tbs[pi] = float(tb)
+        ids = []
+        for ba, bb in pairs:
+            for b in (ba, bb):
+                if id(b) not in slot_of:
+                    slot_of[id(b)] = len(bodies)
+                    bodies.append(b)
+            pair_body.append((slot_of[id(ba)], slot_of[id(bb)]))
+            pair_problem.append(pi)
+            ids.append((body_id(ba), body_id(bb)))
+        # fusion groups: distinct (body_a id, body_b id) in sorted order (ccd.py:539)
+        uniq = sorted(set(ids))
+        rank = {u: r for r, u in enumerate(uniq)}
+        pair_group.extend(rank[i] for i in ids)
+    return _assemble(bodies, pair_body, pair_problem, pair_group, dts, tbs)
+
+
+def _assemble(bodies, pair_body, pair_problem, pair_group, dts, tbs) -> HostScene:
+    trees = {}
+    order = []
+    for b in bodies:
+        k = id(b.tree)
+        if k not in trees:
+            trees[k] = pack_tree(b.tree)
+            order.append(k)
+    tree_off = {}
+    off = 0
+    for k in order:
+        tree_off[k] = off
+        off += len(trees[k].records)
+    tris = np.empty((off, RECORD), dtype=np.float64)
+    orig = np.empty(off, dtype=np.int32)
+    max_children = 1
+    for k in order:
+        pt = trees[k]
+        tris[tree_off[k]:tree_off[k] + len(pt.records)] = pt.records
+        orig[tree_off[k]:tree_off[k] + len(pt.records)] = pt.orig
+        max_children = max(max_children, pt.max_children)
+    n_b = len(bodies)
+    state = np.empty((n_b, 16))
+    lev = np.zeros((n_b, 18), dtype=np.int64)
+    ids = np.empty(n_b, dtype=np.int64)
+    for i, b in enumerate(bodies):
+        pt = trees[id(b.tree)]
+        state[i] = body_state_row(b)
+        L = len(pt.level_size)
+        lev[i, 0] = L
+        ids[i] = body_id(b)
+        lev[i, 1] = ids[i]
+        lev[i, 2:2 + L] = tree_off[id(b.tree)] + pt.level_off
+        lev[i, 10:10 + L] = pt.level_size
+    return HostScene(
+        tris=tris, tri_orig=orig, body_state=state, body_levels=lev,
+        pair_body=np.asarray(pair_body, dtype=np.int32).reshape(-1, 2),
+        pair_problem=np.asarray(pair_problem, dtype=np.int32),
+        pair_group=np.asarray(pair_group, dtype=np.int32),
+        problem_dt=np.asarray(dts, dtype=np.float64), problem_tbase=np.asarray(tbs, dtype=np.float64),
+        max_children=max_children, n_problems=len(dts), body_ids=ids)

@@ -1,0 +1,96 @@
+"""Host-side input construction and packing (no GPU)."""
+
+import numpy as np
+import pytest
+
+from helpers import golden
+from golden import scene_codec as SC
+from paper_2309_15417_b200 import bodies as B
+from paper_2309_15417_b200 import packing, scenes
+from paper_2309_15417_b200.surrogate import build_surrogate_tree
+
+
+@pytest.mark.parametrize("k", range(8))
+def test_tree_builder_matches_reference_trees(k):
+    case = golden("trees")["trees"][k]
+    v, f = case["vertices"], case["triangles"]
+    ref = SC.decode_tree(case["tree"])
+    corners = np.stack([v[f[:, 0]], v[f[:, 1]], v[f[:, 2]]], axis=1)
+    got = build_surrogate_tree(corners, case["epsilon"])
+    assert got.level_sizes() == ref.level_sizes()
+    for a, b in zip(got.levels, ref.levels):
+        # bit-exact on the build host; LAPACK may differ in the last bits elsewhere
+        np.testing.assert_allclose(a.corners, b.corners, rtol=1e-12, atol=1e-14)
+        np.testing.assert_allclose(a.epsilon, b.epsilon, rtol=1e-12, atol=1e-14)
+        if b.children is not None:
+            for ca, cb in zip(a.children, b.children):
+                np.testing.assert_array_equal(ca, cb)
+
+
+def test_icosphere_counts():
+    for s in range(4):
+        v, f = scenes.icosphere(s)
+        assert len(f) == 20 * 4 ** s
+        assert len(v) == 10 * 4 ** s + 2
+        np.testing.assert_allclose(np.linalg.norm(v, axis=1), 1.0)
+
+
+def _tree_of(n_sub=2):
+    v, f = scenes.icosphere(n_sub)
+    return build_surrogate_tree(np.stack([v[f[:, 0]], v[f[:, 1]], v[f[:, 2]]], 1), 0.01)
+
+
+def test_packed_children_are_contiguous_and_map_back():
+    tree = _tree_of(2)
+    pt = packing._pack_tree(tree)
+    L = len(tree.levels)
+    for lvl in range(1, L):
+        off, size = pt.level_off[lvl], pt.level_size[lvl]
+        fine_off = pt.level_off[lvl - 1]
+        for r in range(size):
+            rec = pt.records[off + r]
+            ch = rec[11:12].view(np.uint64)[0]
+            first, count = int(ch & np.uint64(0xFFFFFFFF)), int(ch >> np.uint64(32))
+            parent = pt.orig[off + r]
+            want = sorted(tree.levels[lvl].children[parent])
+            got = sorted(pt.orig[fine_off + first: fine_off + first + count])
+            assert got == want
+    for lvl in range(L):
+        off, size = pt.level_off[lvl], pt.level_size[lvl]
+        np.testing.assert_array_equal(pt.records[off:off + size, :9].reshape(-1, 3, 3),
+                                      tree.levels[lvl].corners[pt.orig[off:off + size]])
+        np.testing.assert_array_equal(pt.records[off:off + size, 9],
+                                      tree.levels[lvl].epsilon[pt.orig[off:off + size]])
+
+
+def test_pack_groups_and_shared_bodies():
+    tree = _tree_of(1)
+    a = B.Particle(0, tree, 0.01, 1.0, B.timeline(B.state((0, 0, 0))))
+    b = B.Particle(1, tree, 0.01, 1.0, B.timeline(B.state((2, 0, 0))))
+    c = B.Particle(2, tree, 0.01, 1.0, B.timeline(B.state((4, 0, 0))))
+    s = B.StaticBody(-1, tree, 0.01)
+    hs = packing.pack([([(a, b)], 0.0, 0.0), ([(b, c), (a, c), (c, s), (a, c)], 0.5, 1.0)])
+    assert len(hs.body_state) == 4          # shared objects packed once
+    assert len(hs.tris) == sum(l.size for l in tree.levels)  # one tree copy
+    assert hs.pair_problem.tolist() == [0, 1, 1, 1, 1]
+    # groups rank the distinct (id_a, id_b) pairs of each problem
+    assert hs.pair_group.tolist() == [0, 1, 0, 2, 0]
+    assert hs.body_state[3, 13] == 1.0 and hs.body_levels[3, 1] == -1
+
+
+def test_scenes_are_seeded():
+    s1 = scenes.config1(n_pairs=3, subdiv=1)
+    s2 = scenes.config1(n_pairs=3, subdiv=1)
+    for k in s1.particles:
+        np.testing.assert_array_equal(s1.particles[k].timeline.current.position,
+                                      s2.particles[k].timeline.current.position)
+        np.testing.assert_array_equal(s1.particles[k].tree.levels[0].corners,
+                                      s2.particles[k].tree.levels[0].corners)
+
+
+def test_domino_pairs_are_sphere_overlaps():
+    s = scenes.config2(n_boxes=40)
+    r = s.particles[0].radius
+    assert abs(r - (np.sqrt(0.05 ** 2 + 0.25 ** 2 + 0.5 ** 2) + 1e-3)) < 1e-12
+    assert all(0.18 * (b - a) <= 2 * r for a, b in s.pairs)
+    assert len(s.pairs) == sum(min(6, 39 - i) for i in range(40))
