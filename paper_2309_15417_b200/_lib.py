@@ -12,7 +12,7 @@ import os
 import threading
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libltsgpu.so")
+LIB_PATH = os.environ.get("LTSG_LIB") or os.path.join(_HERE, "libltsgpu.so")
 
 LTSG_OK, LTSG_EINVAL, LTSG_ECUDA, LTSG_ECAPACITY = 0, 1, 2, 3
 

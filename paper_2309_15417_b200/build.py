@@ -49,14 +49,15 @@ def _stale() -> bool:
     return any(os.path.getmtime(d) > t for d in deps)
 
 
-def build(force: bool = False, verbose: bool = False, extra=()) -> str:
-    if not force and not _stale():
+def build(force: bool = False, verbose: bool = False, extra=(), out: str | None = None) -> str:
+    lib = out or LIB
+    if out is None and not force and not _stale():
         return LIB
     objs = []
     nvcc = nvcc_path()
-    tmp = LIB + ".tmp"
+    tmp = lib + ".tmp"
     for src in SOURCES:
-        obj = os.path.join(CSRC, src.replace(".cu", ".o"))
+        obj = os.path.join(CSRC, src.replace(".cu", f".{os.getpid()}.o"))
         cmd = [nvcc, *NVCC_FLAGS, *extra, "-I", os.path.join(REPO, "include"), "-c",
                os.path.join(CSRC, src), "-o", obj]
         if verbose:
@@ -67,18 +68,21 @@ def build(force: bool = False, verbose: bool = False, extra=()) -> str:
     cmd = [nvcc, "-gencode", "arch=compute_100a,code=sm_100a", "-shared", "-Xcompiler", "-fPIC",
            *objs, "-o", tmp]
     subprocess.run(cmd, check=True)
-    os.replace(tmp, LIB)
+    os.replace(tmp, lib)
     for obj in objs:
         os.remove(obj)
-    return LIB
+    return lib
 
 
 def main(argv=None) -> int:
     ap = argparse.ArgumentParser()
     ap.add_argument("--force", action="store_true")
     ap.add_argument("--verbose", action="store_true")
+    ap.add_argument("--out", default=None, help="build a variant library to this path")
+    ap.add_argument("-D", dest="defines", action="append", default=[], help="extra -D for nvcc")
     args = ap.parse_args(argv)
-    print(build(force=args.force, verbose=args.verbose))
+    print(build(force=args.force, verbose=args.verbose, extra=[f"-D{d}" for d in args.defines],
+                out=args.out))
     return 0
 
 

@@ -1,20 +1,24 @@
 // The 15-feature triangle-pair distance over shared-memory-staged triangles.
 //
 // Same arithmetic as geom.cuh's feature_dist (bit-identical results), laid
-// out for throughput on sm_100a:
+// out for FP64 throughput on sm_100a:
 //  * the two world triangles, their edge vectors and squared edge lengths are
 //    staged once per row in shared memory, structure-of-arrays across the
-//    block's threads (element k of thread t at s[k * stride + t], so a warp's
-//    accesses are conflict-free), and computed once instead of once per
-//    feature;
+//    block (element k of thread t at s[k * kStride + t]: conflict-free, and
+//    with a compile-time stride every access is an immediate-offset LDS);
 //  * the six point-triangle and nine segment-segment features run as two
-//    compact loops (not unrolled): one copy of each feature's code keeps the
-//    kernel inside the instruction cache;
-//  * divisions are skipped wherever their rounded quotient cannot change the
-//    result: a clamped parameter whose numerator lies outside (0, den) is
-//    exactly 0 or 1 after the clamp, and t > 1 is decided exactly without
-//    dividing (see seg_param below).  Both choices are proven per case in
-//    the comments and checked bit-for-bit against the reference's rows.
+//    compact loops -- one copy of each feature's code stays in the
+//    instruction cache;
+//  * each feature is branch-free: the Voronoi region (point-triangle) and the
+//    clamp case (segment-segment) only select operands, and every lane runs
+//    the same instruction stream; divisions are predicated on the lanes that
+//    need them;
+//  * divisions are skipped wherever their rounded quotient cannot matter:
+//    np.clip(num / den, 0, 1) with den > 0 is exactly 0 for num <= 0 and
+//    exactly 1 for num >= den; t > 1 is decided exactly without dividing;
+//  * comparisons against zero and the running minimum use integer compares
+//    on the IEEE bit patterns (exact for the finite values that occur), which
+//    keeps them off the FP64 pipe.
 #pragma once
 
 #include "geom.cuh"
@@ -26,10 +30,10 @@ namespace ltsg {
 constexpr int kStA = 0, kStB = 9, kStEA = 18, kStEB = 27, kStAA = 36, kStBB = 39;
 constexpr int kStaged = 42;
 
+template <int kStride>
 struct Staged {
   double* s;
-  int stride;
-  __device__ __forceinline__ double& at(int k) const { return s[k * stride]; }
+  __device__ __forceinline__ double& at(int k) const { return s[k * kStride]; }
   __device__ __forceinline__ V3 v3(int k) const { return V3{at(k), at(k + 1), at(k + 2)}; }
   __device__ __forceinline__ void put(int k, V3 v) const {
     at(k) = v.x;
@@ -38,9 +42,26 @@ struct Staged {
   }
 };
 
-// Stage triangles a, b: corners, edges e_k = v[k+1] - v[k] and |e_k|^2 in
-// dot_simd order (the reference computes both per feature; same values).
-__device__ __forceinline__ void stage_pair(const Staged& st, const Tri& a, const Tri& b) {
+// Exact comparisons with zero through the bit pattern (finite x):
+// x <= 0.0 holds for -0.0 (INT64_MIN) and every negative; x >= 0.0 for +0.0,
+// -0.0 and every positive; x < 0.0 for negatives except -0.0.
+__device__ __forceinline__ bool le0(double x) { return __double_as_longlong(x) <= 0; }
+__device__ __forceinline__ bool ge0(double x) {
+  const long long b = __double_as_longlong(x);
+  return b >= 0 || b == (long long)0x8000000000000000ULL;
+}
+__device__ __forceinline__ bool lt0(double x) {
+  const long long b = __double_as_longlong(x);
+  return b < 0 && b != (long long)0x8000000000000000ULL;
+}
+// min of two non-negative doubles (squared distances) by their bit patterns
+__device__ __forceinline__ double min_nonneg(double a, double b) {
+  const unsigned long long x = __double_as_longlong(a), y = __double_as_longlong(b);
+  return __longlong_as_double(x < y ? x : y);
+}
+
+template <int kStride>
+__device__ __forceinline__ void stage_pair(const Staged<kStride>& st, const Tri& a, const Tri& b) {
 #pragma unroll
   for (int k = 0; k < 3; ++k) {
     st.put(kStA + 3 * k, a.v[k]);
@@ -57,111 +78,127 @@ __device__ __forceinline__ void stage_pair(const Staged& st, const Tri& a, const
   }
 }
 
-// clip01(num / den) for den > 0, as np.clip(_safe_div(num, den), 0, 1):
-// num <= 0 gives a quotient <= 0 (or -0) which clips to +0; num >= den gives
-// a quotient >= 1 which clips to 1; only 0 < num < den needs the division.
-// Requires den > 1e-300 so that _safe_div divides by den itself.
+// np.clip(num / den, 0, 1) for den > 1e-300 (so _safe_div divides by den):
+// a non-positive numerator gives a quotient <= 0 (or -0) that clips to +0, a
+// numerator >= den gives a quotient >= 1 that clips to 1, so only
+// 0 < num < den divides.
 __device__ __forceinline__ double clip_quot(double num, double den) {
-  if (!(num > 0.0)) return num != num ? num : 0.0;
-  if (num >= den) return 1.0;
-  return dv(num, den);
+  double q = 0.0;
+  if (num > 0.0 && num < den) q = dv(num, den);
+  else if (num >= den) q = 1.0;
+  return q;
 }
 
-// Squared distance of segments (kernels.py:78-115) with the division
-// shortcuts.  u, w edge vectors; uu, ww their squared lengths.
-__device__ __forceinline__ double seg_sq_fast(V3 p1, V3 u, double uu, V3 p2, V3 w, double ww) {
-  const bool u_ok = uu > kTiny, w_ok = ww > kTiny;
-  if (!u_ok || !w_ok) return segment_segment_sq<false>(p1, u, uu, p2, w, ww);
+// Squared point-triangle distance (kernels.py:23-75), branch-free.
+// ab = e0, ac = -e2 (exact negation of v0 - v2), bc = e1.  The closest point
+// is q = (P + D1*s1) + D2*s2: vertex regions use s1 = s2 = 0 (q == P up to
+// the sign of zeros, which squaring removes), edges s2 = 0.
+__device__ __forceinline__ double pt_sq_uniform(V3 p, V3 a, V3 b, V3 c, V3 ab, V3 ac, V3 bc) {
+  const V3 ap = p - a, bp = p - b, cp = p - c;
+  const double d1 = dot_simd(ab, ap), d2 = dot_simd(ac, ap);
+  const double d3 = dot_simd(ab, bp), d4 = dot_simd(ac, bp);
+  const double d5 = dot_simd(ab, cp), d6 = dot_simd(ac, cp);
+  const double vc = sub(mul(d1, d4), mul(d3, d2));
+  const double vb = sub(mul(d5, d2), mul(d1, d6));
+  const double va = sub(mul(d3, d6), mul(d5, d4));
+  const double e43 = sub(d4, d3), e56 = sub(d5, d6);
+  const bool in_a = le0(d1) && le0(d2);
+  const bool in_b = ge0(d3) && d4 <= d3;
+  const bool in_c = ge0(d6) && d5 <= d6;
+  const bool on_ab = le0(vc) && ge0(d1) && le0(d3);
+  const bool on_ac = le0(vb) && ge0(d2) && le0(d6);
+  const bool on_bc = le0(va) && ge0(e43) && ge0(e56);
+  const bool vertex = in_a || in_b || in_c;
+  // operand selection in reverse priority order (later overrides earlier)
+  const double den = add(add(va, vb), vc);
+  double n1 = vb, m1 = den;  // face
+  V3 P = a, D1 = ab;
+  bool face = true;
+  if (on_bc) { n1 = e43; m1 = add(e43, e56); P = b; D1 = bc; face = false; }
+  if (on_ac) { n1 = d2; m1 = sub(d2, d6); P = a; D1 = ac; face = false; }
+  if (on_ab) { n1 = d1; m1 = sub(d1, d3); P = a; D1 = ab; face = false; }
+  if (vertex) { P = in_a ? a : (in_b ? b : c); face = false; }
+  double s1 = 0.0, s2 = 0.0;
+  if (!vertex) s1 = sdiv(n1, m1);
+  if (face) s2 = sdiv(vc, den);
+  const V3 q = (P + scale(D1, s1)) + scale(ac, s2);
+  return sqn(p - q);
+}
+
+// Squared distance of segments [p1, p1+u], [p2, p2+w] (kernels.py:78-115),
+// branch-free; uu = |u|^2, ww = |w|^2 (dot_simd order).
+__device__ __forceinline__ double ss_sq_uniform(V3 p1, V3 u, double uu, V3 p2, V3 w, double ww) {
+  if (!(uu > 1e-280) || !(ww > 1e-280)) return segment_segment_sq<false>(p1, u, uu, p2, w, ww);
   const V3 r = p1 - p2;
   const double wr = dot_simd(w, r);
   const double ur = dot_simd(u, r);
   const double uw = dot_simd(u, w);
   const double det = sub(mul(uu, ww), mul(uw, uw));
-  double s = 0.0;
-  // det > thr > 0 there, so _safe_div divides by det
-  if (det > add(mul(mul(1e-14, uu), ww), kTiny)) s = clip_quot(sub(mul(uw, wr), mul(ur, ww)), det);
-  const double tn = add(mul(uw, s), wr);
-  double t;
-  if (tn < 0.0) {  // t < 0: re-clamp s from -ur/uu, t clips to 0
-    s = clip_quot(-ur, uu);
-    t = 0.0;
-  } else {
-    // t > 1 exactly when RN(tn/ww) > 1, i.e. tn/ww > 1 + 2^-53 (ties round to
-    // the even 1.0).  For ww < tn < 2ww, tn - ww is exact (Sterbenz) and
-    // ww * 2^-53 is exact, so the comparison is exact.
-    bool above;
-    if (!(tn > ww)) above = false;
-    else if (tn >= mul(2.0, ww)) above = true;
-    else above = sub(tn, ww) > mul(ww, 0x1p-53);
-    if (above) {
-      s = clip_quot(sub(uw, ur), uu);
-      t = 1.0;
-    } else {
-      t = tn == 0.0 ? 0.0 : clip01(dv(tn, ww));
-    }
-  }
-  const V3 q1 = p1 + scale(u, s);
-  const V3 q2 = p2 + scale(w, t);
-  return sqn(q1 - q2);
+  // parallel rows (det <= 1e-14*uu*ww + tiny) take s = 0 (kernels.py:99-100)
+  const bool nonpar = det > add(mul(mul(1e-14, uu), ww), kTiny);
+  const double s0 = nonpar ? clip_quot(sub(mul(uw, wr), mul(ur, ww)), det) : 0.0;
+  const double tn = add(mul(uw, s0), wr);
+  // t = tn/ww; t < 0 iff tn < 0; t > 1 iff tn/ww > 1 + 2^-53 (RN ties to the
+  // even 1.0), decided exactly: for ww < tn < 2ww, tn - ww is exact
+  // (Sterbenz) and ww*2^-53 is exact (ww > 1e-280).
+  const bool neg = lt0(tn);
+  const bool above = tn > ww && (tn >= mul(2.0, ww) || sub(tn, ww) > mul(ww, 0x1p-53));
+  // second quotient: re-clamped s (t outside [0,1]) or t itself
+  double n2 = tn, m2 = ww;
+  if (neg) { n2 = -ur; m2 = uu; }
+  if (above) { n2 = sub(uw, ur); m2 = uu; }
+  const double q2 = clip_quot(n2, m2);
+  const bool clamp_t = neg || above;
+  const double s = clamp_t ? q2 : s0;
+  const double t = clamp_t ? (above ? 1.0 : 0.0) : q2;
+  return sqn((p1 + scale(u, s)) - (p2 + scale(w, t)));
 }
 
-// Squared point-triangle distance (kernels.py:23-75), edges from the stage:
-// ab = e0, ac = -e2 (exact negation of v0 - v2), bc = e1.
-__device__ __forceinline__ double pt_sq_fast(V3 p, V3 a, V3 b, V3 c, V3 ab, V3 ac, V3 bc) {
-  const V3 ap = p - a;
-  const double d1 = dot_simd(ab, ap);
-  const double d2 = dot_simd(ac, ap);
-  if (d1 <= 0.0 && d2 <= 0.0) return sqn(ap);
-  const V3 bp = p - b;
-  const double d3 = dot_simd(ab, bp);
-  const double d4 = dot_simd(ac, bp);
-  if (d3 >= 0.0 && d4 <= d3) return sqn(bp);
-  const V3 cp = p - c;
-  const double d5 = dot_simd(ab, cp);
-  const double d6 = dot_simd(ac, cp);
-  if (d6 >= 0.0 && d5 <= d6) return sqn(cp);
-  const double vc = sub(mul(d1, d4), mul(d3, d2));
-  V3 q;
-  if (vc <= 0.0 && d1 >= 0.0 && d3 <= 0.0) {
-    q = a + scale(ab, sdiv(d1, sub(d1, d3)));
-  } else {
-    const double vb = sub(mul(d5, d2), mul(d1, d6));
-    if (vb <= 0.0 && d2 >= 0.0 && d6 <= 0.0) {
-      q = a + scale(ac, sdiv(d2, sub(d2, d6)));
-    } else {
-      const double va = sub(mul(d3, d6), mul(d5, d4));
-      const double e43 = sub(d4, d3);
-      const double e56 = sub(d5, d6);
-      if (va <= 0.0 && e43 >= 0.0 && e56 >= 0.0) {
-        q = b + scale(bc, sdiv(e43, add(e43, e56)));
-      } else {
-        const double den = add(add(va, vb), vc);
-        q = (a + scale(ab, sdiv(vb, den))) + scale(ac, sdiv(vc, den));
-      }
-    }
-  }
-  return sqn(p - q);
-}
+// Minimum squared 15-feature distance of the staged pair (ccd.py:135-153).
+// Each loop iteration carries two (point-triangle) or three (segment-segment)
+// independent features so the scheduler can overlap their FP64 latencies.
+#ifndef LTSG_ILP
+#define LTSG_ILP 0
+#endif
 
-// Minimum squared 15-feature distance of the staged pair.
-__device__ __forceinline__ double staged_dist_sq(const Staged& st) {
+template <int kStride>
+__device__ __forceinline__ double staged_dist_sq(const Staged<kStride>& st) {
   double best = __longlong_as_double(0x7ff0000000000000LL);
+#if LTSG_ILP
+#pragma unroll 1
+  for (int q = 0; q < 3; ++q) {
+    // vertex q of A against triangle B, vertex q of B against triangle A
+    const double da = pt_sq_uniform(st.v3(kStA + 3 * q), st.v3(kStB), st.v3(kStB + 3), st.v3(kStB + 6),
+                                    st.v3(kStEB), neg(st.v3(kStEB + 6)), st.v3(kStEB + 3));
+    const double db = pt_sq_uniform(st.v3(kStB + 3 * q), st.v3(kStA), st.v3(kStA + 3), st.v3(kStA + 6),
+                                    st.v3(kStEA), neg(st.v3(kStEA + 6)), st.v3(kStEA + 3));
+    best = min_nonneg(best, min_nonneg(da, db));
+  }
+#pragma unroll 1
+  for (int i = 0; i < 3; ++i) {
+    const V3 p1 = st.v3(kStA + 3 * i), u = st.v3(kStEA + 3 * i);
+    const double uu = st.at(kStAA + i);
+    const double d0 = ss_sq_uniform(p1, u, uu, st.v3(kStB), st.v3(kStEB), st.at(kStBB));
+    const double d1 = ss_sq_uniform(p1, u, uu, st.v3(kStB + 3), st.v3(kStEB + 3), st.at(kStBB + 1));
+    const double d2 = ss_sq_uniform(p1, u, uu, st.v3(kStB + 6), st.v3(kStEB + 6), st.at(kStBB + 2));
+    best = min_nonneg(best, min_nonneg(d0, min_nonneg(d1, d2)));
+  }
+#else
 #pragma unroll 1
   for (int q = 0; q < 6; ++q) {
     const int pbase = q < 3 ? kStA + 3 * q : kStB + 3 * (q - 3);
     const int tbase = q < 3 ? kStB : kStA;
     const int ebase = q < 3 ? kStEB : kStEA;
-    const V3 p = st.v3(pbase);
-    const V3 a = st.v3(tbase), b = st.v3(tbase + 3), c = st.v3(tbase + 6);
-    const V3 ab = st.v3(ebase), bc = st.v3(ebase + 3), ac = neg(st.v3(ebase + 6));
-    best = fmin(best, pt_sq_fast(p, a, b, c, ab, ac, bc));
+    best = min_nonneg(best, pt_sq_uniform(st.v3(pbase), st.v3(tbase), st.v3(tbase + 3), st.v3(tbase + 6),
+                                          st.v3(ebase), neg(st.v3(ebase + 6)), st.v3(ebase + 3)));
   }
 #pragma unroll 1
   for (int f = 0; f < 9; ++f) {
     const int i = f / 3, j = f - 3 * (f / 3);
-    best = fmin(best, seg_sq_fast(st.v3(kStA + 3 * i), st.v3(kStEA + 3 * i), st.at(kStAA + i),
-                                  st.v3(kStB + 3 * j), st.v3(kStEB + 3 * j), st.at(kStBB + j)));
+    best = min_nonneg(best, ss_sq_uniform(st.v3(kStA + 3 * i), st.v3(kStEA + 3 * i), st.at(kStAA + i),
+                                          st.v3(kStB + 3 * j), st.v3(kStEB + 3 * j), st.at(kStBB + j)));
   }
+#endif
   return best;
 }
 

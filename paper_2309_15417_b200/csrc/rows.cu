@@ -61,10 +61,10 @@ __global__ void k_segment_segment(const double* p1, const double* q1, const doub
   }
 }
 
-__global__ void __launch_bounds__(128) k_feature_distances(const double* ta, const double* tb, int64_t n,
+__global__ void __launch_bounds__(128, 4) k_feature_distances(const double* ta, const double* tb, int64_t n,
                                                            double* dist) {
   __shared__ double s_stage[kStaged * 128];
-  const Staged st{s_stage + threadIdx.x, 128};
+  const Staged<128> st{s_stage + threadIdx.x};
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
        i += (int64_t)gridDim.x * blockDim.x) {
     stage_pair(st, ldtri(ta, i), ldtri(tb, i));

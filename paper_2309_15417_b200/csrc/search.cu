@@ -222,7 +222,8 @@ __device__ __forceinline__ Tri world_at(const Motion& m, const double* r, double
   return world_tri(R, pos, L);
 }
 
-__device__ __forceinline__ double row_distance(const Staged& st, const double* tris, const BodyInfo& A,
+template <int kStride>
+__device__ __forceinline__ double row_distance(const Staged<kStride>& st, const double* tris, const BodyInfo& A,
                                                const BodyInfo& B, int la, int ia, int lb, int ib,
                                                double tau) {
   stage_pair(st, world_at(A.m, rec(tris, A, la, ia), tau), world_at(B.m, rec(tris, B, lb, ib), tau));
@@ -254,6 +255,9 @@ struct ScreenOut {
 };
 
 constexpr int kScreenWarps = 2;
+#ifndef LTSG_SCREEN_MINB
+#define LTSG_SCREEN_MINB 8
+#endif
 constexpr int kRowsPerWarp = 32 * kMaxSamples;
 
 __device__ __forceinline__ int sample_count(double span, double speed, double h) {
@@ -285,7 +289,7 @@ __device__ __forceinline__ int warp_incl_scan(int v, int lane) {
 // [w0, dt] (ccd.py:321-370) and decided (ccd.py:404-446).  A warp owns 32
 // consecutive candidates; their 1..33 samples are flattened into rows and
 // spread over the 32 lanes, so lanes stay busy whatever the sample counts.
-__global__ void __launch_bounds__(32 * kScreenWarps)
+__global__ void __launch_bounds__(32 * kScreenWarps, LTSG_SCREEN_MINB)
 k_screen(const Cand* __restrict__ front, int64_t n, const PairInfo* __restrict__ pairs,
          const BodyInfo* __restrict__ bodies, const double* __restrict__ tris, ScreenOut out) {
   __shared__ union {  // per warp: candidate info, later reused for child descriptors
@@ -294,7 +298,7 @@ k_screen(const Cand* __restrict__ front, int64_t n, const PairInfo* __restrict__
   } s_u[kScreenWarps];
   __shared__ uint8_t s_bits[kScreenWarps][kRowsPerWarp];
   extern __shared__ double s_stage[];  // kStaged x (32 * kScreenWarps), dynamic
-  const Staged st{s_stage + threadIdx.x, 32 * kScreenWarps};
+  const Staged<32 * kScreenWarps> st{s_stage + threadIdx.x};
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
   const int64_t n_warps = (n + 31) / 32;
@@ -470,7 +474,7 @@ k_zoom(const Entry* __restrict__ entries, int64_t n, const PairInfo* __restrict_
        Interval* __restrict__ queue, Bracket* brackets, Counters* ctr) {
   __shared__ double s_grid[kZoomWarps][kZoomSamples + 1];
   __shared__ double s_stage[kStaged * 32 * kZoomWarps];
-  const Staged st{s_stage + threadIdx.x, 32 * kZoomWarps};
+  const Staged<32 * kZoomWarps> st{s_stage + threadIdx.x};
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
   const int64_t gw = blockIdx.x * (int64_t)kZoomWarps + warp;
@@ -558,7 +562,7 @@ __global__ void k_bisect(const Bracket* __restrict__ br, int64_t n, const PairIn
                          const BodyInfo* __restrict__ bodies, const double* __restrict__ tris,
                          Cross* cross, unsigned long long cross_base, unsigned long long* tau_min_bits) {
   __shared__ double s_stage[kStaged * 64];
-  const Staged st{s_stage + threadIdx.x, 64};
+  const Staged<64> st{s_stage + threadIdx.x};
   const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (i >= n) return;
   const Bracket b = br[i];
@@ -718,103 +722,6 @@ __device__ __forceinline__ bool key_less(const Soa& o, int64_t a, int64_t b) {
   return o.tri_b[a] < o.tri_b[b];
 }
 
-// filter_contacts for one (problem, body pair) group per thread: canonical
-// stable sort, union-find over points within max(threshold), merge
-// (ccd.py:540-576).  Fused results land in the group's own slot range.
-__global__ void k_fuse_big(Soa o, int64_t* idx, const int64_t* g_off, int64_t n_groups, int64_t n_total,
-                           int32_t* parent, Soa f, int64_t* g_fused, int32_t* prob_count,
-                           const int32_t* big_list, const int32_t* big_count) {
-  const int64_t bi = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (bi >= *big_count) return;
-  const int64_t g = big_list[bi];
-  const int64_t off = g_off[g];
-  const int64_t n = (g + 1 < n_groups ? g_off[g + 1] : n_total) - off;
-  int64_t* ix = idx + off;
-  int32_t* par = parent + off;
-  for (int64_t i = 1; i < n; ++i) {
-    const int64_t v = ix[i];
-    int64_t j = i - 1;
-    while (j >= 0 && key_less(o, v, ix[j])) {
-      ix[j + 1] = ix[j];
-      --j;
-    }
-    ix[j + 1] = v;
-  }
-  for (int64_t i = 0; i < n; ++i) par[i] = (int32_t)i;
-  auto find = [&](int32_t i) {
-    while (par[i] != i) i = par[i];
-    return i;
-  };
-  for (int64_t i = 0; i < n; ++i) {
-    const int64_t a = ix[i];
-    const V3 pa{o.position[3 * a], o.position[3 * a + 1], o.position[3 * a + 2]};
-    for (int64_t j = i + 1; j < n; ++j) {
-      const int64_t b = ix[j];
-      const double rad = fmax(o.threshold[a], o.threshold[b]);
-      const V3 pb{o.position[3 * b], o.position[3 * b + 1], o.position[3 * b + 2]};
-      if (norm_blas(pa - pb) <= rad) par[find((int32_t)j)] = find((int32_t)i);
-    }
-  }
-  for (int64_t i = 0; i < n; ++i) par[i] = find((int32_t)i);
-  int64_t nf = 0;
-  for (int64_t r = 0; r < n; ++r) {
-    if (par[r] != r) continue;
-    V3 ps{0, 0, 0}, ns{0, 0, 0};
-    int64_t cnt = 0, rep = -1, first = -1;
-    double dmax = 0.0, tmin = 0.0, thr = 0.0;
-    // members in ascending sorted index; a root need not be its smallest member
-    for (int64_t i = 0; i < n; ++i) {
-      if (par[i] != r) continue;
-      const int64_t a = ix[i];
-      const V3 pp{o.position[3 * a], o.position[3 * a + 1], o.position[3 * a + 2]};
-      const V3 nn{o.normal[3 * a], o.normal[3 * a + 1], o.normal[3 * a + 2]};
-      if (cnt == 0) {
-        first = a;
-        ps = pp;
-        ns = nn;
-        dmax = o.depth[a];
-        tmin = o.t[a];
-        thr = o.threshold[a];
-        rep = a;
-      } else {
-        ps = ps + pp;  // np.mean / np.sum over axis 0: sequential
-        ns = ns + nn;
-        if (o.depth[a] > dmax) dmax = o.depth[a];
-        if (o.t[a] < tmin) tmin = o.t[a];
-        if (o.threshold[a] > thr) thr = o.threshold[a];
-        if (o.t[a] < o.t[rep] || (o.t[a] == o.t[rep] && -o.depth[a] < -o.depth[rep])) rep = a;
-      }
-      ++cnt;
-    }
-    const double c = (double)cnt;
-    const V3 pos{dv(ps.x, c), dv(ps.y, c), dv(ps.z, c)};
-    const double ln = norm_blas(ns);
-    V3 nrm;
-    if (ln > 1e-12) {
-      nrm = V3{dv(ns.x, ln), dv(ns.y, ln), dv(ns.z, ln)};
-    } else {
-      nrm = V3{o.normal[3 * first], o.normal[3 * first + 1], o.normal[3 * first + 2]};
-    }
-    const int64_t dst = off + nf;
-    f.problem[dst] = o.problem[rep];
-    f.body_a[dst] = o.body_a[rep];
-    f.body_b[dst] = o.body_b[rep];
-    f.position[3 * dst] = pos.x;
-    f.position[3 * dst + 1] = pos.y;
-    f.position[3 * dst + 2] = pos.z;
-    f.normal[3 * dst] = nrm.x;
-    f.normal[3 * dst + 1] = nrm.y;
-    f.normal[3 * dst + 2] = nrm.z;
-    f.depth[dst] = dmax;
-    f.t[dst] = tmin;
-    f.tri_a[dst] = o.tri_a[rep];
-    f.tri_b[dst] = o.tri_b[rep];
-    f.threshold[dst] = thr;
-    ++nf;
-  }
-  g_fused[g] = nf;
-  if (n > 0) atomicAdd(prob_count + o.problem[ix[0]], (int32_t)nf);
-}
 
 
 // filter_contacts, one block per (problem, body pair) group of at most
@@ -822,7 +729,7 @@ __global__ void k_fuse_big(Soa o, int64_t* idx, const int64_t* g_off, int64_t n_
 // once, the stable sort is a parallel rank sort, the "within max(threshold)"
 // adjacency is a bit matrix built by all threads, and one thread replays the
 // reference's union-find over it (ccd.py:543-555) so roots -- and therefore
-// the output order -- are identical.  Larger groups go to k_fuse_big.
+// the output order -- are identical.  Larger groups go to k_fuse_large.
 constexpr int kFuseCap = 256;
 constexpr int kFuseWords = kFuseCap / 32;
 constexpr int kFuseThreads = 128;
@@ -997,6 +904,157 @@ k_fuse_block(Soa o, int64_t* __restrict__ idx, const int64_t* __restrict__ g_off
   }
 }
 
+// Groups larger than kFuseCap: one 512-thread block per group, the same
+// steps as k_fuse_block with the per-record arrays and the adjacency bit
+// matrix in global scratch (records stay in their group's slot range).
+constexpr int kFuseLargeThreads = 512;
+
+__global__ void __launch_bounds__(kFuseLargeThreads)
+k_fuse_large(Soa o, int64_t* __restrict__ idx, const int64_t* __restrict__ g_off, int64_t n_groups,
+             int64_t n_total, Soa f, int64_t* g_fused, int32_t* prob_count, const int32_t* big_list,
+             const int64_t* adj_off, FuseKey* key, int64_t* gi, double* pos, double* thrs, int32_t* par,
+             int32_t* slot, uint32_t* adj_all) {
+  __shared__ int32_t s_nroots;
+  const int tid = threadIdx.x;
+  const int64_t g = big_list[blockIdx.x];
+  const int64_t off = g_off[g];
+  const int n = (int)((g + 1 < n_groups ? g_off[g + 1] : n_total) - off);
+  int64_t* ix = idx + off;
+  FuseKey* k_ = key + off;
+  int64_t* gi_ = gi + off;
+  double* px = pos + 3 * off;
+  double* th = thrs + off;
+  int32_t* pr = par + off;
+  int32_t* sl = slot + off;
+  const int words = (n + 31) / 32;
+  uint32_t* adj = adj_all + adj_off[blockIdx.x];
+  for (int i = tid; i < n; i += kFuseLargeThreads) {
+    const int64_t a = ix[i];
+    FuseKey k;
+    k.t = o.t[a];
+    k.r0 = round9(o.position[3 * a]);
+    k.r1 = round9(o.position[3 * a + 1]);
+    k.r2 = round9(o.position[3 * a + 2]);
+    k.ta = o.tri_a[a];
+    k.tb = o.tri_b[a];
+    k_[i] = k;
+  }
+  __syncthreads();
+  for (int i = tid; i < n; i += kFuseLargeThreads) {
+    const FuseKey ki = k_[i];
+    int rank = 0;
+    for (int j = 0; j < n; ++j) {
+      const FuseKey kj = k_[j];
+      rank += (fkey_less(kj, ki) || (j < i && !fkey_less(ki, kj))) ? 1 : 0;
+    }
+    const int64_t a = ix[i];
+    gi_[rank] = a;
+    px[3 * rank] = o.position[3 * a];
+    px[3 * rank + 1] = o.position[3 * a + 1];
+    px[3 * rank + 2] = o.position[3 * a + 2];
+    th[rank] = o.threshold[a];
+  }
+  __syncthreads();
+  for (int r = tid; r < n; r += kFuseLargeThreads) ix[r] = gi_[r];
+  for (int w = tid; w < n * words; w += kFuseLargeThreads) {
+    const int row = w / words, word = w % words;
+    const V3 pi{px[3 * row], px[3 * row + 1], px[3 * row + 2]};
+    const double ti = th[row];
+    uint32_t bits = 0;
+    for (int b = 0; b < 32; ++b) {
+      const int j = word * 32 + b;
+      if (j <= row || j >= n) continue;
+      const V3 pj{px[3 * j], px[3 * j + 1], px[3 * j + 2]};
+      if (norm_blas(pi - pj) <= fmax(ti, th[j])) bits |= 1u << b;
+    }
+    adj[(int64_t)row * words + word] = bits;
+  }
+  __syncthreads();
+  if (tid == 0) {
+    for (int i = 0; i < n; ++i) pr[i] = i;
+    auto find = [&](int x) {  // path halving, as the reference's find (ccd.py:545-549)
+      while (pr[x] != x) {
+        pr[x] = pr[pr[x]];
+        x = pr[x];
+      }
+      return x;
+    };
+    for (int i = 0; i < n; ++i) {
+      const int ri = find(i);
+      for (int word = i / 32; word < words; ++word) {
+        uint32_t bits = adj[(int64_t)i * words + word];
+        while (bits) {
+          const int j = word * 32 + __ffs(bits) - 1;
+          bits &= bits - 1;
+          pr[find(j)] = ri;
+        }
+      }
+    }
+    int nr = 0;
+    for (int i = 0; i < n; ++i) pr[i] = find(i);
+    for (int i = 0; i < n; ++i)
+      if (pr[i] == i) sl[i] = nr++;
+    s_nroots = nr;
+  }
+  __syncthreads();
+  for (int r = tid; r < n; r += kFuseLargeThreads) {
+    if (pr[r] != r) continue;
+    V3 ps{0, 0, 0}, ns{0, 0, 0};
+    int cnt = 0;
+    int64_t rep = -1, first = -1;
+    double dmax = 0.0, tmin = 0.0, thr = 0.0;
+    for (int i = 0; i < n; ++i) {
+      if (pr[i] != r) continue;
+      const int64_t a = gi_[i];
+      const V3 pp{px[3 * i], px[3 * i + 1], px[3 * i + 2]};
+      const V3 nn{o.normal[3 * a], o.normal[3 * a + 1], o.normal[3 * a + 2]};
+      const double da = o.depth[a], ta = o.t[a], tha = o.threshold[a];
+      if (cnt == 0) {
+        first = a;
+        rep = a;
+        ps = pp;
+        ns = nn;
+        dmax = da;
+        tmin = ta;
+        thr = tha;
+      } else {
+        ps = ps + pp;
+        ns = ns + nn;
+        if (da > dmax) dmax = da;
+        if (ta < tmin) tmin = ta;
+        if (tha > thr) thr = tha;
+        if (ta < o.t[rep] || (ta == o.t[rep] && -da < -o.depth[rep])) rep = a;
+      }
+      ++cnt;
+    }
+    const double c = (double)cnt;
+    const V3 psn{dv(ps.x, c), dv(ps.y, c), dv(ps.z, c)};
+    const double ln = norm_blas(ns);
+    V3 nrm;
+    if (ln > 1e-12) nrm = V3{dv(ns.x, ln), dv(ns.y, ln), dv(ns.z, ln)};
+    else nrm = V3{o.normal[3 * first], o.normal[3 * first + 1], o.normal[3 * first + 2]};
+    const int64_t dst = off + sl[r];
+    f.problem[dst] = o.problem[rep];
+    f.body_a[dst] = o.body_a[rep];
+    f.body_b[dst] = o.body_b[rep];
+    f.position[3 * dst] = psn.x;
+    f.position[3 * dst + 1] = psn.y;
+    f.position[3 * dst + 2] = psn.z;
+    f.normal[3 * dst] = nrm.x;
+    f.normal[3 * dst + 1] = nrm.y;
+    f.normal[3 * dst + 2] = nrm.z;
+    f.depth[dst] = dmax;
+    f.t[dst] = tmin;
+    f.tri_a[dst] = o.tri_a[rep];
+    f.tri_b[dst] = o.tri_b[rep];
+    f.threshold[dst] = thr;
+  }
+  if (tid == 0) {
+    g_fused[g] = s_nroots;
+    atomicAdd(prob_count + o.problem[ix[0]], s_nroots);
+  }
+}
+
 __global__ void k_compact(Soa f, const int64_t* g_off, const int64_t* g_fused, const int64_t* g_dst,
                           int64_t n_groups, Soa o) {
   for (int64_t g = blockIdx.x; g < n_groups; g += gridDim.x) {
@@ -1037,7 +1095,7 @@ __global__ void __launch_bounds__(128)
 k_allpairs(const PairInfo* __restrict__ pairs, int64_t n_pairs, const BodyInfo* __restrict__ bodies,
            const double* __restrict__ tris, unsigned long long* hits) {
   __shared__ double s_stage[kStaged * 128];
-  const Staged st{s_stage + threadIdx.x, 128};
+  const Staged<128> st{s_stage + threadIdx.x};
   unsigned long long local = 0;
   for (int64_t k = blockIdx.y; k < n_pairs; k += gridDim.y) {
     const PairInfo p = pairs[k];
@@ -1415,9 +1473,39 @@ static int fuse_stage(ltsg_workspace* ws, cudaStream_t st, Soa ro, unsigned long
   k_fuse_block<<<(int)std::min<int64_t>(n_groups, 148 * 8), kFuseThreads, 0, st>>>(
       ro, idx, g_off, n_groups, n_rec, fs, g_fused, prob_count, big_list, big_count);
   LTSG_LAUNCHED();
-  k_fuse_big<<<grid_for(n_groups, 32), 32, 0, st>>>(ro, idx, g_off, n_groups, n_rec, parent, fs, g_fused,
-                                                    prob_count, big_list, big_count);
-  LTSG_LAUNCHED();
+  int32_t n_big = 0;
+  LTSG_CUDA(cudaMemcpyAsync(&n_big, big_count, sizeof(int32_t), cudaMemcpyDeviceToHost, st));
+  LTSG_CUDA(cudaStreamSynchronize(st));
+  if (n_big > 0) {
+    std::vector<int32_t> hb(n_big);
+    std::vector<int64_t> hoff(n_groups + 1);
+    LTSG_CUDA(cudaMemcpyAsync(hb.data(), big_list, sizeof(int32_t) * n_big, cudaMemcpyDeviceToHost, st));
+    LTSG_CUDA(cudaMemcpyAsync(hoff.data(), g_off, sizeof(int64_t) * n_groups, cudaMemcpyDeviceToHost, st));
+    LTSG_CUDA(cudaStreamSynchronize(st));
+    hoff[n_groups] = n_rec;
+    std::vector<int64_t> aoff(n_big + 1, 0);
+    for (int b = 0; b < n_big; ++b) {
+      const int64_t n = hoff[hb[b] + 1] - hoff[hb[b]];
+      aoff[b + 1] = aoff[b] + n * ((n + 31) / 32);
+    }
+    int64_t* d_aoff;
+    uint32_t* adj;
+    FuseKey* keys;
+    int64_t* gi;
+    double *pos, *thr;
+    int32_t* slot;
+    LTSG_TRY(ws_get(ws, "fl_aoff", (size_t)n_big + 1, &d_aoff));
+    LTSG_TRY(ws_get(ws, "fl_adj", (size_t)aoff[n_big], &adj));
+    LTSG_TRY(ws_get(ws, "fl_keys", (size_t)n_rec, &keys));
+    LTSG_TRY(ws_get(ws, "fl_gi", (size_t)n_rec, &gi));
+    LTSG_TRY(ws_get(ws, "fl_pos", (size_t)n_rec * 3, &pos));
+    LTSG_TRY(ws_get(ws, "fl_thr", (size_t)n_rec, &thr));
+    LTSG_TRY(ws_get(ws, "fl_slot", (size_t)n_rec, &slot));
+    LTSG_CUDA(cudaMemcpyAsync(d_aoff, aoff.data(), sizeof(int64_t) * (n_big + 1), cudaMemcpyHostToDevice, st));
+    k_fuse_large<<<n_big, kFuseLargeThreads, 0, st>>>(ro, idx, g_off, n_groups, n_rec, fs, g_fused, prob_count,
+                                                      big_list, d_aoff, keys, gi, pos, thr, parent, slot, adj);
+    LTSG_LAUNCHED();
+  }
 
   // raw output in canonical order (group, then fusion key)
   if (out->raw_t) {
