@@ -228,8 +228,21 @@ def run_scene(ds: DeviceScene, *, widen: float = _WIDEN, exhaustive: bool = Fals
         return out.to_host(res)
 
 
+import threading as _threading
+
+_packers = _threading.local()
+
+
+def _packer() -> packing.Packer:
+    pk = getattr(_packers, "p", None)
+    if pk is None:
+        pk = packing.Packer(pinned=True)
+        _packers.p = pk
+    return pk
+
+
 def _run_problems(problems, *, widen, exhaustive=False, raw=False) -> BatchResult:
-    hs = packing.pack(problems)
+    hs = _packer().pack(problems)
     try:
         return run_scene(DeviceScene(hs), widen=widen, exhaustive=exhaustive, raw=raw)
     except _lib.CapacityError:

@@ -163,6 +163,108 @@ def body_state_row(body) -> np.ndarray:
     return row
 
 
+class Packer:
+    """Re-uses the assembled, pinned tree block across calls that pack the
+    same bodies (an engine sweeping the same particles): only the kinematic
+    states and the pair tables are rebuilt.  Trees are immutable after
+    construction, so the cache is keyed on tree identity."""
+
+    def __init__(self, pinned: bool = True):
+        self.pinned = pinned
+        self._key = None
+        self._static = None
+
+    def pack(self, problems) -> HostScene:
+        bodies, pair_body, pair_problem, pair_group, dts, tbs = _tables(problems)
+        key = tuple(id(b.tree) for b in bodies)
+        if key != self._key:
+            self._static = _assemble_static(bodies, self.pinned)
+            self._key = key
+            self._trees = [b.tree for b in bodies]  # keep ids alive while cached
+        tris, orig, lev, max_children = self._static
+        state = _pinned((len(bodies), 16), np.float64) if self.pinned else np.empty((len(bodies), 16))
+        ids = np.empty(len(bodies), dtype=np.int64)
+        for i, b in enumerate(bodies):
+            state[i] = body_state_row(b)
+            ids[i] = body_id(b)
+        lev = lev.copy()
+        lev[:, 1] = ids
+        return HostScene(
+            tris=tris, tri_orig=orig, body_state=state, body_levels=lev,
+            pair_body=np.asarray(pair_body, dtype=np.int32).reshape(-1, 2),
+            pair_problem=np.asarray(pair_problem, dtype=np.int32),
+            pair_group=np.asarray(pair_group, dtype=np.int32),
+            problem_dt=np.asarray(dts, dtype=np.float64), problem_tbase=np.asarray(tbs, dtype=np.float64),
+            max_children=max_children, n_problems=len(dts), body_ids=ids)
+
+
+def _pinned(shape, dtype):
+    import torch
+
+    t = torch.empty(shape, dtype={np.float64: torch.float64, np.int32: torch.int32,
+                                  np.int64: torch.int64}[dtype], pin_memory=True)
+    return t.numpy()
+
+
+def _tables(problems):
+    slot_of = {}
+    bodies = []
+    pair_body = []
+    pair_problem = []
+    pair_group = []
+    dts = np.empty(len(problems))
+    tbs = np.empty(len(problems))
+    for pi, (pairs, dt, tb) in enumerate(problems):
+        dts[pi] = float(dt)
+        tbs[pi] = float(tb)
+        ids = []
+        for ba, bb in pairs:
+            for b in (ba, bb):
+                if id(b) not in slot_of:
+                    slot_of[id(b)] = len(bodies)
+                    bodies.append(b)
+            pair_body.append((slot_of[id(ba)], slot_of[id(bb)]))
+            pair_problem.append(pi)
+            ids.append((body_id(ba), body_id(bb)))
+        # fusion groups: distinct (body_a id, body_b id) in sorted order (ccd.py:539)
+        uniq = sorted(set(ids))
+        rank = {u: r for r, u in enumerate(uniq)}
+        pair_group.extend(rank[i] for i in ids)
+    return bodies, pair_body, pair_problem, pair_group, dts, tbs
+
+
+def _assemble_static(bodies, pinned):
+    """Concatenated tree records of the bodies' distinct trees + level table."""
+    trees = {}
+    order = []
+    for b in bodies:
+        k = id(b.tree)
+        if k not in trees:
+            trees[k] = pack_tree(b.tree)
+            order.append(k)
+    tree_off = {}
+    off = 0
+    for k in order:
+        tree_off[k] = off
+        off += len(trees[k].records)
+    tris = _pinned((off, RECORD), np.float64) if pinned else np.empty((off, RECORD))
+    orig = _pinned((off,), np.int32) if pinned else np.empty(off, dtype=np.int32)
+    max_children = 1
+    for k in order:
+        pt = trees[k]
+        tris[tree_off[k]:tree_off[k] + len(pt.records)] = pt.records
+        orig[tree_off[k]:tree_off[k] + len(pt.records)] = pt.orig
+        max_children = max(max_children, pt.max_children)
+    lev = np.zeros((len(bodies), 18), dtype=np.int64)
+    for i, b in enumerate(bodies):
+        pt = trees[id(b.tree)]
+        L = len(pt.level_size)
+        lev[i, 0] = L
+        lev[i, 2:2 + L] = tree_off[id(b.tree)] + pt.level_off
+        lev[i, 10:10 + L] = pt.level_size
+    return tris, orig, lev, max_children
+
+
 def pack(problems) -> HostScene:
     """Pack a batch of problems.
 

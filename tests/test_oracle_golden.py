@@ -86,3 +86,16 @@ def test_config_shaped_scenes_bit_exact(idx):
     res = run_case(O, case)
     compare_result(res, case["result"], raw=res.raw, label=case["name"])
     assert sum(res.stats.values()) == case["rows"]
+
+
+def test_acceptance_criterion2_pairs_bit_exact():
+    """The 200 seeded pairs of the reference's acceptance criterion 2
+    (test_acceptance.py:280-353), replayed; exhaustive mode on the first 30."""
+    for case in golden("scenes_crit2")["cases"]:
+        res = run_case(O, case)
+        compare_result(res, case["result"], raw=res.raw, label=case["name"])
+        assert sum(res.stats.values()) == case["rows"], case["name"]
+        if "exhaustive_result" in case:
+            ex = run_case(O, case, exhaustive=True)
+            compare_result(ex, case["exhaustive_result"], raw=ex.raw, label=case["name"] + " ex")
+            assert sum(ex.stats.values()) == case["exhaustive_rows"]
