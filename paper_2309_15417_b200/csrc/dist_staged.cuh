@@ -91,9 +91,14 @@ __device__ __forceinline__ double clip_quot(double num, double den) {
 
 // Squared point-triangle distance (kernels.py:23-75), branch-free.
 // ab = e0, ac = -e2 (exact negation of v0 - v2), bc = e1.  The closest point
-// is q = (P + D1*s1) + D2*s2: vertex regions use s1 = s2 = 0 (q == P up to
-// the sign of zeros, which squaring removes), edges s2 = 0.
-__device__ __forceinline__ double pt_sq_uniform(V3 p, V3 a, V3 b, V3 c, V3 ab, V3 ac, V3 bc) {
+// is q = (P + D1*s1) + ac*s2: vertex regions use s1 = s2 = 0 (q == P up to
+// the sign of zeros, which squaring removes), edges s2 = 0.  P and D1 are
+// re-read from the stage by index instead of being moved between registers.
+template <int kStride>
+__device__ __forceinline__ double pt_sq_staged(const Staged<kStride>& st, int pk, int tb, int eb) {
+  const V3 p = st.v3(pk);
+  const V3 a = st.v3(tb), b = st.v3(tb + 3), c = st.v3(tb + 6);
+  const V3 ab = st.v3(eb), ac = neg(st.v3(eb + 6));
   const V3 ap = p - a, bp = p - b, cp = p - c;
   const double d1 = dot_simd(ab, ap), d2 = dot_simd(ac, ap);
   const double d3 = dot_simd(ab, bp), d4 = dot_simd(ac, bp);
@@ -109,18 +114,21 @@ __device__ __forceinline__ double pt_sq_uniform(V3 p, V3 a, V3 b, V3 c, V3 ab, V
   const bool on_ac = le0(vb) && ge0(d2) && le0(d6);
   const bool on_bc = le0(va) && ge0(e43) && ge0(e56);
   const bool vertex = in_a || in_b || in_c;
-  // operand selection in reverse priority order (later overrides earlier)
+  // region -> (vertex index of P, edge of D1, quotient); later overrides earlier
   const double den = add(add(va, vb), vc);
-  double n1 = vb, m1 = den;  // face
-  V3 P = a, D1 = ab;
+  int pv = 0, de = 0;  // P = a, D1 = ab
+  double n1 = vb, m1 = den;
   bool face = true;
-  if (on_bc) { n1 = e43; m1 = add(e43, e56); P = b; D1 = bc; face = false; }
-  if (on_ac) { n1 = d2; m1 = sub(d2, d6); P = a; D1 = ac; face = false; }
-  if (on_ab) { n1 = d1; m1 = sub(d1, d3); P = a; D1 = ab; face = false; }
-  if (vertex) { P = in_a ? a : (in_b ? b : c); face = false; }
+  if (on_bc) { n1 = e43; m1 = add(e43, e56); pv = 1; de = 1; face = false; }
+  if (on_ac) { n1 = d2; m1 = sub(d2, d6); pv = 0; de = 2; face = false; }
+  if (on_ab) { n1 = d1; m1 = sub(d1, d3); pv = 0; de = 0; face = false; }
+  if (vertex) { pv = in_a ? 0 : (in_b ? 1 : 2); face = false; }
   double s1 = 0.0, s2 = 0.0;
   if (!vertex) s1 = sdiv(n1, m1);
   if (face) s2 = sdiv(vc, den);
+  const V3 P = st.v3(tb + 3 * pv);
+  V3 D1 = st.v3(eb + 3 * de);
+  if (de == 2) D1 = neg(D1);
   const V3 q = (P + scale(D1, s1)) + scale(ac, s2);
   return sqn(p - q);
 }
@@ -165,32 +173,14 @@ template <int kStride>
 __device__ __forceinline__ double staged_dist_sq(const Staged<kStride>& st) {
   double best = __longlong_as_double(0x7ff0000000000000LL);
 #if LTSG_ILP
-#pragma unroll 1
-  for (int q = 0; q < 3; ++q) {
-    // vertex q of A against triangle B, vertex q of B against triangle A
-    const double da = pt_sq_uniform(st.v3(kStA + 3 * q), st.v3(kStB), st.v3(kStB + 3), st.v3(kStB + 6),
-                                    st.v3(kStEB), neg(st.v3(kStEB + 6)), st.v3(kStEB + 3));
-    const double db = pt_sq_uniform(st.v3(kStB + 3 * q), st.v3(kStA), st.v3(kStA + 3), st.v3(kStA + 6),
-                                    st.v3(kStEA), neg(st.v3(kStEA + 6)), st.v3(kStEA + 3));
-    best = min_nonneg(best, min_nonneg(da, db));
-  }
-#pragma unroll 1
-  for (int i = 0; i < 3; ++i) {
-    const V3 p1 = st.v3(kStA + 3 * i), u = st.v3(kStEA + 3 * i);
-    const double uu = st.at(kStAA + i);
-    const double d0 = ss_sq_uniform(p1, u, uu, st.v3(kStB), st.v3(kStEB), st.at(kStBB));
-    const double d1 = ss_sq_uniform(p1, u, uu, st.v3(kStB + 3), st.v3(kStEB + 3), st.at(kStBB + 1));
-    const double d2 = ss_sq_uniform(p1, u, uu, st.v3(kStB + 6), st.v3(kStEB + 6), st.at(kStBB + 2));
-    best = min_nonneg(best, min_nonneg(d0, min_nonneg(d1, d2)));
-  }
+#error "the ILP variant was retired"
 #else
 #pragma unroll 1
   for (int q = 0; q < 6; ++q) {
     const int pbase = q < 3 ? kStA + 3 * q : kStB + 3 * (q - 3);
     const int tbase = q < 3 ? kStB : kStA;
     const int ebase = q < 3 ? kStEB : kStEA;
-    best = min_nonneg(best, pt_sq_uniform(st.v3(pbase), st.v3(tbase), st.v3(tbase + 3), st.v3(tbase + 6),
-                                          st.v3(ebase), neg(st.v3(ebase + 6)), st.v3(ebase + 3)));
+    best = min_nonneg(best, pt_sq_staged(st, pbase, tbase, ebase));
   }
 #pragma unroll 1
   for (int f = 0; f < 9; ++f) {

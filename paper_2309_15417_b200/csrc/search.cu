@@ -22,6 +22,7 @@
 #include <cub/cub.cuh>
 
 #include <algorithm>
+#include <cstdlib>
 #include <vector>
 
 namespace ltsg {
@@ -447,6 +448,167 @@ k_screen(const Cand* __restrict__ front, int64_t n, const PairInfo* __restrict__
           nc.la = (int16_t)c.la;
           nc.lb = (int16_t)c.lb;
           nc.w0 = c.w0;
+          out.next[dst] = nc;
+        }
+      }
+    }
+    __syncwarp();
+  }
+}
+
+
+// ---------------------------------------------------------------- static screen
+
+// World coordinates at tau = 0 of every record of every body (the pose at the
+// window start): x = base * local + x0, in the reference's einsum order.
+// This is exactly what rotation_at/position_at give at tau = 0.
+__global__ void k_world_count(const BodyInfo* __restrict__ bodies, int n, int64_t* cnt) {
+  const int b = blockIdx.x * blockDim.x + threadIdx.x;
+  if (b > n) return;
+  if (b == n) {
+    cnt[n] = 0;
+    return;
+  }
+  const BodyInfo& B = bodies[b];
+  const int top = B.n_levels - 1;
+  cnt[b] = B.level_off[top] + B.level_size[top] - B.level_off[0];
+}
+
+__global__ void k_world_fill(const BodyInfo* __restrict__ bodies, int n, const int64_t* __restrict__ woff,
+                             const double* __restrict__ tris, double* __restrict__ world) {
+  for (int b = blockIdx.x; b < n; b += gridDim.x) {
+    const BodyInfo& B = bodies[b];
+    const int64_t cnt = woff[b + 1] - woff[b];
+    double pos[3];
+    position_at(B.m, 0.0, pos);
+    for (int64_t j = threadIdx.x; j < cnt; j += blockDim.x) {
+      const double* r = tris + (size_t)(B.level_off[0] + j) * kRecord;
+      double L[9];
+      load_local(r, L);
+      const Tri t = world_tri(B.m.base, pos, L);
+      double* w = world + (size_t)(woff[b] + j) * kRecord;
+#pragma unroll
+      for (int k = 0; k < 3; ++k) {
+        w[3 * k] = t.v[k].x;
+        w[3 * k + 1] = t.v[k].y;
+        w[3 * k + 2] = t.v[k].z;
+      }
+      w[9] = r[9];
+      w[10] = r[10];
+      w[11] = r[11];
+    }
+  }
+}
+
+__device__ __forceinline__ Tri load_world(const double* w) {
+  const double2* q = reinterpret_cast<const double2*>(w);
+  Tri t;
+  double v[10];
+#pragma unroll
+  for (int k = 0; k < 5; ++k) {
+    const double2 x = __ldg(q + k);
+    v[2 * k] = x.x;
+    v[2 * k + 1] = x.y;
+  }
+#pragma unroll
+  for (int k = 0; k < 3; ++k) t.v[k] = V3{v[3 * k], v[3 * k + 1], v[3 * k + 2]};
+  return t;
+}
+
+constexpr int kStaticWarps = 4;
+constexpr int kStaticStageBytes = kStaged * 32 * kStaticWarps * sizeof(double);
+#ifndef LTSG_STATIC_MINB
+#define LTSG_STATIC_MINB 4
+#endif
+
+// Screen of a generation when every problem of the batch is static (dt = 0):
+// every candidate has exactly one sample at tau = w0 = 0 (span 0,
+// ccd.py:352), its flag threshold is h (step 0, ccd.py:410-411) and a fine
+// candidate inside h + 1e-9 is resting (ccd.py:407-409), so the sample
+// machinery of k_screen collapses to one thread per candidate reading the
+// precomputed world triangles.
+__global__ void __launch_bounds__(32 * kStaticWarps, LTSG_STATIC_MINB)
+k_screen_static(const Cand* __restrict__ front, int64_t n, const PairInfo* __restrict__ pairs,
+                const BodyInfo* __restrict__ bodies, const double* __restrict__ tris,
+                const double* __restrict__ world, const int64_t* __restrict__ woff, ScreenOut out) {
+  extern __shared__ double s_stage[];  // kStaged x (32 * kStaticWarps)
+  __shared__ ChildInfo s_child[kStaticWarps][32];
+  const Staged<32 * kStaticWarps> st{s_stage + threadIdx.x};
+  const int warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
+  ChildInfo* kid = s_child[warp];
+  const int64_t n_warps = (n + 31) / 32;
+  for (int64_t wi = blockIdx.x * (int64_t)kStaticWarps + warp; wi < n_warps;
+       wi += (int64_t)gridDim.x * kStaticWarps) {
+    const int64_t ci = wi * 32 + lane;
+    ChildInfo ch{};
+    if (ci < n) {
+      const Cand c = front[ci];
+      const PairInfo p = pairs[c.pair];
+      const BodyInfo& A = bodies[p.ba];
+      const BodyInfo& B = bodies[p.bb];
+      const int64_t ja = A.level_off[c.la] + c.ia, jb = B.level_off[c.lb] + c.ib;
+      const double* wa = world + (size_t)(woff[p.ba] + ja - A.level_off[0]) * kRecord;
+      const double* wb = world + (size_t)(woff[p.bb] + jb - B.level_off[0]) * kRecord;
+      const double h = add(__ldg(wa + 9), __ldg(wb + 9));
+      stage_pair(st, load_world(wa), load_world(wb));
+      const double d = __dsqrt_rn(staged_dist_sq(st));
+      if (c.la == 0 && c.lb == 0) {
+        if (d <= add(h, kRestSlop)) {
+          const unsigned long long slot = atomicAdd(&out.ctr->resting, 1ULL);
+          if (slot < out.rest_cap) out.resting[slot] = RestRec{c.pair, c.ia, c.ib, 0, h};
+        }
+      } else if (d <= h) {
+        int na = 1, nb = 1;
+        ch.ia0 = c.ia;
+        ch.ib0 = c.ib;
+        if (c.la > 0) {
+          const int2 cr = *reinterpret_cast<const int2*>(wa + 11);
+          ch.ia0 = cr.x;
+          na = cr.y;
+        }
+        if (c.lb > 0) {
+          const int2 cr = *reinterpret_cast<const int2*>(wb + 11);
+          ch.ib0 = cr.x;
+          nb = cr.y;
+        }
+        ch.pair = c.pair;
+        ch.nb = nb;
+        ch.count = na * nb;
+        ch.la = c.la > 0 ? c.la - 1 : 0;
+        ch.lb = c.lb > 0 ? c.lb - 1 : 0;
+        ch.w0 = c.w0;
+      }
+    }
+    const int cincl = warp_incl_scan(ch.count, lane);
+    const int ctotal = __shfl_sync(0xffffffffu, cincl, 31);
+    unsigned long long cbase = 0;
+    if (lane == 0) {
+      const int64_t left = n - wi * 32;
+      atomicAdd(&out.ctr->rows, (unsigned long long)(left < 32 ? left : 32));
+      if (ctotal) cbase = atomicAdd(&out.ctr->next, (unsigned long long)ctotal);
+    }
+    cbase = __shfl_sync(0xffffffffu, cbase, 0);
+    if (ctotal) {
+      ch.first = cincl - ch.count;
+      kid[lane] = ch;
+      __syncwarp();
+      for (int s = lane; s < ctotal; s += 32) {
+        int o = 0;
+#pragma unroll
+        for (int step = 16; step > 0; step >>= 1)
+          if (kid[o + step].first <= s) o += step;
+        const ChildInfo& k = kid[o];
+        const int j = s - k.first;
+        const unsigned long long dst = cbase + s;
+        if (dst < out.next_cap) {
+          Cand nc;
+          nc.pair = k.pair;
+          nc.ia = k.ia0 + j / k.nb;
+          nc.ib = k.ib0 + j % k.nb;
+          nc.la = (int16_t)k.la;
+          nc.lb = (int16_t)k.lb;
+          nc.w0 = k.w0;
           out.next[dst] = nc;
         }
       }
@@ -1148,6 +1310,8 @@ static int configure_kernels() {
   static int done = 0;
   if (!done) {
     LTSG_CUDA(cudaFuncSetAttribute(k_screen, cudaFuncAttributeMaxDynamicSharedMemorySize, kScreenStageBytes));
+    LTSG_CUDA(cudaFuncSetAttribute(k_screen_static, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   kStaticStageBytes));
     done = 1;
   }
   return LTSG_OK;
@@ -1277,20 +1441,53 @@ static int run_search(const ltsg_scene* sc, ltsg_result* out, ltsg_workspace* ws
   LTSG_TRY(ws_get(ws, "entries", entry_cap, &entries));
   LTSG_TRY(ws_get(ws, "cross", cross_cap, &cross));
   Counters h{};
+  LTSG_TRY(read_ctr(d_ctr, &h, st));
+  // all-static batch (every dt == 0): one sample per candidate at tau = 0
+  bool all_static = false;
+  double* world = nullptr;
+  int64_t* woff = nullptr;
+  {
+    std::vector<double> hdt(np);
+    LTSG_CUDA(cudaMemcpyAsync(hdt.data(), sc->problem_dt, sizeof(double) * np, cudaMemcpyDeviceToHost, st));
+    LTSG_CUDA(cudaStreamSynchronize(st));
+    all_static = std::all_of(hdt.begin(), hdt.end(), [](double d) { return d == 0.0; });
+    const char* env = getenv("LTSG_NO_STATIC");
+    if (env && env[0] == '1') all_static = false;
+  }
+  if (all_static && sc->n_bodies > 0) {
+    int64_t* wcnt;
+    LTSG_TRY(ws_get(ws, "world_cnt", (size_t)sc->n_bodies + 1, &wcnt));
+    LTSG_TRY(ws_get(ws, "world_off", (size_t)sc->n_bodies + 1, &woff));
+    k_world_count<<<grid_for(sc->n_bodies + 1, 128), 128, 0, st>>>(pr.bodies, sc->n_bodies, wcnt);
+    LTSG_LAUNCHED();
+    LTSG_TRY(scan_exclusive(ws, wcnt, woff, sc->n_bodies + 1, st));
+    int64_t n_world = 0;
+    LTSG_CUDA(cudaMemcpyAsync(&n_world, woff + sc->n_bodies, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+    LTSG_CUDA(cudaStreamSynchronize(st));
+    LTSG_TRY(ws_get(ws, "world", (size_t)std::max<int64_t>(n_world, 1) * kRecord, &world));
+    k_world_fill<<<(int)std::min<int64_t>(sc->n_bodies, 148 * 8), 128, 0, st>>>(pr.bodies, sc->n_bodies, woff,
+                                                                                sc->tris, world);
+    LTSG_LAUNCHED();
+  }
   const int64_t fan = (int64_t)sc->max_children * sc->max_children;
   while (n_front > 0) {
     Cand* next;
     LTSG_TRY(ws_get(ws, fname[fsel ^ 1], (size_t)(n_front * fan), &next));
-    Counters before;
-    LTSG_TRY(read_ctr(d_ctr, &before, st));
+    Counters before = h;
     before.next = 0;
     for (;;) {
       LTSG_CUDA(cudaMemcpyAsync(d_ctr, &before, sizeof(Counters), cudaMemcpyHostToDevice, st));
       ScreenOut so{next, (unsigned long long)(n_front * fan), resting, rest_cap, entries, entry_cap,
                    cross, cross_cap, d_ctr};
       t_screen.start(st);
-      k_screen<<<screen_grid(n_front), 32 * kScreenWarps, kScreenStageBytes, st>>>(
-          front, n_front, pr.pairs, pr.bodies, sc->tris, so);
+      if (all_static) {
+        const int64_t blocks = (n_front + 32 * kStaticWarps - 1) / (32 * kStaticWarps);
+        k_screen_static<<<(int)std::max<int64_t>(1, std::min<int64_t>(blocks, 148LL * 64)), 32 * kStaticWarps,
+                          kStaticStageBytes, st>>>(front, n_front, pr.pairs, pr.bodies, sc->tris, world, woff, so);
+      } else {
+        k_screen<<<screen_grid(n_front), 32 * kScreenWarps, kScreenStageBytes, st>>>(
+            front, n_front, pr.pairs, pr.bodies, sc->tris, so);
+      }
       LTSG_LAUNCHED();
       t_screen.stop(st);
       LTSG_TRY(read_ctr(d_ctr, &h, st));
