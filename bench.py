@@ -296,6 +296,7 @@ def run_ours(args, rank, world, local_rank):
     # per-kernel device time of the screen from the library's own events
     screen_ms = sum(s.get("ms_screen", 0.0) for s in stats)
     screen_rows = sum(s["rows_screen"] for s in stats)
+    exact_rows = sum(s.get("rows_screen_exact", s["rows_screen"]) for s in stats)
     launches = sum(s.get("launches", 0) for s in stats)
 
     # ---- end to end through the public API from host bodies
@@ -341,7 +342,8 @@ def run_ours(args, rank, world, local_rank):
 
     if rank == 0:
         value = tests_all / (total_ms * 1e-3)
-        achieved = screen_rows * FLOPS_PER_TEST / (screen_ms * 1e-3) / 1e12 if screen_ms > 0 else 0.0
+        # flops of the rows that actually ran the exact 15-feature distance
+        achieved = exact_rows * FLOPS_PER_TEST / (screen_ms * 1e-3) / 1e12 if screen_ms > 0 else 0.0
         line = {
             "metric": METRIC, "value": value, "unit": "tests/s", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": total_ms / args.steps,
@@ -366,7 +368,11 @@ def run_ours(args, rank, world, local_rank):
                          "peak_source": "in-run DFMA microbenchmark (ltsg_fp64_peak); "
                                         "MEASURED_PEAKS.json has no FP64 entry",
                          "flops_per_test": FLOPS_PER_TEST,
-                         "screen_ms_per_step": screen_ms / args.steps},
+                         "screen_ms_per_step": screen_ms / args.steps,
+                         "screen_rows_per_step": screen_rows / args.steps,
+                         "screen_rows_exact_per_step": exact_rows / args.steps,
+                         "note": "rows settled by the certified sphere cull are counted as tests in "
+                                 "`value` (their decision is identical) but not in `achieved`"},
             "gpu_launches": launches,
             "breakdown_ms_per_step": {
                 "screen": screen_ms / args.steps,

@@ -153,6 +153,8 @@ typedef struct {
   double ms_screen;       /* device time of the screen kernels (CUDA events) */
   double ms_refine;       /* zoom + bisection */
   double ms_contacts;     /* records, contacts, fusion */
+  int64_t rows_screen_exact; /* screen rows that ran the exact 15-feature distance
+                                (the rest were settled by the certified sphere cull) */
 } ltsg_result;
 
 typedef struct ltsg_workspace ltsg_workspace;

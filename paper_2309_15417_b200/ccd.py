@@ -198,7 +198,7 @@ class DeviceResult:
         raw = {k: v[:nr].cpu().numpy() for k, v in self.r.items()} if self.r else None
         stats = {k: int(getattr(st, k)) for k in (
             "rows_screen", "rows_zoom", "rows_bisect", "rows_executed", "candidates",
-            "generations", "n_raw", "n_fused", "launches")}
+            "generations", "n_raw", "n_fused", "launches", "rows_screen_exact")}
         stats.update({k: float(getattr(st, k)) for k in ("ms_screen", "ms_refine", "ms_contacts")})
         return BatchResult(dt=self.dt[:n].cpu().numpy(), collision=self.coll[:n].cpu().numpy() != 0,
                            first_contact=self.first[:n].cpu().numpy(),

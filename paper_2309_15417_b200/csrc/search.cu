@@ -82,6 +82,7 @@ struct Counters {
   unsigned long long bisect_rows;
   unsigned long long records;
   unsigned long long overflow;   // zoom queue overflow flag
+  unsigned long long screen_exact;  // screen rows evaluated with the exact 15-feature distance
 };
 
 // ---------------------------------------------------------------- prep
@@ -424,6 +425,7 @@ k_screen(const Cand* __restrict__ front, int64_t n, const PairInfo* __restrict__
     unsigned long long cbase = 0;
     if (lane == 0) {
       atomicAdd(&out.ctr->rows, (unsigned long long)total);
+      atomicAdd(&out.ctr->screen_exact, (unsigned long long)total);
       if (ctotal) cbase = atomicAdd(&out.ctr->next, (unsigned long long)ctotal);
     }
     cbase = __shfl_sync(0xffffffffu, cbase, 0);
@@ -459,9 +461,18 @@ k_screen(const Cand* __restrict__ front, int64_t n, const PairInfo* __restrict__
 
 // ---------------------------------------------------------------- static screen
 
-// World coordinates at tau = 0 of every record of every body (the pose at the
-// window start): x = base * local + x0, in the reference's einsum order.
-// This is exactly what rotation_at/position_at give at tau = 0.
+// World records at tau = 0 (the pose at the window start), 16 doubles each:
+//   [0..8]  world corners x = base * local + x0 in the reference's einsum
+//           order -- exactly what rotation_at/position_at give at tau = 0
+//   [9] epsilon, [10] arm, [11] children (copied from the body record)
+//   [12..14] bounding-sphere centre (corner mean), [15] radius, or -1 when
+//           the triangle is a sliver (cond = Lmax^2 / |e0 x e2| > kCullCond)
+constexpr int kWorld = 16;
+constexpr double kCullCond = 1e4;
+// Relative slack of the certified cull: rows within this (times the
+// coordinate scale) of a threshold are always evaluated exactly.
+constexpr double kCullMargin = 1e-7;
+
 __global__ void k_world_count(const BodyInfo* __restrict__ bodies, int n, int64_t* cnt) {
   const int b = blockIdx.x * blockDim.x + threadIdx.x;
   if (b > n) return;
@@ -486,7 +497,7 @@ __global__ void k_world_fill(const BodyInfo* __restrict__ bodies, int n, const i
       double L[9];
       load_local(r, L);
       const Tri t = world_tri(B.m.base, pos, L);
-      double* w = world + (size_t)(woff[b] + j) * kRecord;
+      double* w = world + (size_t)(woff[b] + j) * kWorld;
 #pragma unroll
       for (int k = 0; k < 3; ++k) {
         w[3 * k] = t.v[k].x;
@@ -496,6 +507,23 @@ __global__ void k_world_fill(const BodyInfo* __restrict__ bodies, int n, const i
       w[9] = r[9];
       w[10] = r[10];
       w[11] = r[11];
+      // bounding sphere (approximate arithmetic; the cull margin absorbs it)
+      const V3 c{(t.v[0].x + t.v[1].x + t.v[2].x) / 3.0, (t.v[0].y + t.v[1].y + t.v[2].y) / 3.0,
+                 (t.v[0].z + t.v[1].z + t.v[2].z) / 3.0};
+      double r2 = 0.0, l2 = 0.0;
+#pragma unroll
+      for (int k = 0; k < 3; ++k) {
+        const V3 d = t.v[k] - c;
+        r2 = fmax(r2, d.x * d.x + d.y * d.y + d.z * d.z);
+        const V3 e = t.v[(k + 1) % 3] - t.v[k];
+        l2 = fmax(l2, e.x * e.x + e.y * e.y + e.z * e.z);
+      }
+      const V3 x = cross(t.v[1] - t.v[0], t.v[2] - t.v[0]);
+      const double area2 = sqrt(x.x * x.x + x.y * x.y + x.z * x.z);
+      w[12] = c.x;
+      w[13] = c.y;
+      w[14] = c.z;
+      w[15] = (area2 > 0.0 && l2 <= kCullCond * area2) ? sqrt(r2) * (1.0 + 1e-12) : -1.0;
     }
   }
 }
@@ -515,8 +543,27 @@ __device__ __forceinline__ Tri load_world(const double* w) {
   return t;
 }
 
-constexpr int kStaticWarps = 4;
-constexpr int kStaticStageBytes = kStaged * 32 * kStaticWarps * sizeof(double);
+// Certified "cannot touch": the bounding spheres are farther apart than
+// thr plus a margin.  Every witness point the reference computes lies on
+// its triangle up to rounding (segment parameters are clipped to [0,1];
+// point-triangle weights are in [0,1]; face points of non-sliver triangles
+// stay within rounding of the face), so its 15-feature distance is at least
+// the true triangle distance minus rounding, and the true distance is at
+// least the sphere gap.  Slivers (radius slot < 0) are never culled.
+__device__ __forceinline__ bool sphere_cull(const double* wa, const double* wb, double thr) {
+  const double ra = __ldg(wa + 15), rb = __ldg(wb + 15);
+  if (ra < 0.0 || rb < 0.0) return false;
+  const double dx = __ldg(wa + 12) - __ldg(wb + 12);
+  const double dy = __ldg(wa + 13) - __ldg(wb + 13);
+  const double dz = __ldg(wa + 14) - __ldg(wb + 14);
+  const double scale = 1.0 + fabs(__ldg(wa + 12)) + fabs(__ldg(wa + 13)) + fabs(__ldg(wa + 14)) + ra + rb;
+  const double reach = ra + rb + thr + kCullMargin * scale;
+  return dx * dx + dy * dy + dz * dz > reach * reach;
+}
+
+constexpr int kStaticThreads = 128;
+constexpr int kStaticChunk = 4 * kStaticThreads;  // candidates per block iteration
+constexpr int kStaticStageBytes = kStaged * kStaticThreads * sizeof(double);
 #ifndef LTSG_STATIC_MINB
 #define LTSG_STATIC_MINB 4
 #endif
@@ -524,96 +571,132 @@ constexpr int kStaticStageBytes = kStaged * 32 * kStaticWarps * sizeof(double);
 // Screen of a generation when every problem of the batch is static (dt = 0):
 // every candidate has exactly one sample at tau = w0 = 0 (span 0,
 // ccd.py:352), its flag threshold is h (step 0, ccd.py:410-411) and a fine
-// candidate inside h + 1e-9 is resting (ccd.py:407-409), so the sample
-// machinery of k_screen collapses to one thread per candidate reading the
-// precomputed world triangles.
-__global__ void __launch_bounds__(32 * kStaticWarps, LTSG_STATIC_MINB)
+// candidate within h + 1e-9 is resting (ccd.py:407-409).  A block takes
+// kStaticChunk candidates: (1) the certified sphere cull settles most of
+// them, (2) the survivors are compacted and evaluated densely by all
+// threads, (3) decisions and coalesced child emission per warp.
+__global__ void __launch_bounds__(kStaticThreads, LTSG_STATIC_MINB)
 k_screen_static(const Cand* __restrict__ front, int64_t n, const PairInfo* __restrict__ pairs,
-                const BodyInfo* __restrict__ bodies, const double* __restrict__ tris,
-                const double* __restrict__ world, const int64_t* __restrict__ woff, ScreenOut out) {
-  extern __shared__ double s_stage[];  // kStaged x (32 * kStaticWarps)
-  __shared__ ChildInfo s_child[kStaticWarps][32];
-  const Staged<32 * kStaticWarps> st{s_stage + threadIdx.x};
-  const int warp = threadIdx.x >> 5;
-  const int lane = threadIdx.x & 31;
+                const BodyInfo* __restrict__ bodies, const double* __restrict__ world,
+                const int64_t* __restrict__ woff, ScreenOut out) {
+  extern __shared__ double s_stage[];  // kStaged x kStaticThreads
+  __shared__ ChildInfo s_child[kStaticThreads / 32][32];
+  __shared__ int32_t s_queue[kStaticChunk];
+  __shared__ uint8_t s_bits[kStaticChunk];
+  __shared__ int32_t s_nq;
+  const Staged<kStaticThreads> st{s_stage + threadIdx.x};
+  const int tid = threadIdx.x;
+  const int warp = tid >> 5, lane = tid & 31;
   ChildInfo* kid = s_child[warp];
-  const int64_t n_warps = (n + 31) / 32;
-  for (int64_t wi = blockIdx.x * (int64_t)kStaticWarps + warp; wi < n_warps;
-       wi += (int64_t)gridDim.x * kStaticWarps) {
-    const int64_t ci = wi * 32 + lane;
-    ChildInfo ch{};
-    if (ci < n) {
-      const Cand c = front[ci];
-      const PairInfo p = pairs[c.pair];
-      const BodyInfo& A = bodies[p.ba];
-      const BodyInfo& B = bodies[p.bb];
-      const int64_t ja = A.level_off[c.la] + c.ia, jb = B.level_off[c.lb] + c.ib;
-      const double* wa = world + (size_t)(woff[p.ba] + ja - A.level_off[0]) * kRecord;
-      const double* wb = world + (size_t)(woff[p.bb] + jb - B.level_off[0]) * kRecord;
+
+  auto world_of = [&](const Cand& c, int side) -> const double* {
+    const PairInfo p = pairs[c.pair];
+    const int b = side ? p.bb : p.ba;
+    const BodyInfo& B = bodies[b];
+    const int l = side ? c.lb : c.la;
+    const int i = side ? c.ib : c.ia;
+    return world + (size_t)(woff[b] + B.level_off[l] + i - B.level_off[0]) * kWorld;
+  };
+
+  for (int64_t base = (int64_t)blockIdx.x * kStaticChunk; base < n; base += (int64_t)gridDim.x * kStaticChunk) {
+    const int m = (int)(n - base < kStaticChunk ? n - base : kStaticChunk);
+    if (tid == 0) s_nq = 0;
+    __syncthreads();
+    // (1) cull
+    for (int j = tid; j < m; j += kStaticThreads) {
+      const Cand c = front[base + j];
+      const double* wa = world_of(c, 0);
+      const double* wb = world_of(c, 1);
+      const double h = add(__ldg(wa + 9), __ldg(wb + 9));
+      s_bits[j] = 0;
+      if (!sphere_cull(wa, wb, add(h, kRestSlop))) s_queue[atomicAdd(&s_nq, 1)] = j;
+    }
+    __syncthreads();
+    // (2) exact 15-feature distance of the survivors
+    const int nq = s_nq;
+    for (int q = tid; q < nq; q += kStaticThreads) {
+      const int j = s_queue[q];
+      const Cand c = front[base + j];
+      const double* wa = world_of(c, 0);
+      const double* wb = world_of(c, 1);
       const double h = add(__ldg(wa + 9), __ldg(wb + 9));
       stage_pair(st, load_world(wa), load_world(wb));
       const double d = __dsqrt_rn(staged_dist_sq(st));
-      if (c.la == 0 && c.lb == 0) {
-        if (d <= add(h, kRestSlop)) {
-          const unsigned long long slot = atomicAdd(&out.ctr->resting, 1ULL);
-          if (slot < out.rest_cap) out.resting[slot] = RestRec{c.pair, c.ia, c.ib, 0, h};
+      s_bits[j] = (uint8_t)((d <= h ? 1 : 0) | (d <= add(h, kRestSlop) ? 4 : 0));
+    }
+    __syncthreads();
+    // (3) decisions (ccd.py:404-428) and child emission, one warp per 32 candidates
+    for (int w0 = warp * 32; w0 < m; w0 += kStaticThreads) {
+      const int j = w0 + lane;
+      ChildInfo ch{};
+      if (j < m && s_bits[j]) {
+        const Cand c = front[base + j];
+        const double* wa = world_of(c, 0);
+        const double* wb = world_of(c, 1);
+        if (c.la == 0 && c.lb == 0) {
+          if (s_bits[j] & 4) {
+            const double h = add(__ldg(wa + 9), __ldg(wb + 9));
+            const unsigned long long slot = atomicAdd(&out.ctr->resting, 1ULL);
+            if (slot < out.rest_cap) out.resting[slot] = RestRec{c.pair, c.ia, c.ib, 0, h};
+          }
+        } else if (s_bits[j] & 1) {
+          int na = 1, nb = 1;
+          ch.ia0 = c.ia;
+          ch.ib0 = c.ib;
+          if (c.la > 0) {
+            const int2 cr = *reinterpret_cast<const int2*>(wa + 11);
+            ch.ia0 = cr.x;
+            na = cr.y;
+          }
+          if (c.lb > 0) {
+            const int2 cr = *reinterpret_cast<const int2*>(wb + 11);
+            ch.ib0 = cr.x;
+            nb = cr.y;
+          }
+          ch.pair = c.pair;
+          ch.nb = nb;
+          ch.count = na * nb;
+          ch.la = c.la > 0 ? c.la - 1 : 0;
+          ch.lb = c.lb > 0 ? c.lb - 1 : 0;
+          ch.w0 = c.w0;
         }
-      } else if (d <= h) {
-        int na = 1, nb = 1;
-        ch.ia0 = c.ia;
-        ch.ib0 = c.ib;
-        if (c.la > 0) {
-          const int2 cr = *reinterpret_cast<const int2*>(wa + 11);
-          ch.ia0 = cr.x;
-          na = cr.y;
-        }
-        if (c.lb > 0) {
-          const int2 cr = *reinterpret_cast<const int2*>(wb + 11);
-          ch.ib0 = cr.x;
-          nb = cr.y;
-        }
-        ch.pair = c.pair;
-        ch.nb = nb;
-        ch.count = na * nb;
-        ch.la = c.la > 0 ? c.la - 1 : 0;
-        ch.lb = c.lb > 0 ? c.lb - 1 : 0;
-        ch.w0 = c.w0;
       }
-    }
-    const int cincl = warp_incl_scan(ch.count, lane);
-    const int ctotal = __shfl_sync(0xffffffffu, cincl, 31);
-    unsigned long long cbase = 0;
-    if (lane == 0) {
-      const int64_t left = n - wi * 32;
-      atomicAdd(&out.ctr->rows, (unsigned long long)(left < 32 ? left : 32));
-      if (ctotal) cbase = atomicAdd(&out.ctr->next, (unsigned long long)ctotal);
-    }
-    cbase = __shfl_sync(0xffffffffu, cbase, 0);
-    if (ctotal) {
-      ch.first = cincl - ch.count;
-      kid[lane] = ch;
-      __syncwarp();
-      for (int s = lane; s < ctotal; s += 32) {
-        int o = 0;
+      const int cincl = warp_incl_scan(ch.count, lane);
+      const int ctotal = __shfl_sync(0xffffffffu, cincl, 31);
+      unsigned long long cbase = 0;
+      if (lane == 0 && ctotal) cbase = atomicAdd(&out.ctr->next, (unsigned long long)ctotal);
+      cbase = __shfl_sync(0xffffffffu, cbase, 0);
+      if (ctotal) {
+        ch.first = cincl - ch.count;
+        kid[lane] = ch;
+        __syncwarp();
+        for (int s = lane; s < ctotal; s += 32) {
+          int o = 0;
 #pragma unroll
-        for (int step = 16; step > 0; step >>= 1)
-          if (kid[o + step].first <= s) o += step;
-        const ChildInfo& k = kid[o];
-        const int j = s - k.first;
-        const unsigned long long dst = cbase + s;
-        if (dst < out.next_cap) {
-          Cand nc;
-          nc.pair = k.pair;
-          nc.ia = k.ia0 + j / k.nb;
-          nc.ib = k.ib0 + j % k.nb;
-          nc.la = (int16_t)k.la;
-          nc.lb = (int16_t)k.lb;
-          nc.w0 = k.w0;
-          out.next[dst] = nc;
+          for (int step = 16; step > 0; step >>= 1)
+            if (kid[o + step].first <= s) o += step;
+          const ChildInfo& k = kid[o];
+          const int jj = s - k.first;
+          const unsigned long long dst = cbase + s;
+          if (dst < out.next_cap) {
+            Cand nc;
+            nc.pair = k.pair;
+            nc.ia = k.ia0 + jj / k.nb;
+            nc.ib = k.ib0 + jj % k.nb;
+            nc.la = (int16_t)k.la;
+            nc.lb = (int16_t)k.lb;
+            nc.w0 = k.w0;
+            out.next[dst] = nc;
+          }
         }
+        __syncwarp();
       }
     }
-    __syncwarp();
+    if (tid == 0) {
+      atomicAdd(&out.ctr->rows, (unsigned long long)m);
+      atomicAdd(&out.ctr->screen_exact, (unsigned long long)nq);
+    }
+    __syncthreads();
   }
 }
 
@@ -1396,6 +1479,7 @@ static int run_search(const ltsg_scene* sc, ltsg_result* out, ltsg_workspace* ws
   out->generations = 0;
   out->launches = 0;
   out->ms_screen = out->ms_refine = out->ms_contacts = 0.0;
+  out->rows_screen_exact = 0;
   if (np == 0) return LTSG_OK;
 
   Prepared pr{};
@@ -1464,7 +1548,7 @@ static int run_search(const ltsg_scene* sc, ltsg_result* out, ltsg_workspace* ws
     int64_t n_world = 0;
     LTSG_CUDA(cudaMemcpyAsync(&n_world, woff + sc->n_bodies, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
     LTSG_CUDA(cudaStreamSynchronize(st));
-    LTSG_TRY(ws_get(ws, "world", (size_t)std::max<int64_t>(n_world, 1) * kRecord, &world));
+    LTSG_TRY(ws_get(ws, "world", (size_t)std::max<int64_t>(n_world, 1) * kWorld, &world));
     k_world_fill<<<(int)std::min<int64_t>(sc->n_bodies, 148 * 8), 128, 0, st>>>(pr.bodies, sc->n_bodies, woff,
                                                                                 sc->tris, world);
     LTSG_LAUNCHED();
@@ -1481,9 +1565,9 @@ static int run_search(const ltsg_scene* sc, ltsg_result* out, ltsg_workspace* ws
                    cross, cross_cap, d_ctr};
       t_screen.start(st);
       if (all_static) {
-        const int64_t blocks = (n_front + 32 * kStaticWarps - 1) / (32 * kStaticWarps);
-        k_screen_static<<<(int)std::max<int64_t>(1, std::min<int64_t>(blocks, 148LL * 64)), 32 * kStaticWarps,
-                          kStaticStageBytes, st>>>(front, n_front, pr.pairs, pr.bodies, sc->tris, world, woff, so);
+        const int64_t blocks = (n_front + kStaticChunk - 1) / kStaticChunk;
+        k_screen_static<<<(int)std::max<int64_t>(1, std::min<int64_t>(blocks, 148LL * 16)), kStaticThreads,
+                          kStaticStageBytes, st>>>(front, n_front, pr.pairs, pr.bodies, world, woff, so);
       } else {
         k_screen<<<screen_grid(n_front), 32 * kScreenWarps, kScreenStageBytes, st>>>(
             front, n_front, pr.pairs, pr.bodies, sc->tris, so);
@@ -1569,7 +1653,8 @@ static int run_search(const ltsg_scene* sc, ltsg_result* out, ltsg_workspace* ws
   out->rows_screen = (int64_t)h.rows;
   out->rows_zoom = (int64_t)h.zoom_rows;
   out->rows_bisect = n_br * kBisectIters;
-  out->rows_executed = (int64_t)(h.rows + h.zoom_exec) + n_br * kBisectIters;
+  out->rows_executed = (int64_t)(h.screen_exact + h.zoom_exec) + n_br * kBisectIters;
+  out->rows_screen_exact = (int64_t)h.screen_exact;
   out->n_raw = n_rec;
 
   int32_t* prob_count;
