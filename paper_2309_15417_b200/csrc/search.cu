@@ -506,7 +506,13 @@ __global__ void k_world_fill(const BodyInfo* __restrict__ bodies, int n, const i
       }
       w[9] = r[9];
       w[10] = r[10];
-      w[11] = r[11];
+      {  // first child as an absolute world index (children are contiguous)
+        int lvl = 0;
+        while (lvl + 1 < B.n_levels && B.level_off[0] + j >= B.level_off[lvl + 1]) ++lvl;
+        int2 ch = *reinterpret_cast<const int2*>(r + 11);
+        if (lvl > 0) ch.x = (int32_t)(woff[b] + B.level_off[lvl - 1] - B.level_off[0] + ch.x);
+        *reinterpret_cast<int2*>(w + 11) = ch;
+      }
       // bounding sphere (approximate arithmetic; the cull margin absorbs it)
       const V3 c{(t.v[0].x + t.v[1].x + t.v[2].x) / 3.0, (t.v[0].y + t.v[1].y + t.v[2].y) / 3.0,
                  (t.v[0].z + t.v[1].z + t.v[2].z) / 3.0};
@@ -561,142 +567,161 @@ __device__ __forceinline__ bool sphere_cull(const double* wa, const double* wb, 
   return dx * dx + dy * dy + dz * dz > reach * reach;
 }
 
-constexpr int kStaticThreads = 128;
-constexpr int kStaticChunk = 4 * kStaticThreads;  // candidates per block iteration
-constexpr int kStaticStageBytes = kStaged * kStaticThreads * sizeof(double);
+constexpr int kStaticWarps = 4;
+constexpr int kStaticStageBytes = kStaged * 32 * kStaticWarps * sizeof(double);
 #ifndef LTSG_STATIC_MINB
 #define LTSG_STATIC_MINB 4
 #endif
 
-// Screen of a generation when every problem of the batch is static (dt = 0):
-// every candidate has exactly one sample at tau = w0 = 0 (span 0,
-// ccd.py:352), its flag threshold is h (step 0, ccd.py:410-411) and a fine
-// candidate within h + 1e-9 is resting (ccd.py:407-409).  A block takes
-// kStaticChunk candidates: (1) the certified sphere cull settles most of
-// them, (2) the survivors are compacted and evaluated densely by all
-// threads, (3) decisions and coalesced child emission per warp.
-__global__ void __launch_bounds__(kStaticThreads, LTSG_STATIC_MINB)
+// Static batches (every problem has dt = 0) run a leaner traversal.  Every
+// candidate has exactly one sample at tau = w0 = 0 (span 0, ccd.py:352), its
+// flag threshold is h (step 0, ccd.py:410-411) and a fine candidate within
+// h + 1e-9 is resting (ccd.py:407-409).  Candidates carry absolute indices
+// of their world records (Cand::ia/ib), and a child is tested against the
+// certified sphere cull the moment it is emitted: a culled child is a
+// decided row (not flagged, not resting) and is only counted, so the next
+// frontier holds exactly the rows that need the 15-feature distance.
+__device__ __forceinline__ bool static_child_cull(const double* world, int32_t wa, int32_t wb) {
+  const double* pa = world + (size_t)wa * kWorld;
+  const double* pb = world + (size_t)wb * kWorld;
+  const double h = add(__ldg(pa + 9), __ldg(pb + 9));
+  return sphere_cull(pa, pb, add(h, kRestSlop));
+}
+
+// Seeds (roots x roots per pair, ccd.py:385-391) in world indices, culled.
+__global__ void k_seed_static(const PairInfo* __restrict__ pairs, int64_t n_pairs,
+                              const BodyInfo* __restrict__ bodies, const int64_t* __restrict__ woff,
+                              const double* __restrict__ world, Cand* out, unsigned long long cap,
+                              Counters* ctr) {
+  const int lane = threadIdx.x & 31;
+  for (int64_t k = blockIdx.x; k < n_pairs; k += gridDim.x) {
+    const PairInfo p = pairs[k];
+    const BodyInfo& A = bodies[p.ba];
+    const BodyInfo& B = bodies[p.bb];
+    const int la = A.n_levels - 1, lb = B.n_levels - 1;
+    const int64_t na = A.level_size[la], nb = B.level_size[lb];
+    const int64_t a0 = woff[p.ba] + A.level_off[la] - A.level_off[0];
+    const int64_t b0 = woff[p.bb] + B.level_off[lb] - B.level_off[0];
+    for (int64_t j0 = threadIdx.x - lane; j0 < na * nb; j0 += blockDim.x) {
+      const int64_t j = j0 + lane;
+      bool keep = false;
+      int32_t wa = 0, wb = 0;
+      if (j < na * nb) {
+        wa = (int32_t)(a0 + j / nb);
+        wb = (int32_t)(b0 + j % nb);
+        keep = !static_child_cull(world, wa, wb);
+      }
+      const unsigned m = __ballot_sync(0xffffffffu, keep);
+      const int nvalid = (int)min((int64_t)32, na * nb - j0);
+      unsigned long long base = 0;
+      if (lane == 0) {
+        atomicAdd(&ctr->rows, (unsigned long long)(nvalid - __popc(m)));
+        if (m) base = atomicAdd(&ctr->next, (unsigned long long)__popc(m));
+      }
+      base = __shfl_sync(0xffffffffu, base, 0);
+      if (keep) {
+        const unsigned long long dst = base + __popc(m & ((1u << lane) - 1u));
+        if (dst < cap) out[dst] = Cand{(int32_t)k, wa, wb, (int16_t)la, (int16_t)lb, 0.0};
+      }
+    }
+  }
+}
+
+__global__ void __launch_bounds__(32 * kStaticWarps, LTSG_STATIC_MINB)
 k_screen_static(const Cand* __restrict__ front, int64_t n, const PairInfo* __restrict__ pairs,
                 const BodyInfo* __restrict__ bodies, const double* __restrict__ world,
                 const int64_t* __restrict__ woff, ScreenOut out) {
-  extern __shared__ double s_stage[];  // kStaged x kStaticThreads
-  __shared__ ChildInfo s_child[kStaticThreads / 32][32];
-  __shared__ int32_t s_queue[kStaticChunk];
-  __shared__ uint8_t s_bits[kStaticChunk];
-  __shared__ int32_t s_nq;
-  const Staged<kStaticThreads> st{s_stage + threadIdx.x};
-  const int tid = threadIdx.x;
-  const int warp = tid >> 5, lane = tid & 31;
+  extern __shared__ double s_stage[];  // kStaged x (32 * kStaticWarps)
+  __shared__ ChildInfo s_child[kStaticWarps][32];
+  const Staged<32 * kStaticWarps> st{s_stage + threadIdx.x};
+  const int warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
   ChildInfo* kid = s_child[warp];
-
-  auto world_of = [&](const Cand& c, int side) -> const double* {
-    const PairInfo p = pairs[c.pair];
-    const int b = side ? p.bb : p.ba;
-    const BodyInfo& B = bodies[b];
-    const int l = side ? c.lb : c.la;
-    const int i = side ? c.ib : c.ia;
-    return world + (size_t)(woff[b] + B.level_off[l] + i - B.level_off[0]) * kWorld;
-  };
-
-  for (int64_t base = (int64_t)blockIdx.x * kStaticChunk; base < n; base += (int64_t)gridDim.x * kStaticChunk) {
-    const int m = (int)(n - base < kStaticChunk ? n - base : kStaticChunk);
-    if (tid == 0) s_nq = 0;
-    __syncthreads();
-    // (1) cull
-    for (int j = tid; j < m; j += kStaticThreads) {
-      const Cand c = front[base + j];
-      const double* wa = world_of(c, 0);
-      const double* wb = world_of(c, 1);
-      const double h = add(__ldg(wa + 9), __ldg(wb + 9));
-      s_bits[j] = 0;
-      if (!sphere_cull(wa, wb, add(h, kRestSlop))) s_queue[atomicAdd(&s_nq, 1)] = j;
-    }
-    __syncthreads();
-    // (2) exact 15-feature distance of the survivors
-    const int nq = s_nq;
-    for (int q = tid; q < nq; q += kStaticThreads) {
-      const int j = s_queue[q];
-      const Cand c = front[base + j];
-      const double* wa = world_of(c, 0);
-      const double* wb = world_of(c, 1);
+  const int64_t n_warps = (n + 31) / 32;
+  for (int64_t wi = blockIdx.x * (int64_t)kStaticWarps + warp; wi < n_warps;
+       wi += (int64_t)gridDim.x * kStaticWarps) {
+    const int64_t ci = wi * 32 + lane;
+    ChildInfo ch{};
+    if (ci < n) {
+      const Cand c = front[ci];
+      const double* wa = world + (size_t)c.ia * kWorld;
+      const double* wb = world + (size_t)c.ib * kWorld;
       const double h = add(__ldg(wa + 9), __ldg(wb + 9));
       stage_pair(st, load_world(wa), load_world(wb));
       const double d = __dsqrt_rn(staged_dist_sq(st));
-      s_bits[j] = (uint8_t)((d <= h ? 1 : 0) | (d <= add(h, kRestSlop) ? 4 : 0));
-    }
-    __syncthreads();
-    // (3) decisions (ccd.py:404-428) and child emission, one warp per 32 candidates
-    for (int w0 = warp * 32; w0 < m; w0 += kStaticThreads) {
-      const int j = w0 + lane;
-      ChildInfo ch{};
-      if (j < m && s_bits[j]) {
-        const Cand c = front[base + j];
-        const double* wa = world_of(c, 0);
-        const double* wb = world_of(c, 1);
-        if (c.la == 0 && c.lb == 0) {
-          if (s_bits[j] & 4) {
-            const double h = add(__ldg(wa + 9), __ldg(wb + 9));
-            const unsigned long long slot = atomicAdd(&out.ctr->resting, 1ULL);
-            if (slot < out.rest_cap) out.resting[slot] = RestRec{c.pair, c.ia, c.ib, 0, h};
-          }
-        } else if (s_bits[j] & 1) {
-          int na = 1, nb = 1;
-          ch.ia0 = c.ia;
-          ch.ib0 = c.ib;
-          if (c.la > 0) {
-            const int2 cr = *reinterpret_cast<const int2*>(wa + 11);
-            ch.ia0 = cr.x;
-            na = cr.y;
-          }
-          if (c.lb > 0) {
-            const int2 cr = *reinterpret_cast<const int2*>(wb + 11);
-            ch.ib0 = cr.x;
-            nb = cr.y;
-          }
-          ch.pair = c.pair;
-          ch.nb = nb;
-          ch.count = na * nb;
-          ch.la = c.la > 0 ? c.la - 1 : 0;
-          ch.lb = c.lb > 0 ? c.lb - 1 : 0;
-          ch.w0 = c.w0;
+      if (c.la == 0 && c.lb == 0) {
+        if (d <= add(h, kRestSlop)) {
+          const PairInfo p = pairs[c.pair];
+          const unsigned long long slot = atomicAdd(&out.ctr->resting, 1ULL);
+          if (slot < out.rest_cap)
+            out.resting[slot] = RestRec{c.pair, (int32_t)(c.ia - woff[p.ba]), (int32_t)(c.ib - woff[p.bb]), 0, h};
         }
+      } else if (d <= h) {
+        int na = 1, nb = 1;
+        ch.ia0 = c.ia;
+        ch.ib0 = c.ib;
+        if (c.la > 0) {
+          const int2 cr = *reinterpret_cast<const int2*>(wa + 11);
+          ch.ia0 = cr.x;
+          na = cr.y;
+        }
+        if (c.lb > 0) {
+          const int2 cr = *reinterpret_cast<const int2*>(wb + 11);
+          ch.ib0 = cr.x;
+          nb = cr.y;
+        }
+        ch.pair = c.pair;
+        ch.nb = nb;
+        ch.count = na * nb;
+        ch.la = c.la > 0 ? c.la - 1 : 0;
+        ch.lb = c.lb > 0 ? c.lb - 1 : 0;
       }
-      const int cincl = warp_incl_scan(ch.count, lane);
-      const int ctotal = __shfl_sync(0xffffffffu, cincl, 31);
-      unsigned long long cbase = 0;
-      if (lane == 0 && ctotal) cbase = atomicAdd(&out.ctr->next, (unsigned long long)ctotal);
-      cbase = __shfl_sync(0xffffffffu, cbase, 0);
-      if (ctotal) {
-        ch.first = cincl - ch.count;
-        kid[lane] = ch;
-        __syncwarp();
-        for (int s = lane; s < ctotal; s += 32) {
+    }
+    const int cincl = warp_incl_scan(ch.count, lane);
+    const int ctotal = __shfl_sync(0xffffffffu, cincl, 31);
+    if (lane == 0) {
+      const int64_t left = n - wi * 32;
+      atomicAdd(&out.ctr->rows, (unsigned long long)(left < 32 ? left : 32));
+      atomicAdd(&out.ctr->screen_exact, (unsigned long long)(left < 32 ? left : 32));
+    }
+    if (ctotal) {
+      ch.first = cincl - ch.count;
+      kid[lane] = ch;
+      __syncwarp();
+      unsigned long long culled = 0;
+      for (int s0 = 0; s0 < ctotal; s0 += 32) {
+        const int s = s0 + lane;
+        bool keep = false;
+        Cand nc{};
+        if (s < ctotal) {
           int o = 0;
 #pragma unroll
           for (int step = 16; step > 0; step >>= 1)
             if (kid[o + step].first <= s) o += step;
           const ChildInfo& k = kid[o];
           const int jj = s - k.first;
-          const unsigned long long dst = cbase + s;
-          if (dst < out.next_cap) {
-            Cand nc;
-            nc.pair = k.pair;
-            nc.ia = k.ia0 + jj / k.nb;
-            nc.ib = k.ib0 + jj % k.nb;
-            nc.la = (int16_t)k.la;
-            nc.lb = (int16_t)k.lb;
-            nc.w0 = k.w0;
-            out.next[dst] = nc;
-          }
+          nc.pair = k.pair;
+          nc.ia = k.ia0 + jj / k.nb;
+          nc.ib = k.ib0 + jj % k.nb;
+          nc.la = (int16_t)k.la;
+          nc.lb = (int16_t)k.lb;
+          nc.w0 = 0.0;
+          keep = !static_child_cull(world, nc.ia, nc.ib);
         }
-        __syncwarp();
+        const unsigned m = __ballot_sync(0xffffffffu, keep);
+        const int nvalid = ctotal - s0 < 32 ? ctotal - s0 : 32;
+        culled += (unsigned long long)(nvalid - __popc(m));
+        unsigned long long base = 0;
+        if (lane == 0 && m) base = atomicAdd(&out.ctr->next, (unsigned long long)__popc(m));
+        base = __shfl_sync(0xffffffffu, base, 0);
+        if (keep) {
+          const unsigned long long dst = base + __popc(m & ((1u << lane) - 1u));
+          if (dst < out.next_cap) out.next[dst] = nc;
+        }
       }
+      if (lane == 0 && culled) atomicAdd(&out.ctr->rows, culled);
+      __syncwarp();
     }
-    if (tid == 0) {
-      atomicAdd(&out.ctr->rows, (unsigned long long)m);
-      atomicAdd(&out.ctr->screen_exact, (unsigned long long)nq);
-    }
-    __syncthreads();
   }
 }
 
@@ -1494,6 +1519,38 @@ static int run_search(const ltsg_scene* sc, ltsg_result* out, ltsg_workspace* ws
   k_init_problems<<<grid_for(np, 128), 128, 0, st>>>(tau_min, np);
   LTSG_LAUNCHED();
 
+  // ---- static batches: tau = 0 world records, sphere data, culled seeds
+  bool all_static = false;
+  double* world = nullptr;
+  int64_t* woff = nullptr;
+  if (!sc->exhaustive && sc->n_pairs > 0) {
+    std::vector<double> hdt(np);
+    LTSG_CUDA(cudaMemcpyAsync(hdt.data(), sc->problem_dt, sizeof(double) * np, cudaMemcpyDeviceToHost, st));
+    LTSG_CUDA(cudaStreamSynchronize(st));
+    all_static = std::all_of(hdt.begin(), hdt.end(), [](double d) { return d == 0.0; });
+    const char* env = getenv("LTSG_NO_STATIC");
+    if (env && env[0] == '1') all_static = false;
+  }
+  if (all_static) {
+    int64_t* wcnt;
+    LTSG_TRY(ws_get(ws, "world_cnt", (size_t)sc->n_bodies + 1, &wcnt));
+    LTSG_TRY(ws_get(ws, "world_off", (size_t)sc->n_bodies + 1, &woff));
+    k_world_count<<<grid_for(sc->n_bodies + 1, 128), 128, 0, st>>>(pr.bodies, sc->n_bodies, wcnt);
+    LTSG_LAUNCHED();
+    LTSG_TRY(scan_exclusive(ws, wcnt, woff, sc->n_bodies + 1, st));
+    int64_t n_world = 0;
+    LTSG_CUDA(cudaMemcpyAsync(&n_world, woff + sc->n_bodies, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+    LTSG_CUDA(cudaStreamSynchronize(st));
+    if (n_world >= (int64_t)1 << 31) {
+      all_static = false;  // world indices are int32 in the candidates
+    } else {
+      LTSG_TRY(ws_get(ws, "world", (size_t)std::max<int64_t>(n_world, 1) * kWorld, &world));
+      k_world_fill<<<(int)std::min<int64_t>(sc->n_bodies, 148 * 8), 128, 0, st>>>(pr.bodies, sc->n_bodies,
+                                                                                  woff, sc->tris, world);
+      LTSG_LAUNCHED();
+    }
+  }
+
   // ---- seeds: all root x root pairs (fine x fine when exhaustive), ccd.py:385-391
   int64_t n_front = 0;
   const char* fname[2] = {"front0", "front1"};
@@ -1511,9 +1568,20 @@ static int run_search(const ltsg_scene* sc, ltsg_result* out, ltsg_workspace* ws
     LTSG_CUDA(cudaMemcpyAsync(&n_front, off + sc->n_pairs, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
     LTSG_CUDA(cudaStreamSynchronize(st));
     LTSG_TRY(ws_get(ws, fname[fsel], (size_t)n_front, &front));
-    k_seed_fill<<<(int)std::min<int64_t>(sc->n_pairs, 148 * 16), 128, 0, st>>>(
-        pr.pairs, sc->n_pairs, pr.bodies, sc->exhaustive, off, front);
-    LTSG_LAUNCHED();
+    if (all_static) {
+      k_seed_static<<<(int)std::min<int64_t>(sc->n_pairs, 148 * 16), 128, 0, st>>>(
+          pr.pairs, sc->n_pairs, pr.bodies, woff, world, front, (unsigned long long)n_front, d_ctr);
+      LTSG_LAUNCHED();
+      Counters hs;
+      LTSG_TRY(read_ctr(d_ctr, &hs, st));
+      n_front = (int64_t)hs.next;
+      hs.next = 0;
+      LTSG_CUDA(cudaMemcpyAsync(d_ctr, &hs, sizeof(Counters), cudaMemcpyHostToDevice, st));
+    } else {
+      k_seed_fill<<<(int)std::min<int64_t>(sc->n_pairs, 148 * 16), 128, 0, st>>>(
+          pr.pairs, sc->n_pairs, pr.bodies, sc->exhaustive, off, front);
+      LTSG_LAUNCHED();
+    }
   }
 
   // ---- generations
@@ -1526,33 +1594,6 @@ static int run_search(const ltsg_scene* sc, ltsg_result* out, ltsg_workspace* ws
   LTSG_TRY(ws_get(ws, "cross", cross_cap, &cross));
   Counters h{};
   LTSG_TRY(read_ctr(d_ctr, &h, st));
-  // all-static batch (every dt == 0): one sample per candidate at tau = 0
-  bool all_static = false;
-  double* world = nullptr;
-  int64_t* woff = nullptr;
-  {
-    std::vector<double> hdt(np);
-    LTSG_CUDA(cudaMemcpyAsync(hdt.data(), sc->problem_dt, sizeof(double) * np, cudaMemcpyDeviceToHost, st));
-    LTSG_CUDA(cudaStreamSynchronize(st));
-    all_static = std::all_of(hdt.begin(), hdt.end(), [](double d) { return d == 0.0; });
-    const char* env = getenv("LTSG_NO_STATIC");
-    if (env && env[0] == '1') all_static = false;
-  }
-  if (all_static && sc->n_bodies > 0) {
-    int64_t* wcnt;
-    LTSG_TRY(ws_get(ws, "world_cnt", (size_t)sc->n_bodies + 1, &wcnt));
-    LTSG_TRY(ws_get(ws, "world_off", (size_t)sc->n_bodies + 1, &woff));
-    k_world_count<<<grid_for(sc->n_bodies + 1, 128), 128, 0, st>>>(pr.bodies, sc->n_bodies, wcnt);
-    LTSG_LAUNCHED();
-    LTSG_TRY(scan_exclusive(ws, wcnt, woff, sc->n_bodies + 1, st));
-    int64_t n_world = 0;
-    LTSG_CUDA(cudaMemcpyAsync(&n_world, woff + sc->n_bodies, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
-    LTSG_CUDA(cudaStreamSynchronize(st));
-    LTSG_TRY(ws_get(ws, "world", (size_t)std::max<int64_t>(n_world, 1) * kWorld, &world));
-    k_world_fill<<<(int)std::min<int64_t>(sc->n_bodies, 148 * 8), 128, 0, st>>>(pr.bodies, sc->n_bodies, woff,
-                                                                                sc->tris, world);
-    LTSG_LAUNCHED();
-  }
   const int64_t fan = (int64_t)sc->max_children * sc->max_children;
   while (n_front > 0) {
     Cand* next;
@@ -1565,8 +1606,8 @@ static int run_search(const ltsg_scene* sc, ltsg_result* out, ltsg_workspace* ws
                    cross, cross_cap, d_ctr};
       t_screen.start(st);
       if (all_static) {
-        const int64_t blocks = (n_front + kStaticChunk - 1) / kStaticChunk;
-        k_screen_static<<<(int)std::max<int64_t>(1, std::min<int64_t>(blocks, 148LL * 16)), kStaticThreads,
+        const int64_t blocks = (n_front + 32 * kStaticWarps - 1) / (32 * kStaticWarps);
+        k_screen_static<<<(int)std::max<int64_t>(1, std::min<int64_t>(blocks, 148LL * 32)), 32 * kStaticWarps,
                           kStaticStageBytes, st>>>(front, n_front, pr.pairs, pr.bodies, world, woff, so);
       } else {
         k_screen<<<screen_grid(n_front), 32 * kScreenWarps, kScreenStageBytes, st>>>(
