@@ -74,9 +74,10 @@ int ltsg_overlap_centroid(const double* tri_a, const double* tri_b, const double
  * ccd.py:527-577).
  *
  * Packed scene (device, built by the host packer):
- *  tris       n_tris x 12 float64 triangle records: 9 body-frame corners,
- *             epsilon, arm (max corner norm), and (int32 first child,
- *             int32 child count) packed into the 12th slot.  Each tree level
+ *  tris       n_tris x 16 float64 triangle records: 9 body-frame corners,
+ *             epsilon, arm (max corner norm), (int32 first child, int32 child
+ *             count) packed into slot 11, and the body-frame bounding sphere
+ *             (centroid in 12..14, radius in 15, -1 for slivers).  Each tree level
  *             is stored so that a parent's children form a contiguous range
  *             of the next finer level.
  *  tri_orig   n_tris int32: the triangle's index in the reference tree level

@@ -28,7 +28,12 @@
 namespace ltsg {
 
 constexpr int kMaxLevels = 8;
-constexpr int kRecord = 12;  // doubles per triangle record
+constexpr int kRecord = 16;  // doubles per triangle record
+constexpr int kWorld = 16;   // doubles per tau = 0 world record
+// Relative slack of the certified culls: rows within this (times the
+// coordinate scale) of a threshold are always evaluated exactly.
+constexpr double kCullMargin = 1e-7;
+constexpr double kCullCond = 1e4;  // slivers (Lmax^2 > kCullCond * |e0 x e2|) are never culled
 
 struct BodyInfo {
   Motion m;
@@ -235,8 +240,8 @@ __device__ __forceinline__ double row_distance(const Staged<kStride>& st, const 
 // ---------------------------------------------------------------- screen
 
 struct CandInfo {
-  double w0, dt, h, speed, thr;
-  int32_t pair, ia, ib, la, lb, count, first, pad;
+  double w0, dt, h, speed, thr, cull_lo, cull_hi;
+  int32_t pair, ia, ib, la, lb, count, first, culled;
 };
 
 struct ChildInfo {
@@ -287,6 +292,30 @@ __device__ __forceinline__ int warp_incl_scan(int v, int lane) {
   return v;
 }
 
+// Bounding-sphere gap minus threshold T and margin at time tau (approximate
+// arithmetic; the margin covers it): > 0 means the triangles are farther
+// apart than T at tau, with room to spare.
+__device__ __forceinline__ double sphere_gap(const BodyInfo& A, const double* ra, const BodyInfo& B,
+                                             const double* rb, double tau, double T) {
+  double R[9], pos[3];
+  rotation_at(A.m, tau, R);
+  position_at(A.m, tau, pos);
+  const double ax = __ldg(ra + 12), ay = __ldg(ra + 13), az = __ldg(ra + 14);
+  const double cax = R[0] * ax + R[1] * ay + R[2] * az + pos[0];
+  const double cay = R[3] * ax + R[4] * ay + R[5] * az + pos[1];
+  const double caz = R[6] * ax + R[7] * ay + R[8] * az + pos[2];
+  rotation_at(B.m, tau, R);
+  position_at(B.m, tau, pos);
+  const double bx = __ldg(rb + 12), by = __ldg(rb + 13), bz = __ldg(rb + 14);
+  const double cbx = R[0] * bx + R[1] * by + R[2] * bz + pos[0];
+  const double cby = R[3] * bx + R[4] * by + R[5] * bz + pos[1];
+  const double cbz = R[6] * bx + R[7] * by + R[8] * bz + pos[2];
+  const double dx = cax - cbx, dy = cay - cby, dz = caz - cbz;
+  const double rA = __ldg(ra + 15), rB = __ldg(rb + 15);
+  const double scale = 1.0 + fabs(cax) + fabs(cay) + fabs(caz) + fabs(cbx) + fabs(cby) + fabs(cbz) + rA + rB;
+  return sqrt(dx * dx + dy * dy + dz * dz) - (rA + rB + T + kCullMargin * scale);
+}
+
 // Screen one frontier (one generation): every candidate is sampled over
 // [w0, dt] (ccd.py:321-370) and decided (ccd.py:404-446).  A warp owns 32
 // consecutive candidates; their 1..33 samples are flattened into rows and
@@ -299,6 +328,7 @@ k_screen(const Cand* __restrict__ front, int64_t n, const PairInfo* __restrict__
     ChildInfo child[32];
   } s_u[kScreenWarps];
   __shared__ uint8_t s_bits[kScreenWarps][kRowsPerWarp];
+  __shared__ int16_t s_queue[kScreenWarps][kRowsPerWarp];
   extern __shared__ double s_stage[];  // kStaged x (32 * kScreenWarps), dynamic
   const Staged<32 * kScreenWarps> st{s_stage + threadIdx.x};
   const int warp = threadIdx.x >> 5;
@@ -307,6 +337,7 @@ k_screen(const Cand* __restrict__ front, int64_t n, const PairInfo* __restrict__
   CandInfo* info = s_u[warp].cand;
   ChildInfo* kid = s_u[warp].child;
   uint8_t* bits = s_bits[warp];
+  int16_t* queue = s_queue[warp];
 
   for (int64_t wi = blockIdx.x * (int64_t)kScreenWarps + warp; wi < n_warps;
        wi += (int64_t)gridDim.x * kScreenWarps) {
@@ -318,12 +349,12 @@ k_screen(const Cand* __restrict__ front, int64_t n, const PairInfo* __restrict__
       const PairInfo p = pairs[c.pair];
       const BodyInfo& A = bodies[p.ba];
       const BodyInfo& B = bodies[p.bb];
-      const double* ra = rec(tris, A, c.la, c.ia);
-      const double* rb = rec(tris, B, c.lb, c.ib);
-      me.h = add(__ldg(ra + 9), __ldg(rb + 9));  // ccd.py:339
-      double sp = p.speed0;                      // ccd.py:340-345
-      if (A.m.omega > 0.0) sp = add(sp, mul(A.m.omega, __ldg(ra + 10)));
-      if (B.m.omega > 0.0) sp = add(sp, mul(B.m.omega, __ldg(rb + 10)));
+      const double* ra_ = rec(tris, A, c.la, c.ia);
+      const double* rb_ = rec(tris, B, c.lb, c.ib);
+      me.h = add(__ldg(ra_ + 9), __ldg(rb_ + 9));  // ccd.py:339
+      double sp = p.speed0;                        // ccd.py:340-345
+      if (A.m.omega > 0.0) sp = add(sp, mul(A.m.omega, __ldg(ra_ + 10)));
+      if (B.m.omega > 0.0) sp = add(sp, mul(B.m.omega, __ldg(rb_ + 10)));
       me.speed = sp;
       me.w0 = c.w0;
       me.dt = p.dt;
@@ -332,25 +363,104 @@ k_screen(const Cand* __restrict__ front, int64_t n, const PairInfo* __restrict__
       const double step = me.count > 1
           ? sub(linspace_at(c.w0, p.dt, me.count, 1), linspace_at(c.w0, p.dt, me.count, 0)) : 0.0;
       me.thr = add(me.h, mul(mul(0.5, sp), step));  // ccd.py:410-411
+      // Certified cull window.  The bounding-sphere gap g(tau) of the pair is
+      // `speed`-Lipschitz (every point of a triangle moves at most
+      // |v| + omega*arm, the reference's own bound, ccd.py:340-345), and the
+      // true triangle distance is >= g.  With g evaluated at both window
+      // ends, samples before t_lo or after t_hi provably clear every
+      // threshold (flag, touch, rest) of this candidate.
+      me.cull_lo = -1.0;
+      me.cull_hi = 2.0 * p.dt + 1.0;
+      if (__ldg(ra_ + 15) >= 0.0 && __ldg(rb_ + 15) >= 0.0) {
+        const double T = fmax(me.thr, add(me.h, kRestSlop));
+        const double g0 = sphere_gap(A, ra_, B, rb_, c.w0, T);
+        const double g1 = p.dt > c.w0 ? sphere_gap(A, ra_, B, rb_, p.dt, T) : g0;
+        if (sp > 0.0) {
+          me.cull_lo = c.w0 + g0 / sp;  // rows with tau < cull_lo are cleared
+          me.cull_hi = p.dt - g1 / sp;  // rows with tau > cull_hi are cleared
+        } else if (g0 > 0.0) {
+          me.cull_lo = 2.0 * p.dt + 1.0;  // no motion: the whole window clears
+        }
+        // every sample cleared?
+        me.culled = me.cull_lo > p.dt || me.cull_hi < c.w0 || me.cull_lo > me.cull_hi;
+      }
       me.pair = c.pair;
       me.ia = c.ia;
       me.ib = c.ib;
       me.la = c.la;
       me.lb = c.lb;
     }
-    const int incl = warp_incl_scan(me.count, lane);
+    // rows of culled candidates are decided (all flags false) without being evaluated
+    const int nrows = me.culled ? 0 : me.count;
+    const int incl = warp_incl_scan(nrows, lane);
     const int total = __shfl_sync(0xffffffffu, incl, 31);
-    me.first = incl - me.count;
+    int all_rows = me.count;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) all_rows += __shfl_xor_sync(0xffffffffu, all_rows, o);
+    me.first = incl - nrows;
     info[lane] = me;
     __syncwarp();
 
-    for (int r = lane; r < total; r += 32) {
-      int o = 0;  // owner: last lane with first <= r (valid lanes have count >= 1)
+    // (a) per-row certified sphere cull at the row's own tau: the bounding
+    // spheres of both triangles are moved to tau (same rigid motion as the
+    // triangles); rows whose gap exceeds every threshold plus the margin
+    // are decided (no flag, not below, not resting).  Survivors are queued.
+    int nq = 0;
+    for (int r0 = 0; r0 < total; r0 += 32) {
+      const int r = r0 + lane;
+      bool keep = false;
+      if (r < total) {
+        int o = 0;  // owner: last lane with first <= r among lanes that own rows
+#pragma unroll
+        for (int step = 16; step > 0; step >>= 1)
+          if (info[o + step].first <= r) o += step;
+        while (info[o].culled || info[o].count == 0) --o;
+        const CandInfo& c = info[o];
+        const double tau = linspace_at(c.w0, c.dt, c.count, r - c.first);
+        const PairInfo p = pairs[c.pair];
+        const BodyInfo& A = bodies[p.ba];
+        const BodyInfo& B = bodies[p.bb];
+        const double* ra_ = rec(tris, A, c.la, c.ia);
+        const double* rb_ = rec(tris, B, c.lb, c.ib);
+        const double rA = __ldg(ra_ + 15), rB = __ldg(rb_ + 15);
+        keep = !(tau < c.cull_lo || tau > c.cull_hi);
+        if (keep && rA >= 0.0 && rB >= 0.0) {
+          double R[9], pos[3];
+          rotation_at(A.m, tau, R);
+          position_at(A.m, tau, pos);
+          const double ax = __ldg(ra_ + 12), ay = __ldg(ra_ + 13), az = __ldg(ra_ + 14);
+          const double cax = R[0] * ax + R[1] * ay + R[2] * az + pos[0];
+          const double cay = R[3] * ax + R[4] * ay + R[5] * az + pos[1];
+          const double caz = R[6] * ax + R[7] * ay + R[8] * az + pos[2];
+          rotation_at(B.m, tau, R);
+          position_at(B.m, tau, pos);
+          const double bx = __ldg(rb_ + 12), by = __ldg(rb_ + 13), bz = __ldg(rb_ + 14);
+          const double cbx = R[0] * bx + R[1] * by + R[2] * bz + pos[0];
+          const double cby = R[3] * bx + R[4] * by + R[5] * bz + pos[1];
+          const double cbz = R[6] * bx + R[7] * by + R[8] * bz + pos[2];
+          const double dx = cax - cbx, dy = cay - cby, dz = caz - cbz;
+          const double scale = 1.0 + fabs(cax) + fabs(cay) + fabs(caz) + fabs(cbx) + fabs(cby) + fabs(cbz) + rA + rB;
+          const double reach = rA + rB + fmax(c.thr, add(c.h, kRestSlop)) + kCullMargin * scale;
+          keep = !(dx * dx + dy * dy + dz * dz > reach * reach);
+        }
+        if (!keep) bits[r] = 0;
+      }
+      const unsigned m = __ballot_sync(0xffffffffu, keep);
+      if (keep) queue[nq + __popc(m & ((1u << lane) - 1u))] = (int16_t)r;
+      nq += __popc(m);
+    }
+    __syncwarp();
+    // (b) exact 15-feature distance of the surviving rows, densely
+    for (int q = lane; q < nq; q += 32) {
+      const int r = queue[q];
+      int o = 0;
 #pragma unroll
       for (int step = 16; step > 0; step >>= 1)
         if (info[o + step].first <= r) o += step;
+      while (info[o].culled || info[o].count == 0) --o;
       const CandInfo& c = info[o];
-      const double tau = linspace_at(c.w0, c.dt, c.count, r - c.first);
+      const int i = r - c.first;
+      const double tau = linspace_at(c.w0, c.dt, c.count, i);
       const PairInfo p = pairs[c.pair];
       const double d = row_distance(st, tris, bodies[p.ba], bodies[p.bb], c.la, c.ia, c.lb, c.ib, tau);
       uint8_t b = 0;
@@ -363,7 +473,7 @@ k_screen(const Cand* __restrict__ front, int64_t n, const PairInfo* __restrict__
 
     // per-candidate decisions
     ChildInfo ch{};
-    if (valid) {
+    if (valid && !me.culled) {
       const uint8_t* cb = bits + me.first;
       const bool fine = me.la == 0 && me.lb == 0;
       if (fine && me.w0 == 0.0 && (cb[0] & 4)) {
@@ -424,8 +534,8 @@ k_screen(const Cand* __restrict__ front, int64_t n, const PairInfo* __restrict__
     const int ctotal = __shfl_sync(0xffffffffu, cincl, 31);
     unsigned long long cbase = 0;
     if (lane == 0) {
-      atomicAdd(&out.ctr->rows, (unsigned long long)total);
-      atomicAdd(&out.ctr->screen_exact, (unsigned long long)total);
+      atomicAdd(&out.ctr->rows, (unsigned long long)all_rows);
+      atomicAdd(&out.ctr->screen_exact, (unsigned long long)nq);
       if (ctotal) cbase = atomicAdd(&out.ctr->next, (unsigned long long)ctotal);
     }
     cbase = __shfl_sync(0xffffffffu, cbase, 0);
@@ -467,11 +577,6 @@ k_screen(const Cand* __restrict__ front, int64_t n, const PairInfo* __restrict__
 //   [9] epsilon, [10] arm, [11] children (copied from the body record)
 //   [12..14] bounding-sphere centre (corner mean), [15] radius, or -1 when
 //           the triangle is a sliver (cond = Lmax^2 / |e0 x e2| > kCullCond)
-constexpr int kWorld = 16;
-constexpr double kCullCond = 1e4;
-// Relative slack of the certified cull: rows within this (times the
-// coordinate scale) of a threshold are always evaluated exactly.
-constexpr double kCullMargin = 1e-7;
 
 __global__ void k_world_count(const BodyInfo* __restrict__ bodies, int n, int64_t* cnt) {
   const int b = blockIdx.x * blockDim.x + threadIdx.x;

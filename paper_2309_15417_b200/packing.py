@@ -2,10 +2,12 @@
 
 Layout in HBM (DESIGN.md §"Data layout"):
 
-* one float64 record of 12 slots (96 B, three 32-B sectors) per surrogate
+* one float64 record of 16 slots (128 B, four 32-B sectors) per surrogate
   triangle of every body and level: the 9 body-frame corners (corner-major),
-  epsilon, arm (largest corner norm, ccd._Motion.arm, ccd.py:108-114) and the
-  (int32 first child, int32 child count) pair in slot 11.  Levels of a tree
+  epsilon, arm (largest corner norm, ccd._Motion.arm, ccd.py:108-114), the
+  (int32 first child, int32 child count) pair in slot 11, and the
+  body-frame bounding sphere (centroid, radius; -1 for slivers) in 12..15
+  that the certified cull uses.  Levels of a tree
   are re-ordered top-down so that a parent's children (the Morton groups of
   surrogate.py:99-116) are one contiguous range of the finer level: the
   traversal expands children with coalesced, index-free loads.  `tri_orig`
@@ -28,7 +30,8 @@ from dataclasses import dataclass
 import numpy as np
 
 MAX_LEVELS = 8
-RECORD = 12
+RECORD = 16
+CULL_COND = 1e4  # slivers (Lmax^2 > CULL_COND * |e0 x e2|) are never culled
 
 
 @dataclass
@@ -107,6 +110,18 @@ def _pack_tree(tree) -> PackedTree:
         recs[sl, 9] = np.asarray(lv.epsilon, dtype=np.float64)[p]
         # ccd._Motion.arm: np.linalg.norm(corners, axis=2).max(axis=1)
         recs[sl, 10] = np.linalg.norm(corners, axis=2).max(axis=1)
+        # body-frame bounding sphere for the certified cull: centroid and
+        # radius (slightly inflated), or -1 for slivers
+        cen = corners.mean(axis=1)
+        rad = np.linalg.norm(corners - cen[:, None, :], axis=2).max(axis=1) * (1.0 + 1e-12)
+        e0 = corners[:, 1] - corners[:, 0]
+        e2 = corners[:, 2] - corners[:, 0]
+        area2 = np.linalg.norm(np.cross(e0, e2), axis=1)
+        lmax2 = np.max([np.sum((corners[:, (k + 1) % 3] - corners[:, k]) ** 2, axis=1) for k in range(3)],
+                       axis=0)
+        ok = (area2 > 0.0) & (lmax2 <= CULL_COND * area2)
+        recs[sl, 12:15] = cen
+        recs[sl, 15] = np.where(ok, rad, -1.0)
         if lvl > 0:
             ch = np.zeros(len(p), dtype=np.int64)
             ch[: len(first[lvl])] = first[lvl]

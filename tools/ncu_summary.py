@@ -18,7 +18,7 @@ def source(rep):
                          capture_output=True, text=True).stdout
     r = list(csv.reader(out.splitlines()))
     hdr = r[1]
-    return [dict(zip(hdr, row)) for row in r[2:] if len(row) == len(hdr)]
+    return [dict(zip(hdr, row)) for row in r[2:] if len(row) == len(hdr) and row[0] != hdr[0]]
 
 
 KEYS = ["gpu__time_duration.sum", "sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active",
@@ -49,8 +49,11 @@ def main(rep, rows=None):
         m = re.match(r"\s*(@!?U?P\w+\s+)?([A-Z0-9_]+)", r.get("Source", ""))
         if not m:
             continue
-        cnt[m.group(2)] += int(r["Instructions Executed"] or 0)
-        th[m.group(2)] += int(r["Thread Instructions Executed"] or 0)
+        try:
+            cnt[m.group(2)] += int(r["Instructions Executed"] or 0)
+            th[m.group(2)] += int(r["Thread Instructions Executed"] or 0)
+        except ValueError:
+            continue
     tot = sum(cnt.values())
     print(f"  executed warp instructions {tot}")
     for op, c in cnt.most_common(18):
