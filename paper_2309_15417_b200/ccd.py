@@ -241,10 +241,26 @@ def _packer() -> packing.Packer:
     return pk
 
 
-def _run_problems(problems, *, widen, exhaustive=False, raw=False) -> BatchResult:
+def _run_problems(problems, *, widen, exhaustive=False, raw=False, timings=None) -> BatchResult:
+    import time
+
+    t0 = time.perf_counter()
     hs = _packer().pack(problems)
+    t1 = time.perf_counter()
     try:
-        return run_scene(DeviceScene(hs), widen=widen, exhaustive=exhaustive, raw=raw)
+        ds = DeviceScene(hs)
+        if timings is not None:
+            import torch
+
+            torch.cuda.current_stream().synchronize()
+        t2 = time.perf_counter()
+        out = run_scene(ds, widen=widen, exhaustive=exhaustive, raw=raw)
+        if timings is not None:
+            t3 = time.perf_counter()
+            timings.setdefault("pack_ms", []).append(1e3 * (t1 - t0))
+            timings.setdefault("h2d_ms", []).append(1e3 * (t2 - t1))
+            timings.setdefault("search_d2h_ms", []).append(1e3 * (t3 - t2))
+        return out
     except _lib.CapacityError:
         if len(problems) <= 1:
             raise
@@ -312,12 +328,12 @@ def compute_effective_dt(cluster, particles, statics, pairs, *,
 
 
 def earliest_contacts(pairs, dt, *, widen: float = _WIDEN, exhaustive: bool = False,
-                      raw: bool = False) -> BatchResult:
+                      raw: bool = False, timings=None) -> BatchResult:
     """Batched `pair_earliest_contact` over many independent body pairs."""
     pairs = list(pairs)
     dts = np.broadcast_to(np.asarray(dt, dtype=np.float64), (len(pairs),))
     return _run_problems([_pair_problem(a, b, d) for (a, b), d in zip(pairs, dts)],
-                         widen=widen, exhaustive=exhaustive, raw=raw)
+                         widen=widen, exhaustive=exhaustive, raw=raw, timings=timings)
 
 
 def effective_dts(clusters, particles, statics, pairs_per_cluster, *, widen: float = _WIDEN,

@@ -45,6 +45,10 @@ struct Staged {
 // Exact comparisons with zero through the bit pattern (finite x):
 // x <= 0.0 holds for -0.0 (INT64_MIN) and every negative; x >= 0.0 for +0.0,
 // -0.0 and every positive; x < 0.0 for negatives except -0.0.
+#ifndef LTSG_SIGN_INT
+#define LTSG_SIGN_INT 0
+#endif
+#if LTSG_SIGN_INT
 __device__ __forceinline__ bool le0(double x) { return __double_as_longlong(x) <= 0; }
 __device__ __forceinline__ bool ge0(double x) {
   const long long b = __double_as_longlong(x);
@@ -59,6 +63,14 @@ __device__ __forceinline__ double min_nonneg(double a, double b) {
   const unsigned long long x = __double_as_longlong(a), y = __double_as_longlong(b);
   return __longlong_as_double(x < y ? x : y);
 }
+#else
+// one DSETP each: the kernel is issue-bound, and a 64-bit integer compare
+// costs two or three integer instructions
+__device__ __forceinline__ bool le0(double x) { return x <= 0.0; }
+__device__ __forceinline__ bool ge0(double x) { return x >= 0.0; }
+__device__ __forceinline__ bool lt0(double x) { return x < 0.0; }
+__device__ __forceinline__ double min_nonneg(double a, double b) { return b < a ? b : a; }
+#endif
 
 template <int kStride>
 __device__ __forceinline__ void stage_pair(const Staged<kStride>& st, const Tri& a, const Tri& b) {

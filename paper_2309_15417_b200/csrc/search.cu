@@ -675,7 +675,7 @@ __device__ __forceinline__ bool sphere_cull(const double* wa, const double* wb, 
 constexpr int kStaticWarps = 4;
 constexpr int kStaticStageBytes = kStaged * 32 * kStaticWarps * sizeof(double);
 #ifndef LTSG_STATIC_MINB
-#define LTSG_STATIC_MINB 4
+#define LTSG_STATIC_MINB 5
 #endif
 
 // Static batches (every problem has dt = 0) run a leaner traversal.  Every
@@ -737,11 +737,36 @@ k_screen_static(const Cand* __restrict__ front, int64_t n, const PairInfo* __res
                 const BodyInfo* __restrict__ bodies, const double* __restrict__ world,
                 const int64_t* __restrict__ woff, ScreenOut out) {
   extern __shared__ double s_stage[];  // kStaged x (32 * kStaticWarps)
-  __shared__ ChildInfo s_child[kStaticWarps][32];
   const Staged<32 * kStaticWarps> st{s_stage + threadIdx.x};
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
-  ChildInfo* kid = s_child[warp];
+  // Child descriptors live in the first four stage rows of the warp's own
+  // columns once the rows are evaluated (no extra shared memory: five
+  // blocks fit per SM).
+  auto put_kid = [&](const ChildInfo& c) {
+    int2* col = reinterpret_cast<int2*>(s_stage + threadIdx.x);
+    col[0 * 32 * kStaticWarps] = make_int2(c.first, c.count);
+    col[1 * 32 * kStaticWarps] = make_int2(c.pair, c.ia0);
+    col[2 * 32 * kStaticWarps] = make_int2(c.ib0, c.nb);
+    col[3 * 32 * kStaticWarps] = make_int2(c.la, c.lb);
+  };
+  auto kid_first = [&](int o) { return reinterpret_cast<const int2*>(s_stage + warp * 32 + o)[0].x; };
+  auto get_kid = [&](int o) {
+    const int2* col = reinterpret_cast<const int2*>(s_stage + warp * 32 + o);
+    ChildInfo c;
+    const int2 a = col[0], b = col[1 * 32 * kStaticWarps], d = col[2 * 32 * kStaticWarps],
+               e = col[3 * 32 * kStaticWarps];
+    c.first = a.x;
+    c.count = a.y;
+    c.pair = b.x;
+    c.ia0 = b.y;
+    c.ib0 = d.x;
+    c.nb = d.y;
+    c.la = e.x;
+    c.lb = e.y;
+    c.w0 = 0.0;
+    return c;
+  };
   const int64_t n_warps = (n + 31) / 32;
   for (int64_t wi = blockIdx.x * (int64_t)kStaticWarps + warp; wi < n_warps;
        wi += (int64_t)gridDim.x * kStaticWarps) {
@@ -791,7 +816,8 @@ k_screen_static(const Cand* __restrict__ front, int64_t n, const PairInfo* __res
     }
     if (ctotal) {
       ch.first = cincl - ch.count;
-      kid[lane] = ch;
+      __syncwarp();  // every lane is done with its stage rows
+      put_kid(ch);
       __syncwarp();
       unsigned long long culled = 0;
       for (int s0 = 0; s0 < ctotal; s0 += 32) {
@@ -802,8 +828,8 @@ k_screen_static(const Cand* __restrict__ front, int64_t n, const PairInfo* __res
           int o = 0;
 #pragma unroll
           for (int step = 16; step > 0; step >>= 1)
-            if (kid[o + step].first <= s) o += step;
-          const ChildInfo& k = kid[o];
+            if (kid_first(o + step) <= s) o += step;
+          const ChildInfo k = get_kid(o);
           const int jj = s - k.first;
           nc.pair = k.pair;
           nc.ia = k.ia0 + jj / k.nb;

@@ -190,27 +190,53 @@ class Packer:
         self._static = None
 
     def pack(self, problems) -> HostScene:
-        bodies, pair_body, pair_problem, pair_group, dts, tbs = _tables(problems)
+        # problem structure (which body objects pair up how) is cached too:
+        # an engine re-screens the same clusters every sweep with new states
+        skey = tuple((tuple((id(a), id(b)) for a, b in pairs)) for pairs, _dt, _tb in problems)
+        if skey != getattr(self, "_skey", None):
+            self._tables = _tables(problems)
+            self._skey = skey
+        bodies, pair_body, pair_problem, pair_group, _d, _t = self._tables
+        dts = np.fromiter((float(dt) for _p, dt, _tb in problems), dtype=np.float64, count=len(problems))
+        tbs = np.fromiter((float(tb) for _p, _dt, tb in problems), dtype=np.float64, count=len(problems))
         key = tuple(id(b.tree) for b in bodies)
         if key != self._key:
             self._static = _assemble_static(bodies, self.pinned)
             self._key = key
             self._trees = [b.tree for b in bodies]  # keep ids alive while cached
+            self._pair_arrays = (np.asarray(pair_body, dtype=np.int32).reshape(-1, 2),
+                                 np.asarray(pair_problem, dtype=np.int32),
+                                 np.asarray(pair_group, dtype=np.int32))
         tris, orig, lev, max_children = self._static
-        state = _pinned((len(bodies), 16), np.float64) if self.pinned else np.empty((len(bodies), 16))
-        ids = np.empty(len(bodies), dtype=np.int64)
-        for i, b in enumerate(bodies):
-            state[i] = body_state_row(b)
-            ids[i] = body_id(b)
+        state = _states(bodies, self.pinned)
+        ids = np.fromiter((body_id(b) for b in bodies), dtype=np.int64, count=len(bodies))
         lev = lev.copy()
         lev[:, 1] = ids
+        pb, pp, pg = self._pair_arrays
         return HostScene(
             tris=tris, tri_orig=orig, body_state=state, body_levels=lev,
-            pair_body=np.asarray(pair_body, dtype=np.int32).reshape(-1, 2),
-            pair_problem=np.asarray(pair_problem, dtype=np.int32),
-            pair_group=np.asarray(pair_group, dtype=np.int32),
-            problem_dt=np.asarray(dts, dtype=np.float64), problem_tbase=np.asarray(tbs, dtype=np.float64),
+            pair_body=pb, pair_problem=pp, pair_group=pg,
+            problem_dt=dts, problem_tbase=tbs,
             max_children=max_children, n_problems=len(dts), body_ids=ids)
+
+
+def _states(bodies, pinned):
+    """Body snapshot rows (body_state_row for every body), vectorised."""
+    n = len(bodies)
+    state = _pinned((n, 16), np.float64) if pinned else np.empty((n, 16))
+    state.fill(0.0)
+    dyn = [i for i, b in enumerate(bodies) if hasattr(b, "timeline")]
+    if dyn:
+        cur = [bodies[i].timeline.current for i in dyn]
+        state[dyn, 0:3] = np.array([c.position for c in cur], dtype=np.float64)
+        state[dyn, 3:6] = np.array([c.velocity for c in cur], dtype=np.float64)
+        state[dyn, 6:10] = np.array([c.rotation for c in cur], dtype=np.float64)
+        state[dyn, 10:13] = np.array([c.angular_velocity for c in cur], dtype=np.float64)
+    if len(dyn) < n:
+        stat = np.ones(n, dtype=bool)
+        stat[dyn] = False
+        state[stat, 13] = 1.0
+    return state
 
 
 def _pinned(shape, dtype):
