@@ -252,6 +252,8 @@ struct ChildInfo {
 struct ScreenOut {
   Cand* next;
   unsigned long long next_cap;
+  const unsigned long long* n_in;  // frontier size on the device (async mode) or null
+  unsigned long long* n_out;       // next-frontier counter
   RestRec* resting;
   unsigned long long rest_cap;
   Entry* entries;
@@ -323,6 +325,7 @@ __device__ __forceinline__ double sphere_gap(const BodyInfo& A, const double* ra
 __global__ void __launch_bounds__(32 * kScreenWarps, LTSG_SCREEN_MINB)
 k_screen(const Cand* __restrict__ front, int64_t n, const PairInfo* __restrict__ pairs,
          const BodyInfo* __restrict__ bodies, const double* __restrict__ tris, ScreenOut out) {
+  if (out.n_in) n = (int64_t)min(*out.n_in, out.next_cap);
   __shared__ union {  // per warp: candidate info, later reused for child descriptors
     CandInfo cand[32];
     ChildInfo child[32];
@@ -536,7 +539,7 @@ k_screen(const Cand* __restrict__ front, int64_t n, const PairInfo* __restrict__
     if (lane == 0) {
       atomicAdd(&out.ctr->rows, (unsigned long long)all_rows);
       atomicAdd(&out.ctr->screen_exact, (unsigned long long)nq);
-      if (ctotal) cbase = atomicAdd(&out.ctr->next, (unsigned long long)ctotal);
+      if (ctotal) cbase = atomicAdd(out.n_out, (unsigned long long)ctotal);
     }
     cbase = __shfl_sync(0xffffffffu, cbase, 0);
     if (ctotal) {
@@ -619,8 +622,9 @@ __global__ void k_world_fill(const BodyInfo* __restrict__ bodies, int n, const i
         *reinterpret_cast<int2*>(w + 11) = ch;
       }
       // bounding sphere (approximate arithmetic; the cull margin absorbs it)
-      const V3 c{(t.v[0].x + t.v[1].x + t.v[2].x) / 3.0, (t.v[0].y + t.v[1].y + t.v[2].y) / 3.0,
-                 (t.v[0].z + t.v[1].z + t.v[2].z) / 3.0};
+      constexpr double kThird = 1.0 / 3.0;
+      const V3 c{(t.v[0].x + t.v[1].x + t.v[2].x) * kThird, (t.v[0].y + t.v[1].y + t.v[2].y) * kThird,
+                 (t.v[0].z + t.v[1].z + t.v[2].z) * kThird};
       double r2 = 0.0, l2 = 0.0;
 #pragma unroll
       for (int k = 0; k < 3; ++k) {
@@ -697,7 +701,7 @@ __device__ __forceinline__ bool static_child_cull(const double* world, int32_t w
 __global__ void k_seed_static(const PairInfo* __restrict__ pairs, int64_t n_pairs,
                               const BodyInfo* __restrict__ bodies, const int64_t* __restrict__ woff,
                               const double* __restrict__ world, Cand* out, unsigned long long cap,
-                              Counters* ctr) {
+                              Counters* ctr, unsigned long long* n_out) {
   const int lane = threadIdx.x & 31;
   for (int64_t k = blockIdx.x; k < n_pairs; k += gridDim.x) {
     const PairInfo p = pairs[k];
@@ -721,7 +725,7 @@ __global__ void k_seed_static(const PairInfo* __restrict__ pairs, int64_t n_pair
       unsigned long long base = 0;
       if (lane == 0) {
         atomicAdd(&ctr->rows, (unsigned long long)(nvalid - __popc(m)));
-        if (m) base = atomicAdd(&ctr->next, (unsigned long long)__popc(m));
+        if (m) base = atomicAdd(n_out, (unsigned long long)__popc(m));
       }
       base = __shfl_sync(0xffffffffu, base, 0);
       if (keep) {
@@ -736,6 +740,7 @@ __global__ void __launch_bounds__(32 * kStaticWarps, LTSG_STATIC_MINB)
 k_screen_static(const Cand* __restrict__ front, int64_t n, const PairInfo* __restrict__ pairs,
                 const BodyInfo* __restrict__ bodies, const double* __restrict__ world,
                 const int64_t* __restrict__ woff, ScreenOut out) {
+  if (out.n_in) n = (int64_t)min(*out.n_in, out.next_cap);
   extern __shared__ double s_stage[];  // kStaged x (32 * kStaticWarps)
   const Staged<32 * kStaticWarps> st{s_stage + threadIdx.x};
   const int warp = threadIdx.x >> 5;
@@ -843,7 +848,7 @@ k_screen_static(const Cand* __restrict__ front, int64_t n, const PairInfo* __res
         const int nvalid = ctotal - s0 < 32 ? ctotal - s0 : 32;
         culled += (unsigned long long)(nvalid - __popc(m));
         unsigned long long base = 0;
-        if (lane == 0 && m) base = atomicAdd(&out.ctr->next, (unsigned long long)__popc(m));
+        if (lane == 0 && m) base = atomicAdd(out.n_out, (unsigned long long)__popc(m));
         base = __shfl_sync(0xffffffffu, base, 0);
         if (keep) {
           const unsigned long long dst = base + __popc(m & ((1u << lane) - 1u));
@@ -1157,6 +1162,9 @@ k_fuse_block(Soa o, int64_t* __restrict__ idx, const int64_t* __restrict__ g_off
   __shared__ int64_t s_gi[kFuseCap];
   __shared__ double s_p[3][kFuseCap];
   __shared__ double s_thr[kFuseCap];
+  __shared__ double s_n[3][kFuseCap];
+  __shared__ double s_dep[kFuseCap];
+  __shared__ double s_tt[kFuseCap];
   __shared__ int32_t s_par[kFuseCap];
   __shared__ int32_t s_slot[kFuseCap];
   __shared__ uint32_t s_adj[kFuseCap * kFuseWords];
@@ -1197,6 +1205,11 @@ k_fuse_block(Soa o, int64_t* __restrict__ idx, const int64_t* __restrict__ g_off
       s_p[1][rank] = o.position[3 * a + 1];
       s_p[2][rank] = o.position[3 * a + 2];
       s_thr[rank] = o.threshold[a];
+      s_n[0][rank] = o.normal[3 * a];
+      s_n[1][rank] = o.normal[3 * a + 1];
+      s_n[2][rank] = o.normal[3 * a + 2];
+      s_dep[rank] = o.depth[a];
+      s_tt[rank] = o.t[a];
     }
     __syncthreads();
     for (int r = tid; r < n; r += kFuseThreads) ix[r] = s_gi[r];  // canonical raw order
@@ -1246,30 +1259,29 @@ k_fuse_block(Soa o, int64_t* __restrict__ idx, const int64_t* __restrict__ g_off
     for (int r = tid; r < n; r += kFuseThreads) {
       if (s_par[r] != r) continue;
       V3 ps{0, 0, 0}, ns{0, 0, 0};
-      int cnt = 0;
-      int64_t rep = -1, first = -1;
+      int cnt = 0, rep = -1, first = -1;
       double dmax = 0.0, tmin = 0.0, thr = 0.0;
       for (int i = 0; i < n; ++i) {  // members in ascending sorted order (ccd.py:557-558)
         if (s_par[i] != r) continue;
-        const int64_t a = s_gi[i];
         const V3 pp{s_p[0][i], s_p[1][i], s_p[2][i]};
-        const V3 nn{o.normal[3 * a], o.normal[3 * a + 1], o.normal[3 * a + 2]};
-        const double da = o.depth[a], ta = o.t[a], tha = o.threshold[a];
+        const V3 nn{s_n[0][i], s_n[1][i], s_n[2][i]};
+        const double da = s_dep[i], ta = s_tt[i], tha = s_thr[i];
         if (cnt == 0) {
-          first = a;
-          rep = a;
+          first = i;
+          rep = i;
           ps = pp;
           ns = nn;
           dmax = da;
           tmin = ta;
           thr = tha;
         } else {
-          ps = ps + pp;
+          ps = ps + pp;  // np.mean / np.sum over axis 0: sequential
           ns = ns + nn;
           if (da > dmax) dmax = da;
           if (ta < tmin) tmin = ta;
           if (tha > thr) thr = tha;
-          if (ta < o.t[rep] || (ta == o.t[rep] && -da < -o.depth[rep])) rep = a;
+          // min(group, key=(t, -depth)): the first strictly smaller wins
+          if (ta < s_tt[rep] || (ta == s_tt[rep] && -da < -s_dep[rep])) rep = i;
         }
         ++cnt;
       }
@@ -1280,12 +1292,13 @@ k_fuse_block(Soa o, int64_t* __restrict__ idx, const int64_t* __restrict__ g_off
       if (ln > 1e-12) {
         nrm = V3{dv(ns.x, ln), dv(ns.y, ln), dv(ns.z, ln)};
       } else {
-        nrm = V3{o.normal[3 * first], o.normal[3 * first + 1], o.normal[3 * first + 2]};
+        nrm = V3{s_n[0][first], s_n[1][first], s_n[2][first]};
       }
+      const int64_t ra = s_gi[rep];
       const int64_t dst = off + s_slot[r];
-      f.problem[dst] = o.problem[rep];
-      f.body_a[dst] = o.body_a[rep];
-      f.body_b[dst] = o.body_b[rep];
+      f.problem[dst] = o.problem[ra];
+      f.body_a[dst] = o.body_a[ra];
+      f.body_b[dst] = o.body_b[ra];
       f.position[3 * dst] = pos.x;
       f.position[3 * dst + 1] = pos.y;
       f.position[3 * dst + 2] = pos.z;
@@ -1294,8 +1307,8 @@ k_fuse_block(Soa o, int64_t* __restrict__ idx, const int64_t* __restrict__ g_off
       f.normal[3 * dst + 2] = nrm.z;
       f.depth[dst] = dmax;
       f.t[dst] = tmin;
-      f.tri_a[dst] = o.tri_a[rep];
-      f.tri_b[dst] = o.tri_b[rep];
+      f.tri_a[dst] = o.tri_a[ra];
+      f.tri_b[dst] = o.tri_b[ra];
       f.threshold[dst] = thr;
     }
     if (tid == 0) {
@@ -1682,96 +1695,162 @@ static int run_search(const ltsg_scene* sc, ltsg_result* out, ltsg_workspace* ws
     }
   }
 
-  // ---- seeds: all root x root pairs (fine x fine when exhaustive), ccd.py:385-391
-  int64_t n_front = 0;
-  const char* fname[2] = {"front0", "front1"};
-  int fsel = 0;
-  Cand* front = nullptr;
+  // ---- traversal: seeds (ccd.py:385-391) and generations (ccd.py:393-446).
+  // Async mode enqueues every generation back to back (frontier sizes stay
+  // on the device, buffers are sized from the workspace's history) and
+  // checks once at the end; on any overflow the traversal re-runs in sync
+  // mode, which reads each frontier size back and grows buffers as needed.
+  int64_t seed_total = 0;
+  int64_t *seed_cnt = nullptr, *seed_off = nullptr;
   if (sc->n_pairs > 0) {
-    int64_t *cnt, *off;
-    LTSG_TRY(ws_get(ws, "seed_cnt", (size_t)sc->n_pairs + 1, &cnt));
-    LTSG_TRY(ws_get(ws, "seed_off", (size_t)sc->n_pairs + 1, &off));
+    LTSG_TRY(ws_get(ws, "seed_cnt", (size_t)sc->n_pairs + 1, &seed_cnt));
+    LTSG_TRY(ws_get(ws, "seed_off", (size_t)sc->n_pairs + 1, &seed_off));
     k_seed_count<<<grid_for(sc->n_pairs, 128), 128, 0, st>>>(pr.pairs, sc->n_pairs, pr.bodies,
-                                                             sc->exhaustive, cnt);
+                                                             sc->exhaustive, seed_cnt);
     LTSG_LAUNCHED();
-    LTSG_CUDA(cudaMemsetAsync(cnt + sc->n_pairs, 0, sizeof(int64_t), st));
-    LTSG_TRY(scan_exclusive(ws, cnt, off, sc->n_pairs + 1, st));
-    LTSG_CUDA(cudaMemcpyAsync(&n_front, off + sc->n_pairs, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+    LTSG_CUDA(cudaMemsetAsync(seed_cnt + sc->n_pairs, 0, sizeof(int64_t), st));
+    LTSG_TRY(scan_exclusive(ws, seed_cnt, seed_off, sc->n_pairs + 1, st));
+    LTSG_CUDA(cudaMemcpyAsync(&seed_total, seed_off + sc->n_pairs, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
     LTSG_CUDA(cudaStreamSynchronize(st));
-    LTSG_TRY(ws_get(ws, fname[fsel], (size_t)n_front, &front));
-    if (all_static) {
-      k_seed_static<<<(int)std::min<int64_t>(sc->n_pairs, 148 * 16), 128, 0, st>>>(
-          pr.pairs, sc->n_pairs, pr.bodies, woff, world, front, (unsigned long long)n_front, d_ctr);
-      LTSG_LAUNCHED();
-      Counters hs;
-      LTSG_TRY(read_ctr(d_ctr, &hs, st));
-      n_front = (int64_t)hs.next;
-      hs.next = 0;
-      LTSG_CUDA(cudaMemcpyAsync(d_ctr, &hs, sizeof(Counters), cudaMemcpyHostToDevice, st));
-    } else {
-      k_seed_fill<<<(int)std::min<int64_t>(sc->n_pairs, 148 * 16), 128, 0, st>>>(
-          pr.pairs, sc->n_pairs, pr.bodies, sc->exhaustive, off, front);
-      LTSG_LAUNCHED();
-    }
   }
-
-  // ---- generations
-  size_t rest_cap = 1 << 16, entry_cap = 1 << 14, cross_cap = 1 << 14;
+  constexpr int kMaxGen = 2 * kMaxLevels;
+  unsigned long long* gen_cnt;
+  LTSG_TRY(ws_get(ws, "gen_cnt", kMaxGen + 1, &gen_cnt));
+  const int64_t fan = (int64_t)sc->max_children * sc->max_children;
+  size_t rest_cap = std::max<size_t>(1 << 16, ws->hint_rest), entry_cap = std::max<size_t>(1 << 14, ws->hint_entries),
+         cross_cap = std::max<size_t>(1 << 14, ws->hint_cross);
   RestRec* resting;
   Entry* entries;
   Cross* cross;
-  LTSG_TRY(ws_get(ws, "resting", rest_cap, &resting));
-  LTSG_TRY(ws_get(ws, "entries", entry_cap, &entries));
-  LTSG_TRY(ws_get(ws, "cross", cross_cap, &cross));
   Counters h{};
-  LTSG_TRY(read_ctr(d_ctr, &h, st));
-  const int64_t fan = (int64_t)sc->max_children * sc->max_children;
-  while (n_front > 0) {
-    Cand* next;
-    LTSG_TRY(ws_get(ws, fname[fsel ^ 1], (size_t)(n_front * fan), &next));
-    Counters before = h;
-    before.next = 0;
-    for (;;) {
-      LTSG_CUDA(cudaMemcpyAsync(d_ctr, &before, sizeof(Counters), cudaMemcpyHostToDevice, st));
-      ScreenOut so{next, (unsigned long long)(n_front * fan), resting, rest_cap, entries, entry_cap,
-                   cross, cross_cap, d_ctr};
-      t_screen.start(st);
-      if (all_static) {
-        const int64_t blocks = (n_front + 32 * kStaticWarps - 1) / (32 * kStaticWarps);
-        k_screen_static<<<(int)std::max<int64_t>(1, std::min<int64_t>(blocks, 148LL * 32)), 32 * kStaticWarps,
-                          kStaticStageBytes, st>>>(front, n_front, pr.pairs, pr.bodies, world, woff, so);
-      } else {
-        k_screen<<<screen_grid(n_front), 32 * kScreenWarps, kScreenStageBytes, st>>>(
-            front, n_front, pr.pairs, pr.bodies, sc->tris, so);
-      }
-      LTSG_LAUNCHED();
-      t_screen.stop(st);
-      LTSG_TRY(read_ctr(d_ctr, &h, st));
-      out->ms_screen += t_screen.ms();
-      bool grow = false;
-      if (h.resting > rest_cap) {
-        rest_cap = (size_t)h.resting * 2;
-        LTSG_TRY(ws_get(ws, "resting", rest_cap, &resting, true));
-        grow = true;
-      }
-      if (h.entries > entry_cap) {
-        entry_cap = (size_t)h.entries * 2;
-        LTSG_TRY(ws_get(ws, "entries", entry_cap, &entries, true));
-        grow = true;
-      }
-      if (h.cross > cross_cap) {
-        cross_cap = (size_t)h.cross * 2;
-        LTSG_TRY(ws_get(ws, "cross", cross_cap, &cross, true));
-        grow = true;
-      }
-      if (!grow) break;
+  Cand* front = nullptr;
+
+  auto launch_screen = [&](const Cand* in, int64_t n, const unsigned long long* n_in, Cand* next,
+                           unsigned long long cap, unsigned long long* n_out) -> int {
+    ScreenOut so{next, cap, n_in, n_out, resting, rest_cap, entries, entry_cap, cross, cross_cap, d_ctr};
+    if (all_static) {
+      // async: the frontier size is unknown on the host; a generous grid lets
+      // the block scheduler balance uneven rows (spare blocks exit at once)
+      const int64_t blocks = n_in ? 148LL * 16 : (n + 32 * kStaticWarps - 1) / (32 * kStaticWarps);
+      k_screen_static<<<(int)std::max<int64_t>(1, std::min<int64_t>(blocks, 148LL * 32)), 32 * kStaticWarps,
+                        kStaticStageBytes, st>>>(in, n, pr.pairs, pr.bodies, world, woff, so);
+    } else {
+      const int grid = n_in ? 148 * 32 : screen_grid(n);
+      k_screen<<<grid, 32 * kScreenWarps, kScreenStageBytes, st>>>(in, n, pr.pairs, pr.bodies, sc->tris, so);
     }
-    out->candidates += n_front;
-    out->generations += 1;
-    n_front = (int64_t)h.next;
-    fsel ^= 1;
-    front = next;
+    LTSG_LAUNCHED();
+    return LTSG_OK;
+  };
+
+  auto traverse = [&](bool async_mode, bool* overflow) -> int {
+    *overflow = false;
+    LTSG_CUDA(cudaMemsetAsync(d_ctr, 0, sizeof(Counters), st));
+    LTSG_CUDA(cudaMemsetAsync(gen_cnt, 0, sizeof(unsigned long long) * (kMaxGen + 1), st));
+    LTSG_TRY(ws_get(ws, "resting", rest_cap, &resting));
+    LTSG_TRY(ws_get(ws, "entries", entry_cap, &entries));
+    LTSG_TRY(ws_get(ws, "cross", cross_cap, &cross));
+    out->candidates = 0;
+    out->generations = 0;
+    out->ms_screen = 0.0;
+    if (sc->n_pairs == 0) return LTSG_OK;
+    const size_t cap_async = std::max<size_t>((size_t)(1.25 * (double)ws->hint_front) + 1024, (size_t)seed_total);
+    LTSG_TRY(ws_get(ws, "front0", async_mode ? cap_async : (size_t)seed_total, &front));
+    if (all_static) {
+      k_seed_static<<<(int)std::min<int64_t>(sc->n_pairs, 148 * 16), 128, 0, st>>>(
+          pr.pairs, sc->n_pairs, pr.bodies, woff, world, front, (unsigned long long)seed_total, d_ctr, gen_cnt);
+    } else {
+      k_seed_fill<<<(int)std::min<int64_t>(sc->n_pairs, 148 * 16), 128, 0, st>>>(
+          pr.pairs, sc->n_pairs, pr.bodies, sc->exhaustive, seed_off, front);
+      LTSG_CUDA(cudaMemcpyAsync(gen_cnt, &seed_total, sizeof(unsigned long long), cudaMemcpyHostToDevice, st));
+    }
+    LTSG_LAUNCHED();
+    if (async_mode) {
+      Cand* buf[2];
+      buf[0] = front;
+      LTSG_TRY(ws_get(ws, "front1", cap_async, &buf[1]));
+      t_screen.start(st);
+      for (int g = 1; g <= kMaxGen; ++g)
+        LTSG_TRY(launch_screen(buf[(g - 1) & 1], 0, gen_cnt + g - 1, buf[g & 1], cap_async, gen_cnt + g));
+      t_screen.stop(st);
+      unsigned long long hg[kMaxGen + 1];
+      LTSG_CUDA(cudaMemcpyAsync(hg, gen_cnt, sizeof(hg), cudaMemcpyDeviceToHost, st));
+      LTSG_TRY(read_ctr(d_ctr, &h, st));
+      out->ms_screen = t_screen.ms();
+      for (int g = 0; g <= kMaxGen; ++g) {
+        if (hg[g] > cap_async) *overflow = true;
+        if (g < kMaxGen && hg[g] > 0) {
+          out->candidates += (int64_t)hg[g];
+          out->generations += 1;
+        }
+      }
+      if (hg[kMaxGen] > 0) *overflow = true;  // deeper than the generation budget
+      if (h.resting > rest_cap || h.entries > entry_cap || h.cross > cross_cap) *overflow = true;
+      return LTSG_OK;
+    }
+    // sync mode
+    unsigned long long n_first = 0;
+    LTSG_CUDA(cudaMemcpyAsync(&n_first, gen_cnt, sizeof(n_first), cudaMemcpyDeviceToHost, st));
+    LTSG_TRY(read_ctr(d_ctr, &h, st));
+    int64_t n_front = (int64_t)n_first;
+    int fsel = 0;
+    const char* fname[2] = {"front0", "front1"};
+    size_t max_front = (size_t)n_front;
+    while (n_front > 0) {
+      Cand* next;
+      LTSG_TRY(ws_get(ws, fname[fsel ^ 1], (size_t)(n_front * fan), &next));
+      Counters before = h;
+      for (;;) {
+        LTSG_CUDA(cudaMemcpyAsync(d_ctr, &before, sizeof(Counters), cudaMemcpyHostToDevice, st));
+        LTSG_CUDA(cudaMemsetAsync(gen_cnt + 1, 0, sizeof(unsigned long long), st));
+        t_screen.start(st);
+        LTSG_TRY(launch_screen(front, n_front, nullptr, next, (unsigned long long)(n_front * fan), gen_cnt + 1));
+        t_screen.stop(st);
+        LTSG_TRY(read_ctr(d_ctr, &h, st));
+        out->ms_screen += t_screen.ms();
+        bool grow = false;
+        if (h.resting > rest_cap) {
+          rest_cap = (size_t)h.resting * 2;
+          LTSG_TRY(ws_get(ws, "resting", rest_cap, &resting, true));
+          grow = true;
+        }
+        if (h.entries > entry_cap) {
+          entry_cap = (size_t)h.entries * 2;
+          LTSG_TRY(ws_get(ws, "entries", entry_cap, &entries, true));
+          grow = true;
+        }
+        if (h.cross > cross_cap) {
+          cross_cap = (size_t)h.cross * 2;
+          LTSG_TRY(ws_get(ws, "cross", cross_cap, &cross, true));
+          grow = true;
+        }
+        if (!grow) break;
+      }
+      unsigned long long nn = 0;
+      LTSG_CUDA(cudaMemcpyAsync(&nn, gen_cnt + 1, sizeof(nn), cudaMemcpyDeviceToHost, st));
+      LTSG_CUDA(cudaStreamSynchronize(st));
+      out->candidates += n_front;
+      out->generations += 1;
+      n_front = (int64_t)nn;
+      max_front = std::max(max_front, (size_t)n_front);
+      fsel ^= 1;
+      front = next;
+    }
+    ws->hint_front = std::max(ws->hint_front, max_front);
+    return LTSG_OK;
+  };
+
+  bool overflow = false;
+  const bool try_async = ws->hint_front > 0 && !getenv("LTSG_SYNC");
+  LTSG_TRY(traverse(try_async, &overflow));
+  if (overflow) {
+    rest_cap = std::max(rest_cap, (size_t)h.resting * 2);
+    entry_cap = std::max(entry_cap, (size_t)h.entries * 2);
+    cross_cap = std::max(cross_cap, (size_t)h.cross * 2);
+    LTSG_TRY(traverse(false, &overflow));
   }
+  ws->hint_rest = std::max(ws->hint_rest, (size_t)h.resting);
+  ws->hint_entries = std::max(ws->hint_entries, (size_t)h.entries);
+  ws->hint_cross = std::max(ws->hint_cross, (size_t)h.cross);
 
   // ---- certified zoom + bisection
   t_refine.start(st);
