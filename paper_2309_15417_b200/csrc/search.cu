@@ -593,52 +593,64 @@ __global__ void k_world_count(const BodyInfo* __restrict__ bodies, int n, int64_
   cnt[b] = B.level_off[top] + B.level_size[top] - B.level_off[0];
 }
 
-__global__ void k_world_fill(const BodyInfo* __restrict__ bodies, int n, const int64_t* __restrict__ woff,
-                             const double* __restrict__ tris, double* __restrict__ world) {
+__global__ void __launch_bounds__(128) k_world_fill(const BodyInfo* __restrict__ bodies, int n,
+                                                    const int64_t* __restrict__ woff,
+                                                    const double* __restrict__ tris, double* __restrict__ world) {
+  // 128 records per block iteration, moved through shared memory so that both
+  // the record loads and the world-record stores are fully coalesced.
+  __shared__ double s_rec[128 * kRecord];
   for (int b = blockIdx.x; b < n; b += gridDim.x) {
     const BodyInfo& B = bodies[b];
     const int64_t cnt = woff[b + 1] - woff[b];
     double pos[3];
     position_at(B.m, 0.0, pos);
-    for (int64_t j = threadIdx.x; j < cnt; j += blockDim.x) {
-      const double* r = tris + (size_t)(B.level_off[0] + j) * kRecord;
-      double L[9];
-      load_local(r, L);
-      const Tri t = world_tri(B.m.base, pos, L);
-      double* w = world + (size_t)(woff[b] + j) * kWorld;
+    for (int64_t j0 = 0; j0 < cnt; j0 += 128) {
+      const int m = (int)min((int64_t)128, cnt - j0);
+      const double2* src = reinterpret_cast<const double2*>(tris + (size_t)(B.level_off[0] + j0) * kRecord);
+      double2* sm2 = reinterpret_cast<double2*>(s_rec);
+      for (int k = threadIdx.x; k < m * kRecord / 2; k += blockDim.x) sm2[k] = __ldg(src + k);
+      __syncthreads();
+      if (threadIdx.x < m) {
+        const int64_t j = j0 + threadIdx.x;
+        double* r = s_rec + threadIdx.x * kRecord;
+        double L[9];
 #pragma unroll
-      for (int k = 0; k < 3; ++k) {
-        w[3 * k] = t.v[k].x;
-        w[3 * k + 1] = t.v[k].y;
-        w[3 * k + 2] = t.v[k].z;
-      }
-      w[9] = r[9];
-      w[10] = r[10];
-      {  // first child as an absolute world index (children are contiguous)
-        int lvl = 0;
-        while (lvl + 1 < B.n_levels && B.level_off[0] + j >= B.level_off[lvl + 1]) ++lvl;
-        int2 ch = *reinterpret_cast<const int2*>(r + 11);
-        if (lvl > 0) ch.x = (int32_t)(woff[b] + B.level_off[lvl - 1] - B.level_off[0] + ch.x);
-        *reinterpret_cast<int2*>(w + 11) = ch;
-      }
-      // bounding sphere (approximate arithmetic; the cull margin absorbs it)
-      constexpr double kThird = 1.0 / 3.0;
-      const V3 c{(t.v[0].x + t.v[1].x + t.v[2].x) * kThird, (t.v[0].y + t.v[1].y + t.v[2].y) * kThird,
-                 (t.v[0].z + t.v[1].z + t.v[2].z) * kThird};
-      double r2 = 0.0, l2 = 0.0;
+        for (int k = 0; k < 9; ++k) L[k] = r[k];
+        const Tri t = world_tri(B.m.base, pos, L);
+        double* w = r;  // in place: same 16-slot layout
 #pragma unroll
-      for (int k = 0; k < 3; ++k) {
-        const V3 d = t.v[k] - c;
-        r2 = fmax(r2, d.x * d.x + d.y * d.y + d.z * d.z);
-        const V3 e = t.v[(k + 1) % 3] - t.v[k];
-        l2 = fmax(l2, e.x * e.x + e.y * e.y + e.z * e.z);
+        for (int k = 0; k < 3; ++k) {
+          w[3 * k] = t.v[k].x;
+          w[3 * k + 1] = t.v[k].y;
+          w[3 * k + 2] = t.v[k].z;
+        }
+        {  // first child as an absolute world index (children are contiguous)
+          int lvl = 0;
+          while (lvl + 1 < B.n_levels && B.level_off[0] + j >= B.level_off[lvl + 1]) ++lvl;
+          int2 ch = *reinterpret_cast<const int2*>(r + 11);
+          if (lvl > 0) ch.x = (int32_t)(woff[b] + B.level_off[lvl - 1] - B.level_off[0] + ch.x);
+          *reinterpret_cast<int2*>(w + 11) = ch;
+        }
+        // bounding sphere in world coordinates (approximate; the cull margin absorbs it)
+        const double rad = r[15];
+        constexpr double kThird = 1.0 / 3.0;
+        const V3 c{(t.v[0].x + t.v[1].x + t.v[2].x) * kThird, (t.v[0].y + t.v[1].y + t.v[2].y) * kThird,
+                   (t.v[0].z + t.v[1].z + t.v[2].z) * kThird};
+        double r2 = 0.0;
+#pragma unroll
+        for (int k = 0; k < 3; ++k) {
+          const V3 d = t.v[k] - c;
+          r2 = fmax(r2, d.x * d.x + d.y * d.y + d.z * d.z);
+        }
+        w[12] = c.x;
+        w[13] = c.y;
+        w[14] = c.z;
+        w[15] = rad >= 0.0 ? sqrt(r2) * (1.0 + 1e-12) : -1.0;  // sliver flag from the body record
       }
-      const V3 x = cross(t.v[1] - t.v[0], t.v[2] - t.v[0]);
-      const double area2 = sqrt(x.x * x.x + x.y * x.y + x.z * x.z);
-      w[12] = c.x;
-      w[13] = c.y;
-      w[14] = c.z;
-      w[15] = (area2 > 0.0 && l2 <= kCullCond * area2) ? sqrt(r2) * (1.0 + 1e-12) : -1.0;
+      __syncthreads();
+      double2* dst = reinterpret_cast<double2*>(world + (size_t)(woff[b] + j0) * kWorld);
+      for (int k = threadIdx.x; k < m * kWorld / 2; k += blockDim.x) dst[k] = sm2[k];
+      __syncthreads();
     }
   }
 }
@@ -1169,6 +1181,7 @@ k_fuse_block(Soa o, int64_t* __restrict__ idx, const int64_t* __restrict__ g_off
   __shared__ int32_t s_slot[kFuseCap];
   __shared__ uint32_t s_adj[kFuseCap * kFuseWords];
   __shared__ int32_t s_nroots;
+  __shared__ uint32_t s_lab[kFuseWords];
   const int tid = threadIdx.x;
   for (int64_t g = blockIdx.x; g < n_groups; g += gridDim.x) {
     const int64_t off = g_off[g];
@@ -1229,28 +1242,38 @@ k_fuse_block(Soa o, int64_t* __restrict__ idx, const int64_t* __restrict__ g_off
       s_adj[row * kFuseWords + word] = bits;
     }
     __syncthreads();
-    if (tid == 0) {
-      for (int i = 0; i < n; ++i) s_par[i] = i;
-      for (int i = 0; i < n; ++i) {
-        int ri = i;
-        while (s_par[ri] != ri) ri = s_par[ri];
-        for (int word = i / 32; word < words; ++word) {
-          uint32_t bits = s_adj[i * kFuseWords + word];
-          while (bits) {
-            const int j = word * 32 + __ffs(bits) - 1;
-            bits &= bits - 1;
-            int rj = j;
-            while (s_par[rj] != rj) rj = s_par[rj];
-            s_par[rj] = ri;  // parent[find(j)] = find(i)
+    // Union-find of ccd.py:543-555 replayed row by row: processing row i
+    // attaches the set of every neighbour j > i under find(i), so after the
+    // row every such set carries i's representative.  Keeping the current
+    // representative of every element (quick-find) gives the same
+    // representatives as the reference's parent forest, with each row done
+    // by all threads: collect the neighbours' labels, relabel in parallel.
+    for (int i = tid; i < n; i += kFuseThreads) s_par[i] = i;
+    for (int w = tid; w < kFuseWords; w += kFuseThreads) s_lab[w] = 0u;
+    __syncthreads();
+    for (int i = 0; i < n; ++i) {
+      const int ri = s_par[i];
+      bool any = false;
+      for (int j = i + 1 + tid; j < n; j += kFuseThreads) {
+        if ((s_adj[i * kFuseWords + (j >> 5)] >> (j & 31)) & 1u) {
+          const int rj = s_par[j];
+          if (rj != ri) {
+            atomicOr(&s_lab[rj >> 5], 1u << (rj & 31));
+            any = true;
           }
         }
       }
-      int nr = 0;
-      for (int i = 0; i < n; ++i) {
-        int r = i;
-        while (s_par[r] != r) r = s_par[r];
-        s_par[i] = r;
+      if (!__syncthreads_or(any)) continue;
+      for (int k = tid; k < n; k += kFuseThreads) {
+        const int rk = s_par[k];
+        if ((s_lab[rk >> 5] >> (rk & 31)) & 1u) s_par[k] = ri;
       }
+      __syncthreads();
+      for (int w = tid; w < kFuseWords; w += kFuseThreads) s_lab[w] = 0u;
+      __syncthreads();
+    }
+    if (tid == 0) {
+      int nr = 0;
       for (int i = 0; i < n; ++i)
         if (s_par[i] == i) s_slot[i] = nr++;
       s_nroots = nr;
