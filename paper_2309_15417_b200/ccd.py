@@ -241,11 +241,15 @@ def _packer() -> packing.Packer:
     return pk
 
 
-def _run_problems(problems, *, widen, exhaustive=False, raw=False, timings=None) -> BatchResult:
+def _run_problems(problems, *, widen, exhaustive=False, raw=False, timings=None,
+                  pair_batch=None) -> BatchResult:
     import time
 
     t0 = time.perf_counter()
-    hs = _packer().pack(problems)
+    if pair_batch is not None:
+        hs = _packer().pack_pairs(*pair_batch)
+    else:
+        hs = _packer().pack(problems)
     t1 = time.perf_counter()
     try:
         ds = DeviceScene(hs)
@@ -262,6 +266,9 @@ def _run_problems(problems, *, widen, exhaustive=False, raw=False, timings=None)
             timings.setdefault("search_d2h_ms", []).append(1e3 * (t3 - t2))
         return out
     except _lib.CapacityError:
+        if pair_batch is not None:
+            problems = [_pair_problem(a, b, d) for (a, b), d in
+                        zip(pair_batch[0], np.broadcast_to(pair_batch[1], (len(pair_batch[0]),)))]
         if len(problems) <= 1:
             raise
         half = len(problems) // 2
@@ -332,8 +339,8 @@ def earliest_contacts(pairs, dt, *, widen: float = _WIDEN, exhaustive: bool = Fa
     """Batched `pair_earliest_contact` over many independent body pairs."""
     pairs = list(pairs)
     dts = np.broadcast_to(np.asarray(dt, dtype=np.float64), (len(pairs),))
-    return _run_problems([_pair_problem(a, b, d) for (a, b), d in zip(pairs, dts)],
-                         widen=widen, exhaustive=exhaustive, raw=raw, timings=timings)
+    return _run_problems(None, widen=widen, exhaustive=exhaustive, raw=raw, timings=timings,
+                         pair_batch=(pairs, dts))
 
 
 def effective_dts(clusters, particles, statics, pairs_per_cluster, *, widen: float = _WIDEN,

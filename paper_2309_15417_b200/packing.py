@@ -204,9 +204,11 @@ class Packer:
             self._static = _assemble_static(bodies, self.pinned)
             self._key = key
             self._trees = [b.tree for b in bodies]  # keep ids alive while cached
+        if getattr(self, "_pair_key", None) is not skey:
             self._pair_arrays = (np.asarray(pair_body, dtype=np.int32).reshape(-1, 2),
                                  np.asarray(pair_problem, dtype=np.int32),
                                  np.asarray(pair_group, dtype=np.int32))
+            self._pair_key = skey
         tris, orig, lev, max_children = self._static
         state = _states(bodies, self.pinned)
         ids = np.fromiter((body_id(b) for b in bodies), dtype=np.int64, count=len(bodies))
@@ -218,6 +220,48 @@ class Packer:
             pair_body=pb, pair_problem=pp, pair_group=pg,
             problem_dt=dts, problem_tbase=tbs,
             max_children=max_children, n_problems=len(dts), body_ids=ids)
+
+
+    def pack_pairs(self, pairs, dts) -> HostScene:
+        """Fast path for pair-mode batches (one body pair per problem, as
+        `pair_earliest_contact`): no per-problem Python tuples, one fusion
+        group per problem, t_base 0."""
+        skey = ("pairs", tuple(map(id, (x for ab in pairs for x in ab))))
+        if skey != getattr(self, "_skey", None):
+            slot_of = {}
+            bodies = []
+            pb = np.empty((len(pairs), 2), dtype=np.int32)
+            for k, (a, b) in enumerate(pairs):
+                if body_id(a) == body_id(b):
+                    a = b  # the reference's motions dict collapses equal ids to body_b (ccd.py:501)
+                for side, x in ((0, a), (1, b)):
+                    sl = slot_of.get(id(x))
+                    if sl is None:
+                        sl = slot_of[id(x)] = len(bodies)
+                        bodies.append(x)
+                    pb[k, side] = sl
+            self._tables = (bodies, pb, np.arange(len(pairs), dtype=np.int32),
+                            np.zeros(len(pairs), dtype=np.int32), None, None)
+            self._skey = skey
+            self._key = None  # force the tree block check below
+        bodies, pb, pp, pg, _d, _t = self._tables
+        key = tuple(id(b.tree) for b in bodies)
+        if key != self._key:
+            self._static = _assemble_static(bodies, self.pinned)
+            self._key = key
+            self._trees = [b.tree for b in bodies]
+        self._pair_arrays = (pb, pp, pg)
+        tris, orig, lev, max_children = self._static
+        state = _states(bodies, self.pinned)
+        ids = np.fromiter((body_id(b) for b in bodies), dtype=np.int64, count=len(bodies))
+        lev = lev.copy()
+        lev[:, 1] = ids
+        dts = np.ascontiguousarray(np.broadcast_to(np.asarray(dts, dtype=np.float64), (len(pairs),)))
+        return HostScene(
+            tris=tris, tri_orig=orig, body_state=state, body_levels=lev,
+            pair_body=pb, pair_problem=pp, pair_group=pg,
+            problem_dt=dts, problem_tbase=np.zeros(len(pairs)),
+            max_children=max_children, n_problems=len(pairs), body_ids=ids)
 
 
 def _states(bodies, pinned):
