@@ -34,6 +34,35 @@ class SurrogateLevel:
         return len(self.corners)
 
 
+class ChildIndex:
+    """Children of one surrogate level as a CSR index.  Behaves like the
+    reference's list of sorted index arrays (surrogate.py:115):
+    `children[i]` is parent i's child indices, `len`, iteration."""
+
+    __slots__ = ("ptr", "idx")
+
+    def __init__(self, ptr, idx):
+        self.ptr = np.asarray(ptr, dtype=np.int64)
+        self.idx = np.asarray(idx, dtype=np.int64)
+
+    def __len__(self):
+        return len(self.ptr) - 1
+
+    def __getitem__(self, i):
+        if isinstance(i, slice):
+            return [self[k] for k in range(*i.indices(len(self)))]
+        i = int(i)
+        if i < 0:
+            i += len(self)
+        if not 0 <= i < len(self):
+            raise IndexError(i)
+        return self.idx[self.ptr[i]:self.ptr[i + 1]]
+
+    def __iter__(self):
+        for i in range(len(self)):
+            yield self[i]
+
+
 @dataclass
 class SurrogateTree:
     levels: list                        # levels[0] fine ... levels[-1] coarsest

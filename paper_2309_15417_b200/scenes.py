@@ -137,6 +137,42 @@ def _noisy_icosphere_trees(rng, n, subdiv, noise, eps, radius=1.0):
     return out
 
 
+def _tree_chunk(args):
+    corners, eps = args
+    from .surrogate import build_surrogate_trees
+    return build_surrogate_trees(corners, eps)
+
+
+def make_particles(ids, meshes, eps, states, workers=None):
+    """Batched make_particle for meshes sharing one triangle topology:
+    centres of mass, recentring and surrogate trees vectorised across
+    particles, trees built on `workers` processes for large batches."""
+    import os
+
+    f = meshes[0][1]
+    V = np.stack([np.asarray(v, dtype=np.float64) for v, _ in meshes])
+    a, b, c = V[:, f[:, 0]], V[:, f[:, 1]], V[:, f[:, 2]]
+    dets = np.einsum("pij,pij->pi", a, np.cross(b, c))
+    vol = dets.sum(axis=1) / 6.0
+    com = (dets[..., None] * (a + b + c)).sum(axis=1) / (24.0 * vol)[:, None]
+    Vc = V - com[:, None, :]
+    corners = np.stack([Vc[:, f[:, 0]], Vc[:, f[:, 1]], Vc[:, f[:, 2]]], axis=2)
+    P = len(meshes)
+    workers = workers or min(os.cpu_count() or 1, 32)
+    if P >= 64 and workers > 1:
+        import multiprocessing as mp
+
+        chunks = np.array_split(np.arange(P), min(workers * 4, P))
+        with mp.get_context("fork").Pool(workers) as pool:
+            parts = pool.map(_tree_chunk, [(corners[ch], eps) for ch in chunks])
+        trees = [t for part in parts for t in part]
+    else:
+        trees = _tree_chunk((corners, eps))
+    radius = np.linalg.norm(Vc, axis=2).max(axis=1) + eps
+    return [B.Particle(pid=int(i), tree=t, epsilon=float(eps), radius=float(r), timeline=B.timeline(st))
+            for i, t, r, st in zip(ids, trees, radius, states)]
+
+
 def config1(n_pairs: int = 1024, subdiv: int = 3, seed_offset: int = 1) -> Scene:
     """c1: static noisy-icosphere pairs, centre distance U(1.9, 2.1), eps 0.01."""
     rng = np.random.default_rng(SEED + seed_offset)
@@ -145,15 +181,11 @@ def config1(n_pairs: int = 1024, subdiv: int = 3, seed_offset: int = 1) -> Scene
     quats = random_quaternions(rng, 2 * n_pairs)
     dist = rng.uniform(1.9, 2.1, size=n_pairs)
     axes = unit_vectors(rng, n_pairs)
-    particles = {}
-    pairs = []
-    for k in range(n_pairs):
-        for side, sgn in ((0, -1.0), (1, 1.0)):
-            pid = 2 * k + side
-            v, f = meshes[pid]
-            st = B.state(sgn * 0.5 * dist[k] * axes[k], rotation=quats[pid])
-            particles[pid] = B.make_particle(pid, v, f, eps, st)
-        pairs.append((2 * k, 2 * k + 1))
+    states = [B.state((1.0 if pid % 2 else -1.0) * 0.5 * dist[pid // 2] * axes[pid // 2], rotation=quats[pid])
+              for pid in range(2 * n_pairs)]
+    made = make_particles(range(2 * n_pairs), meshes, eps, states)
+    particles = {p.pid: p for p in made}
+    pairs = [(2 * k, 2 * k + 1) for k in range(n_pairs)]
     return _pair_scene("c1", particles, pairs, 0.0,
                        {"eps": eps, "tris": 20 * 4 ** subdiv, "n_pairs": n_pairs})
 
@@ -249,18 +281,15 @@ def config4(n_pairs: int = 8192, subdiv: int = 3, dt: float = 0.1, seed_offset: 
     spin = rng.normal(0.0, 2.0, size=(2 * n_pairs, 3))
     gaps = rng.uniform(0.0, 0.5, size=n_pairs)
     axes = unit_vectors(rng, n_pairs)
+    states = [B.state(np.zeros(3), velocity=vel[pid], rotation=quats[pid], angular_velocity=spin[pid])
+              for pid in range(2 * n_pairs)]
+    made = make_particles(range(2 * n_pairs), meshes, eps, states)
     particles = {}
     pairs = []
     for k in range(n_pairs):
-        made = []
-        for side in (0, 1):
-            pid = 2 * k + side
-            v, f = meshes[pid]
-            made.append(B.make_particle(pid, v, f, eps, B.state(
-                np.zeros(3), velocity=vel[pid], rotation=quats[pid], angular_velocity=spin[pid])))
-        sep = made[0].radius + made[1].radius + gaps[k]
-        for side, sgn in ((0, -0.5), (1, 0.5)):
-            p = made[side]
+        a, b = made[2 * k], made[2 * k + 1]
+        sep = a.radius + b.radius + gaps[k]
+        for p, sgn in ((a, -0.5), (b, 0.5)):
             p.timeline.current.position = sgn * sep * axes[k]
             p.timeline.old.position = p.timeline.current.position.copy()
             particles[p.pid] = p

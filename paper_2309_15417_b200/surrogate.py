@@ -21,7 +21,7 @@ from __future__ import annotations
 
 import numpy as np
 
-from .bodies import SurrogateLevel, SurrogateTree
+from .bodies import ChildIndex, SurrogateLevel, SurrogateTree
 
 _EPS_PAD = 1e-12
 _TINY = 1e-300
@@ -147,3 +147,84 @@ def build_surrogate_tree(corners, epsilon: float, fanout: int = 4,
         children = [np.sort(g) for g in groups]
         levels.append(SurrogateLevel(corners=parents, epsilon=peps, children=children))
     return SurrogateTree(levels=levels)
+
+
+def _morton_codes(points: np.ndarray, bits: int = 10) -> np.ndarray:
+    """Row-batched Morton codes of (P, n, 3) points, as morton_order computes them."""
+    lo = points.min(axis=1, keepdims=True)
+    span = points.max(axis=1, keepdims=True) - lo
+    span[span <= 0.0] = 1.0
+    q = ((points - lo) * ((2 ** bits - 1) / span)).astype(np.uint64)
+    code = np.zeros(points.shape[:2], dtype=np.uint64)
+    for i in range(bits):
+        for axis in range(3):
+            code |= ((q[..., axis] >> np.uint64(i)) & np.uint64(1)) << np.uint64(3 * i + axis)
+    return code
+
+
+def build_surrogate_trees(corners, epsilon: float, fanout: int = 4, max_levels: int = 8) -> list:
+    """build_surrogate_tree for P meshes with the same triangle count at once.
+
+    `corners` is (P, n, 3, 3).  Every operation is the per-tree one applied
+    along a leading batch axis (Morton codes, stable argsort, batched LAPACK
+    SVD, the dgemv-ordered projections), so each tree equals the one
+    build_surrogate_tree gives for that mesh alone.  Children are stored as
+    a compact CSR index (ChildIndex) instead of one array per parent.
+    """
+    corners = np.ascontiguousarray(np.asarray(corners, dtype=np.float64))
+    P, n = corners.shape[:2]
+    if epsilon <= 0.0:
+        raise ValueError(f"epsilon must be positive, got {epsilon}")
+    levels = [[SurrogateLevel(corners=corners[p], epsilon=np.full(n, float(epsilon)), children=None)]
+              for p in range(P)]
+    cur = corners
+    cur_eps = np.full((P, n), float(epsilon))
+    size = n
+    depth = 1
+    while size > 1 and depth < max_levels:
+        order = np.argsort(_morton_codes(_row_mean(cur, 2)), axis=1, kind="stable")
+        n_full = size // fanout
+        rem = size % fanout
+        G = n_full + (1 if rem else 0)
+        parents = np.empty((P, G, 3, 3))
+        peps = np.empty((P, G))
+        parts = []
+        if n_full:
+            parts.append((0, n_full, order[:, :n_full * fanout].reshape(P, n_full, fanout)))
+        if rem:
+            parts.append((n_full, G, order[:, n_full * fanout:].reshape(P, 1, rem)))
+        for g0, g1, idx in parts:
+            gsz = idx.shape[2]
+            rows = np.take_along_axis(cur, idx.reshape(P, -1)[..., None, None], axis=1)
+            pts = rows.reshape(P * (g1 - g0), gsz * 3, 3)
+            tri = _fit_parents(pts)
+            m = pts.shape[1]
+            dist = _point_triangle_dist(
+                pts,
+                np.broadcast_to(tri[:, None, 0], (len(pts), m, 3)),
+                np.broadcast_to(tri[:, None, 1], (len(pts), m, 3)),
+                np.broadcast_to(tri[:, None, 2], (len(pts), m, 3)))
+            ceps = np.take_along_axis(cur_eps, idx.reshape(P, -1), axis=1).reshape(len(pts), gsz)
+            child_eps = np.repeat(ceps, 3, axis=1)
+            parents[:, g0:g1] = tri.reshape(P, g1 - g0, 3, 3)
+            peps[:, g0:g1] = ((dist + child_eps).max(axis=1) + _EPS_PAD).reshape(P, g1 - g0)
+        srt = np.sort(order, axis=1)
+        if rem:
+            kids_full = np.sort(order[:, :n_full * fanout].reshape(P, n_full, fanout), axis=2)
+            kids_rem = np.sort(order[:, n_full * fanout:], axis=1)
+        else:
+            kids_full = np.sort(order.reshape(P, n_full, fanout), axis=2)
+        ptr = np.concatenate([np.arange(0, n_full * fanout + 1, fanout), [size]] if rem else
+                             [np.arange(0, n_full * fanout + 1, fanout)]).astype(np.int64)
+        del srt
+        for p in range(P):
+            flat = kids_full[p].reshape(-1)
+            if rem:
+                flat = np.concatenate([flat, kids_rem[p]])
+            levels[p].append(SurrogateLevel(corners=parents[p], epsilon=peps[p],
+                                            children=ChildIndex(ptr, flat.astype(np.int64))))
+        cur = parents
+        cur_eps = peps
+        size = G
+        depth += 1
+    return [SurrogateTree(levels=lv) for lv in levels]

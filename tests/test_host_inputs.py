@@ -94,3 +94,22 @@ def test_domino_pairs_are_sphere_overlaps():
     assert abs(r - (np.sqrt(0.05 ** 2 + 0.25 ** 2 + 0.5 ** 2) + 1e-3)) < 1e-12
     assert all(0.18 * (b - a) <= 2 * r for a, b in s.pairs)
     assert len(s.pairs) == sum(min(6, 39 - i) for i in range(40))
+
+
+def test_batched_particles_match_single_builds():
+    from paper_2309_15417_b200.bodies import make_particle
+
+    rng = np.random.default_rng(3)
+    meshes = scenes._noisy_icosphere_trees(rng, 70, 2, 0.05, 0.01)
+    states = [B.state(np.zeros(3)) for _ in meshes]
+    made = scenes.make_particles(range(70), meshes, 0.01, states, workers=2)
+    for k in (0, 33, 69):
+        ref = make_particle(k, meshes[k][0], meshes[k][1], 0.01, states[k])
+        assert made[k].radius == ref.radius
+        for a, b in zip(made[k].tree.levels, ref.tree.levels):
+            np.testing.assert_array_equal(a.corners, b.corners)
+            np.testing.assert_array_equal(a.epsilon, b.epsilon)
+            if b.children is not None:
+                assert len(a.children) == len(b.children)
+                for x, y in zip(a.children, b.children):
+                    np.testing.assert_array_equal(x, y)
