@@ -204,4 +204,96 @@ __device__ __forceinline__ double staged_dist_sq(const Staged<kStride>& st) {
   return best;
 }
 
+// ---------------------------------------------------------------- lite stage
+// A leaner stage for register/shared-memory-bound kernels: corners and
+// squared edge lengths only (24 doubles per thread); edge vectors are
+// recomputed from the corners where used -- the same subtraction, so the
+// same bits.  Layout: A corners 0..8, B corners 9..17, |eA|^2 18..20,
+// |eB|^2 21..23.
+constexpr int kLiteA = 0, kLiteB = 9, kLiteAA = 18, kLiteBB = 21;
+constexpr int kStagedLite = 24;
+
+template <int kStride>
+__device__ __forceinline__ void stage_pair_lite(const Staged<kStride>& st, const Tri& a, const Tri& b) {
+#pragma unroll
+  for (int k = 0; k < 3; ++k) {
+    st.put(kLiteA + 3 * k, a.v[k]);
+    st.put(kLiteB + 3 * k, b.v[k]);
+  }
+#pragma unroll
+  for (int k = 0; k < 3; ++k) {
+    const V3 ea = a.v[(k + 1) % 3] - a.v[k];
+    const V3 eb = b.v[(k + 1) % 3] - b.v[k];
+    st.at(kLiteAA + k) = dot_simd(ea, ea);
+    st.at(kLiteBB + k) = dot_simd(eb, eb);
+  }
+}
+
+template <int kStride>
+__device__ __forceinline__ V3 lite_edge(const Staged<kStride>& st, int base, int k) {
+  const int k1 = k == 2 ? 0 : k + 1;
+  return st.v3(base + 3 * k1) - st.v3(base + 3 * k);
+}
+
+template <int kStride>
+__device__ __forceinline__ double pt_sq_lite(const Staged<kStride>& st, int pk, int tb) {
+  const V3 p = st.v3(pk);
+  const V3 a = st.v3(tb), b = st.v3(tb + 3), c = st.v3(tb + 6);
+  const V3 ab = b - a;
+  const V3 ac = neg(a - c);  // -(e2), e2 = v0 - v2
+  const V3 ap = p - a, bp = p - b, cp = p - c;
+  const double d1 = dot_simd(ab, ap), d2 = dot_simd(ac, ap);
+  const double d3 = dot_simd(ab, bp), d4 = dot_simd(ac, bp);
+  const double d5 = dot_simd(ab, cp), d6 = dot_simd(ac, cp);
+  const double vc = sub(mul(d1, d4), mul(d3, d2));
+  const double vb = sub(mul(d5, d2), mul(d1, d6));
+  const double va = sub(mul(d3, d6), mul(d5, d4));
+  const double e43 = sub(d4, d3), e56 = sub(d5, d6);
+  const bool in_a = le0(d1) && le0(d2);
+  const bool in_b = ge0(d3) && d4 <= d3;
+  const bool in_c = ge0(d6) && d5 <= d6;
+  const bool on_ab = le0(vc) && ge0(d1) && le0(d3);
+  const bool on_ac = le0(vb) && ge0(d2) && le0(d6);
+  const bool on_bc = le0(va) && ge0(e43) && ge0(e56);
+  const bool vertex = in_a || in_b || in_c;
+  const double den = add(add(va, vb), vc);
+  int pv = 0, de = 0;
+  double n1 = vb, m1 = den;
+  bool face = true;
+  if (on_bc) { n1 = e43; m1 = add(e43, e56); pv = 1; de = 1; face = false; }
+  if (on_ac) { n1 = d2; m1 = sub(d2, d6); pv = 0; de = 2; face = false; }
+  if (on_ab) { n1 = d1; m1 = sub(d1, d3); pv = 0; de = 0; face = false; }
+  if (vertex) { pv = in_a ? 0 : (in_b ? 1 : 2); face = false; }
+  double s1 = 0.0, s2 = 0.0;
+  if (!vertex) s1 = sdiv(n1, m1);
+  if (face) s2 = sdiv(vc, den);
+  const V3 P = st.v3(tb + 3 * pv);
+  V3 D1 = lite_edge(st, tb, de);
+  if (de == 2) D1 = neg(D1);
+  const V3 q = (P + scale(D1, s1)) + scale(ac, s2);
+  return sqn(p - q);
+}
+
+template <int kStride>
+__device__ __forceinline__ double staged_dist_sq_lite(const Staged<kStride>& st) {
+  double best = __longlong_as_double(0x7ff0000000000000LL);
+#pragma unroll 1
+  for (int q = 0; q < 6; ++q) {
+    const int pbase = q < 3 ? kLiteA + 3 * q : kLiteB + 3 * (q - 3);
+    const int tbase = q < 3 ? kLiteB : kLiteA;
+    best = min_nonneg(best, pt_sq_lite(st, pbase, tbase));
+  }
+#pragma unroll 1
+  for (int i = 0; i < 3; ++i) {
+    const V3 p1 = st.v3(kLiteA + 3 * i);
+    const V3 u = lite_edge(st, kLiteA, i);
+    const double uu = st.at(kLiteAA + i);
+#pragma unroll 1
+    for (int j = 0; j < 3; ++j)
+      best = min_nonneg(best, ss_sq_uniform(p1, u, uu, st.v3(kLiteB + 3 * j), lite_edge(st, kLiteB, j),
+                                            st.at(kLiteBB + j)));
+  }
+  return best;
+}
+
 }  // namespace ltsg

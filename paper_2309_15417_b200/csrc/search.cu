@@ -237,6 +237,15 @@ __device__ __forceinline__ double row_distance(const Staged<kStride>& st, const 
   return __dsqrt_rn(staged_dist_sq(st));
 }
 
+// Same row with the lite stage (24 doubles per thread).
+template <int kStride>
+__device__ __forceinline__ double row_distance_lite(const Staged<kStride>& st, const double* tris,
+                                                    const BodyInfo& A, const BodyInfo& B, int la, int ia,
+                                                    int lb, int ib, double tau) {
+  stage_pair_lite(st, world_at(A.m, rec(tris, A, la, ia), tau), world_at(B.m, rec(tris, B, lb, ib), tau));
+  return __dsqrt_rn(staged_dist_sq_lite(st));
+}
+
 // ---------------------------------------------------------------- screen
 
 struct CandInfo {
@@ -294,28 +303,126 @@ __device__ __forceinline__ int warp_incl_scan(int v, int lane) {
   return v;
 }
 
-// Bounding-sphere gap minus threshold T and margin at time tau (approximate
-// arithmetic; the margin covers it): > 0 means the triangles are farther
-// apart than T at tau, with room to spare.
-__device__ __forceinline__ double sphere_gap(const BodyInfo& A, const double* ra, const BodyInfo& B,
-                                             const double* rb, double tau, double T) {
-  double R[9], pos[3];
-  rotation_at(A.m, tau, R);
-  position_at(A.m, tau, pos);
-  const double ax = __ldg(ra + 12), ay = __ldg(ra + 13), az = __ldg(ra + 14);
-  const double cax = R[0] * ax + R[1] * ay + R[2] * az + pos[0];
-  const double cay = R[3] * ax + R[4] * ay + R[5] * az + pos[1];
-  const double caz = R[6] * ax + R[7] * ay + R[8] * az + pos[2];
-  rotation_at(B.m, tau, R);
-  position_at(B.m, tau, pos);
-  const double bx = __ldg(rb + 12), by = __ldg(rb + 13), bz = __ldg(rb + 14);
-  const double cbx = R[0] * bx + R[1] * by + R[2] * bz + pos[0];
-  const double cby = R[3] * bx + R[4] * by + R[5] * bz + pos[1];
-  const double cbz = R[6] * bx + R[7] * by + R[8] * bz + pos[2];
-  const double dx = cax - cbx, dy = cay - cby, dz = caz - cbz;
+// ---------------------------------------------------------------- poses
+// Per-body table of the rigid pose at every sample of the grids
+// linspace(0, dt, n), n = 1..33 (561 entries of R row-major + position), for
+// the dt of the body's problem: most moving rows start their window at
+// w0 = 0 (children inherit w0 = 0 unless an earlier sample flagged), so
+// they read their pose instead of recomputing sin/cos and the Rodrigues
+// product.  The entries are computed by rotation_at/position_at themselves,
+// so a row gets the same bits either way.
+constexpr int kPoseEntries = kMaxSamples * (kMaxSamples + 1) / 2;  // 561
+constexpr int kPose = 12;
+
+struct PoseTable {
+  const double* tab;  // n_bodies x kPoseEntries x kPose, or null
+  const double* tdt;  // per body: the dt its table was built for (NaN: none)
+};
+
+__device__ __forceinline__ int grid_entry(int n, int i) { return n * (n - 1) / 2 + i; }
+
+__global__ void k_pose_dt(const PairInfo* __restrict__ pairs, int64_t n_pairs, double* tdt) {
+  const int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (k >= n_pairs) return;
+  const PairInfo p = pairs[k];
+  tdt[p.ba] = p.dt;  // a body shared by problems of different dt keeps one of them
+  tdt[p.bb] = p.dt;
+}
+
+__global__ void k_pose_fill(const BodyInfo* __restrict__ bodies, int n_bodies, const double* __restrict__ tdt,
+                            double* __restrict__ tab) {
+  const int64_t total = (int64_t)n_bodies * kPoseEntries;
+  for (int64_t x = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; x < total;
+       x += (int64_t)gridDim.x * blockDim.x) {
+    const int b = (int)(x / kPoseEntries);
+    const int e = (int)(x - (int64_t)b * kPoseEntries);
+    int n = 1;
+    while (grid_entry(n + 1, 0) <= e) ++n;
+    const int i = e - grid_entry(n, 0);
+    const double dt = tdt[b];
+    if (dt != dt) continue;
+    const double tau = linspace_at(0.0, dt, n, i);
+    double R[9], pos[3];
+    rotation_at(bodies[b].m, tau, R);
+    position_at(bodies[b].m, tau, pos);
+    double* o = tab + x * kPose;
+#pragma unroll
+    for (int k = 0; k < 9; ++k) o[k] = R[k];
+#pragma unroll
+    for (int k = 0; k < 3; ++k) o[9 + k] = pos[k];
+  }
+}
+
+// Pose of body slot `b` at sample i of linspace(w0, dt, n) (= tau).
+__device__ __forceinline__ void pose_at(const BodyInfo& B, int b, double tau, double w0, double dt, int n, int i,
+                                        const PoseTable& pt, double R[9], double pos[3]) {
+  if (pt.tab != nullptr && w0 == 0.0 && pt.tdt[b] == dt) {
+    const double2* e = reinterpret_cast<const double2*>(pt.tab + ((size_t)b * kPoseEntries + grid_entry(n, i)) * kPose);
+    double v[12];
+#pragma unroll
+    for (int k = 0; k < 6; ++k) {
+      const double2 t = __ldg(e + k);
+      v[2 * k] = t.x;
+      v[2 * k + 1] = t.y;
+    }
+#pragma unroll
+    for (int k = 0; k < 9; ++k) R[k] = v[k];
+#pragma unroll
+    for (int k = 0; k < 3; ++k) pos[k] = v[9 + k];
+  } else {
+    rotation_at(B.m, tau, R);
+    position_at(B.m, tau, pos);
+  }
+}
+
+// Bounding-sphere gap (centre distance minus radii, approximate arithmetic;
+// the cull margins cover it) of the candidate's two triangles at sample i.
+__device__ __forceinline__ double sphere_gap_at(const BodyInfo* bodies, const PairInfo& p, const double* ra,
+                                                const double* rb, double tau, double w0, double dt, int n, int i,
+                                                const PoseTable& pt, double* scale) {
+  double ax = 0.0, ay = 0.0, az = 0.0, bx = 0.0, by = 0.0, bz = 0.0;
+#pragma unroll 1
+  for (int side = 0; side < 2; ++side) {
+    const int b = side ? p.bb : p.ba;
+    const double* r = side ? rb : ra;
+    double R[9], pos[3];
+    pose_at(bodies[b], b, tau, w0, dt, n, i, pt, R, pos);
+    const double x = __ldg(r + 12), y = __ldg(r + 13), z = __ldg(r + 14);
+    const double cx = R[0] * x + R[1] * y + R[2] * z + pos[0];
+    const double cy = R[3] * x + R[4] * y + R[5] * z + pos[1];
+    const double cz = R[6] * x + R[7] * y + R[8] * z + pos[2];
+    if (side) { bx = cx; by = cy; bz = cz; } else { ax = cx; ay = cy; az = cz; }
+  }
+  const double dx = ax - bx, dy = ay - by, dz = az - bz;
   const double rA = __ldg(ra + 15), rB = __ldg(rb + 15);
-  const double scale = 1.0 + fabs(cax) + fabs(cay) + fabs(caz) + fabs(cbx) + fabs(cby) + fabs(cbz) + rA + rB;
-  return sqrt(dx * dx + dy * dy + dz * dz) - (rA + rB + T + kCullMargin * scale);
+  *scale = 1.0 + fabs(ax) + fabs(ay) + fabs(az) + fabs(bx) + fabs(by) + fabs(bz) + rA + rB;
+  return sqrt(dx * dx + dy * dy + dz * dz) - (rA + rB);
+}
+
+// Exact 15-feature distance of one row, triangles posed at sample i.
+template <int kStride>
+__device__ __forceinline__ double row_distance_posed(const Staged<kStride>& st, const double* tris,
+                                                     const BodyInfo* bodies, const PairInfo& p, int la, int ia,
+                                                     int lb, int ib, double tau, double w0, double dt, int n,
+                                                     int i, const PoseTable& pt) {
+#pragma unroll 1
+  for (int side = 0; side < 2; ++side) {
+    const int b = side ? p.bb : p.ba;
+    const BodyInfo& B = bodies[b];
+    double R[9], pos[3], L[9];
+    pose_at(B, b, tau, w0, dt, n, i, pt, R, pos);
+    load_local(rec(tris, B, side ? lb : la, side ? ib : ia), L);
+    const Tri t = world_tri(R, pos, L);
+    const int base = side ? kLiteB : kLiteA;
+#pragma unroll
+    for (int k = 0; k < 3; ++k) st.put(base + 3 * k, t.v[k]);
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+      const V3 e = t.v[(k + 1) % 3] - t.v[k];
+      st.at((side ? kLiteBB : kLiteAA) + k) = dot_simd(e, e);
+    }
+  }
+  return __dsqrt_rn(staged_dist_sq_lite(st));
 }
 
 // Screen one frontier (one generation): every candidate is sampled over
@@ -324,7 +431,7 @@ __device__ __forceinline__ double sphere_gap(const BodyInfo& A, const double* ra
 // spread over the 32 lanes, so lanes stay busy whatever the sample counts.
 __global__ void __launch_bounds__(32 * kScreenWarps, LTSG_SCREEN_MINB)
 k_screen(const Cand* __restrict__ front, int64_t n, const PairInfo* __restrict__ pairs,
-         const BodyInfo* __restrict__ bodies, const double* __restrict__ tris, ScreenOut out) {
+         const BodyInfo* __restrict__ bodies, const double* __restrict__ tris, ScreenOut out, PoseTable pt) {
   if (out.n_in) n = (int64_t)min(*out.n_in, out.next_cap);
   __shared__ union {  // per warp: candidate info, later reused for child descriptors
     CandInfo cand[32];
@@ -332,7 +439,7 @@ k_screen(const Cand* __restrict__ front, int64_t n, const PairInfo* __restrict__
   } s_u[kScreenWarps];
   __shared__ uint8_t s_bits[kScreenWarps][kRowsPerWarp];
   __shared__ int16_t s_queue[kScreenWarps][kRowsPerWarp];
-  extern __shared__ double s_stage[];  // kStaged x (32 * kScreenWarps), dynamic
+  extern __shared__ double s_stage[];  // kStagedLite x (32 * kScreenWarps), dynamic
   const Staged<32 * kScreenWarps> st{s_stage + threadIdx.x};
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
@@ -376,8 +483,13 @@ k_screen(const Cand* __restrict__ front, int64_t n, const PairInfo* __restrict__
       me.cull_hi = 2.0 * p.dt + 1.0;
       if (__ldg(ra_ + 15) >= 0.0 && __ldg(rb_ + 15) >= 0.0) {
         const double T = fmax(me.thr, add(me.h, kRestSlop));
-        const double g0 = sphere_gap(A, ra_, B, rb_, c.w0, T);
-        const double g1 = p.dt > c.w0 ? sphere_gap(A, ra_, B, rb_, p.dt, T) : g0;
+        double sc0, sc1;
+        const double g0 = sphere_gap_at(bodies, p, ra_, rb_, c.w0, c.w0, p.dt, me.count, 0, pt, &sc0) -
+                          (T + kCullMargin * sc0);
+        const double g1 = p.dt > c.w0
+            ? sphere_gap_at(bodies, p, ra_, rb_, p.dt, c.w0, p.dt, me.count, me.count - 1, pt, &sc1) -
+                  (T + kCullMargin * sc1)
+            : g0;
         if (sp > 0.0) {
           me.cull_lo = c.w0 + g0 / sp;  // rows with tau < cull_lo are cleared
           me.cull_hi = p.dt - g1 / sp;  // rows with tau > cull_hi are cleared
@@ -419,32 +531,16 @@ k_screen(const Cand* __restrict__ front, int64_t n, const PairInfo* __restrict__
           if (info[o + step].first <= r) o += step;
         while (info[o].culled || info[o].count == 0) --o;
         const CandInfo& c = info[o];
-        const double tau = linspace_at(c.w0, c.dt, c.count, r - c.first);
+        const int i = r - c.first;
+        const double tau = linspace_at(c.w0, c.dt, c.count, i);
         const PairInfo p = pairs[c.pair];
-        const BodyInfo& A = bodies[p.ba];
-        const BodyInfo& B = bodies[p.bb];
-        const double* ra_ = rec(tris, A, c.la, c.ia);
-        const double* rb_ = rec(tris, B, c.lb, c.ib);
-        const double rA = __ldg(ra_ + 15), rB = __ldg(rb_ + 15);
+        const double* ra_ = rec(tris, bodies[p.ba], c.la, c.ia);
+        const double* rb_ = rec(tris, bodies[p.bb], c.lb, c.ib);
         keep = !(tau < c.cull_lo || tau > c.cull_hi);
-        if (keep && rA >= 0.0 && rB >= 0.0) {
-          double R[9], pos[3];
-          rotation_at(A.m, tau, R);
-          position_at(A.m, tau, pos);
-          const double ax = __ldg(ra_ + 12), ay = __ldg(ra_ + 13), az = __ldg(ra_ + 14);
-          const double cax = R[0] * ax + R[1] * ay + R[2] * az + pos[0];
-          const double cay = R[3] * ax + R[4] * ay + R[5] * az + pos[1];
-          const double caz = R[6] * ax + R[7] * ay + R[8] * az + pos[2];
-          rotation_at(B.m, tau, R);
-          position_at(B.m, tau, pos);
-          const double bx = __ldg(rb_ + 12), by = __ldg(rb_ + 13), bz = __ldg(rb_ + 14);
-          const double cbx = R[0] * bx + R[1] * by + R[2] * bz + pos[0];
-          const double cby = R[3] * bx + R[4] * by + R[5] * bz + pos[1];
-          const double cbz = R[6] * bx + R[7] * by + R[8] * bz + pos[2];
-          const double dx = cax - cbx, dy = cay - cby, dz = caz - cbz;
-          const double scale = 1.0 + fabs(cax) + fabs(cay) + fabs(caz) + fabs(cbx) + fabs(cby) + fabs(cbz) + rA + rB;
-          const double reach = rA + rB + fmax(c.thr, add(c.h, kRestSlop)) + kCullMargin * scale;
-          keep = !(dx * dx + dy * dy + dz * dz > reach * reach);
+        if (keep && __ldg(ra_ + 15) >= 0.0 && __ldg(rb_ + 15) >= 0.0) {
+          double scale;
+          const double gap = sphere_gap_at(bodies, p, ra_, rb_, tau, c.w0, c.dt, c.count, i, pt, &scale);
+          keep = !(gap > fmax(c.thr, add(c.h, kRestSlop)) + kCullMargin * scale);
         }
         if (!keep) bits[r] = 0;
       }
@@ -465,7 +561,7 @@ k_screen(const Cand* __restrict__ front, int64_t n, const PairInfo* __restrict__
       const int i = r - c.first;
       const double tau = linspace_at(c.w0, c.dt, c.count, i);
       const PairInfo p = pairs[c.pair];
-      const double d = row_distance(st, tris, bodies[p.ba], bodies[p.bb], c.la, c.ia, c.lb, c.ib, tau);
+      const double d = row_distance_posed(st, tris, bodies, p, c.la, c.ia, c.lb, c.ib, tau, c.w0, c.dt, c.count, i, pt);
       uint8_t b = 0;
       if (d <= c.thr) b |= 1;                  // screen flag
       if (d <= c.h) b |= 2;                    // at or below touching distance
@@ -1579,7 +1675,7 @@ static int scan_exclusive(ltsg_workspace* ws, const int64_t* in, int64_t* out, i
   return LTSG_OK;
 }
 
-constexpr int kScreenStageBytes = kStaged * 32 * kScreenWarps * sizeof(double);
+constexpr int kScreenStageBytes = kStagedLite * 32 * kScreenWarps * sizeof(double);
 
 static int configure_kernels() {
   static int done = 0;
@@ -1718,6 +1814,23 @@ static int run_search(const ltsg_scene* sc, ltsg_result* out, ltsg_workspace* ws
     }
   }
 
+  // ---- pose tables for moving batches
+  PoseTable poses{nullptr, nullptr};
+  if (!all_static && sc->n_pairs > 0 && sc->n_bodies > 0 && !getenv("LTSG_NO_POSES")) {
+    const size_t bytes = (size_t)sc->n_bodies * kPoseEntries * kPose * sizeof(double);
+    if (bytes <= ws->budget / 4) {
+      double *tab, *tdt;
+      LTSG_TRY(ws_get(ws, "pose_tab", (size_t)sc->n_bodies * kPoseEntries * kPose, &tab));
+      LTSG_TRY(ws_get(ws, "pose_dt", (size_t)sc->n_bodies, &tdt));
+      LTSG_CUDA(cudaMemsetAsync(tdt, 0xff, sizeof(double) * sc->n_bodies, st));  // NaN
+      k_pose_dt<<<grid_for(sc->n_pairs, 128), 128, 0, st>>>(pr.pairs, sc->n_pairs, tdt);
+      LTSG_LAUNCHED();
+      k_pose_fill<<<148 * 16, 128, 0, st>>>(pr.bodies, sc->n_bodies, tdt, tab);
+      LTSG_LAUNCHED();
+      poses = PoseTable{tab, tdt};
+    }
+  }
+
   // ---- traversal: seeds (ccd.py:385-391) and generations (ccd.py:393-446).
   // Async mode enqueues every generation back to back (frontier sizes stay
   // on the device, buffers are sized from the workspace's history) and
@@ -1759,7 +1872,8 @@ static int run_search(const ltsg_scene* sc, ltsg_result* out, ltsg_workspace* ws
                         kStaticStageBytes, st>>>(in, n, pr.pairs, pr.bodies, world, woff, so);
     } else {
       const int grid = n_in ? 148 * 32 : screen_grid(n);
-      k_screen<<<grid, 32 * kScreenWarps, kScreenStageBytes, st>>>(in, n, pr.pairs, pr.bodies, sc->tris, so);
+      k_screen<<<grid, 32 * kScreenWarps, kScreenStageBytes, st>>>(in, n, pr.pairs, pr.bodies, sc->tris, so,
+                                                                   poses);
     }
     LTSG_LAUNCHED();
     return LTSG_OK;
