@@ -98,7 +98,7 @@ class ClockSampler:
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
-                 "--format=csv,noheader,nounits", "-lms", "200"],
+                 "--format=csv,noheader,nounits", "-lms", "50"],
                 stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             self.thread = threading.Thread(target=self._read, daemon=True)
             self.thread.start()
@@ -244,18 +244,30 @@ def run_ours(args, rank, world, local_rank):
 
     from paper_2309_15417_b200 import _lib, ccd, packing
 
+    # host setup first: the scene builders fork worker processes, which must
+    # happen before this process starts CUDA
+    t_build = time.perf_counter()
+    scene = build_scene(args.config, rank, args.pairs)
+    problems = scene_problems(scene)
+    hs = packing.pack(problems)
+    t_build = time.perf_counter() - t_build
+
+    # CPU baseline leg (rank 0 only): the oracle on this host's cores over a
+    # bounded sample of the same workload, run before this process starts CUDA
+    cpu = None
+    if rank == 0 and not args.no_cpu:
+        workers = max(1, min(cpu_cores(), 64))
+        r, c, w, n = cpu_sample(problems, min(len(problems), 2 * workers), workers)
+        cpu = {"value": r / w if w > 0 else 0.0, "unit": "tests/s", "cores": workers, "kind": "port",
+               "sample": f"{n} {args.config} problems (of {len(problems)}) through the numpy oracle, "
+                         f"{workers} processes, {w:.1f} s wall"}
+
     torch.cuda.set_device(local_rank)
     dist = None
     if world > 1:
         import torch.distributed as dist
 
         dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
-
-    t_build = time.perf_counter()
-    scene = build_scene(args.config, rank, args.pairs)
-    problems = scene_problems(scene)
-    hs = packing.pack(problems)
-    t_build = time.perf_counter() - t_build
     # The scene holds ~10^6 long-lived numpy objects (the reference's tree
     # format keeps one children array per surrogate triangle); exclude them
     # from cyclic GC scans, as a long-running engine would.
@@ -285,18 +297,19 @@ def run_ours(args, rank, world, local_rank):
     stats = []
     step_ms = []
     barrier()
-    with ClockSampler(local_rank) as clocks:
-        for _ in range(args.steps):
-            flush.fill_(1)
-            ev0 = torch.cuda.Event(enable_timing=True)
-            ev1 = torch.cuda.Event(enable_timing=True)
-            ev0.record()
-            res = ccd.run_scene(ds)
-            ev1.record()
-            ev1.synchronize()
-            step_ms.append(ev0.elapsed_time(ev1))
-            stats.append(res.stats)
-        barrier()
+    # clocks and throttle reasons sampled across both timed loops (device, e2e)
+    clocks = ClockSampler(local_rank).__enter__()
+    for _ in range(args.steps):
+        flush.fill_(1)
+        ev0 = torch.cuda.Event(enable_timing=True)
+        ev1 = torch.cuda.Event(enable_timing=True)
+        ev0.record()
+        res = ccd.run_scene(ds)
+        ev1.record()
+        ev1.synchronize()
+        step_ms.append(ev0.elapsed_time(ev1))
+        stats.append(res.stats)
+    barrier()
     total_ms = sum(step_ms)
     tests = sum(s["rows_screen"] + s["rows_zoom"] + s["rows_bisect"] for s in stats)
     contacts = sum(s["n_raw"] for s in stats)
@@ -323,6 +336,7 @@ def run_ours(args, rank, world, local_rank):
         t1 = time.perf_counter()
         if i >= args.warmup:
             e2e_ms.append(1e3 * (t1 - t0))
+    clocks.__exit__(None, None, None)
     h2d = hs.nbytes
     d2h = sum(v.nbytes for v in out.contacts.values()) + out.dt.nbytes + out.collision.nbytes \
         + out.first_contact.nbytes + out.fused_offset.nbytes
@@ -341,13 +355,6 @@ def run_ours(args, rank, world, local_rank):
         e2e_total = sum(e2e_ms)
         tests_all, contacts_all = float(tests), float(contacts)
 
-    cpu = None
-    if rank == 0 and not args.no_cpu:
-        workers = max(1, min(cpu_cores(), 64))
-        r, c, w, n = cpu_sample(problems, min(len(problems), 2 * workers), workers)
-        cpu = {"value": r / w if w > 0 else 0.0, "unit": "tests/s", "cores": workers, "kind": "port",
-               "sample": f"{n} {args.config} problems (of {len(problems)}) through the numpy oracle, "
-                         f"{workers} processes, {w:.1f} s wall"}
 
     if rank == 0:
         value = tests_all / (total_ms * 1e-3)

@@ -256,7 +256,7 @@ class Packer:
         ids = np.fromiter((body_id(b) for b in bodies), dtype=np.int64, count=len(bodies))
         lev = lev.copy()
         lev[:, 1] = ids
-        dts = np.ascontiguousarray(np.broadcast_to(np.asarray(dts, dtype=np.float64), (len(pairs),)))
+        dts = np.array(np.broadcast_to(np.asarray(dts, dtype=np.float64), (len(pairs),)), copy=True)
         return HostScene(
             tris=tris, tri_orig=orig, body_state=state, body_levels=lev,
             pair_body=pb, pair_problem=pp, pair_group=pg,

@@ -159,7 +159,8 @@ def make_particles(ids, meshes, eps, states, workers=None):
     corners = np.stack([Vc[:, f[:, 0]], Vc[:, f[:, 1]], Vc[:, f[:, 2]]], axis=2)
     P = len(meshes)
     workers = workers or min(os.cpu_count() or 1, 32)
-    if P >= 64 and workers > 1:
+    # fork-based workers only for big batches (bench setup, before CUDA starts)
+    if P >= 1024 and workers > 1:
         import multiprocessing as mp
 
         chunks = np.array_split(np.arange(P), min(workers * 4, P))

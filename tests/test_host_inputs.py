@@ -100,10 +100,10 @@ def test_batched_particles_match_single_builds():
     from paper_2309_15417_b200.bodies import make_particle
 
     rng = np.random.default_rng(3)
-    meshes = scenes._noisy_icosphere_trees(rng, 70, 2, 0.05, 0.01)
+    meshes = scenes._noisy_icosphere_trees(rng, 1030, 1, 0.05, 0.01)
     states = [B.state(np.zeros(3)) for _ in meshes]
-    made = scenes.make_particles(range(70), meshes, 0.01, states, workers=2)
-    for k in (0, 33, 69):
+    made = scenes.make_particles(range(1030), meshes, 0.01, states, workers=2)
+    for k in (0, 517, 1029):
         ref = make_particle(k, meshes[k][0], meshes[k][1], 0.01, states[k])
         assert made[k].radius == ref.radius
         for a, b in zip(made[k].tree.levels, ref.tree.levels):
