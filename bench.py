@@ -151,7 +151,7 @@ def _oracle_job(args):
     pairs, dt, tb = _CPU_PROBLEMS[idx]
     t0 = time.perf_counter()
     if len(pairs) == 1 and tb == 0.0:
-        res = O.pair_earliest_contact(pairs[0][0], pairs[0][1], dt)
+        res = O.pair_earliest_contact(pairs[0][0], pairs[0][1], dt, exhaustive=_CPU_EXHAUSTIVE)
     else:
         from types import SimpleNamespace
 
@@ -170,14 +170,16 @@ def _bid(b):
 
 
 _CPU_PROBLEMS = []
+_CPU_EXHAUSTIVE = False
 
 
-def cpu_sample(problems, n_items: int, workers: int):
+def cpu_sample(problems, n_items: int, workers: int, exhaustive: bool = False):
     """Run the oracle over the first n_items problems on `workers` processes."""
     import multiprocessing as mp
 
-    global _CPU_PROBLEMS
+    global _CPU_PROBLEMS, _CPU_EXHAUSTIVE
     _CPU_PROBLEMS = problems
+    _CPU_EXHAUSTIVE = exhaustive
     idx = list(range(min(n_items, len(problems))))
     t0 = time.perf_counter()
     if workers <= 1:
@@ -239,7 +241,6 @@ def run_reference(args, rank, world):
 def run_ours(args, rank, world, local_rank):
     import ctypes as C
 
-    import numpy as np
     import torch
 
     from paper_2309_15417_b200 import _lib, ccd, packing
@@ -257,7 +258,8 @@ def run_ours(args, rank, world, local_rank):
     cpu = None
     if rank == 0 and not args.no_cpu:
         workers = max(1, min(cpu_cores(), 64))
-        r, c, w, n = cpu_sample(problems, min(len(problems), 2 * workers), workers)
+        per_worker = 1 if args.exhaustive else 2  # an exhaustive c1 pair is ~40 s of numpy
+        r, c, w, n = cpu_sample(problems, min(len(problems), per_worker * workers), workers, args.exhaustive)
         cpu = {"value": r / w if w > 0 else 0.0, "unit": "tests/s", "cores": workers, "kind": "port",
                "sample": f"{n} {args.config} problems (of {len(problems)}) through the numpy oracle, "
                          f"{workers} processes, {w:.1f} s wall"}
@@ -286,6 +288,25 @@ def run_ours(args, rank, world, local_rank):
 
     flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")  # > 126 MB L2
 
+    # roofline of the 15-feature distance itself: every fine x fine row of a
+    # sample of pairs evaluated exactly at tau = 0 (ltsg_exhaustive_rows)
+    allpairs = None
+    if scene.mode == "pair" and not args.no_allpairs:
+        sub = problems[: min(len(problems), 16)]
+        ds_sub = ccd.DeviceScene(packing.pack(sub))
+        sc_sub = ds_sub.struct(1e-3, False)
+        rows_c, hits_c, ms_c = C.c_int64(), C.c_int64(), C.c_double()
+        for _ in range(2):
+            _lib.check(_lib.lib().ltsg_exhaustive_rows(C.byref(sc_sub), C.byref(rows_c), C.byref(hits_c),
+                                                       C.byref(ms_c), _lib.workspace().handle,
+                                                       C.c_void_p(torch.cuda.current_stream().cuda_stream)),
+                       "ltsg_exhaustive_rows")
+        ach = rows_c.value * FLOPS_PER_TEST / (ms_c.value * 1e-3) / 1e12
+        allpairs = {"kernel": "k_allpairs", "pairs": len(sub), "rows": rows_c.value, "hits": hits_c.value,
+                    "ms": ms_c.value, "tests_per_s": rows_c.value / (ms_c.value * 1e-3),
+                    "achieved_tflops": ach, "frac": ach / peak_tflops.value}
+        del ds_sub
+
     def barrier():
         torch.cuda.synchronize()
         if dist is not None:
@@ -293,7 +314,7 @@ def run_ours(args, rank, world, local_rank):
 
     # ---- device-resident steps
     for _ in range(args.warmup):
-        res = ccd.run_scene(ds)
+        res = ccd.run_scene(ds, exhaustive=args.exhaustive)
     stats = []
     step_ms = []
     barrier()
@@ -304,7 +325,7 @@ def run_ours(args, rank, world, local_rank):
         ev0 = torch.cuda.Event(enable_timing=True)
         ev1 = torch.cuda.Event(enable_timing=True)
         ev0.record()
-        res = ccd.run_scene(ds)
+        res = ccd.run_scene(ds, exhaustive=args.exhaustive)
         ev1.record()
         ev1.synchronize()
         step_ms.append(ev0.elapsed_time(ev1))
@@ -330,7 +351,7 @@ def run_ours(args, rank, world, local_rank):
         tm = phases if i >= args.warmup else None
         t0 = time.perf_counter()
         if scene.mode == "pair":
-            out = ccd.earliest_contacts(pairs_obj, scene.dt, timings=tm)
+            out = ccd.earliest_contacts(pairs_obj, scene.dt, timings=tm, exhaustive=args.exhaustive)
         else:
             out = ccd._run_problems(problems, widen=1e-3, timings=tm)
         t1 = time.perf_counter()
@@ -365,7 +386,8 @@ def run_ours(args, rank, world, local_rank):
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": total_ms / args.steps,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic (seeded, BASELINE.json shapes)",
-            "config": {"workload": args.config, "description": CONFIG_DOC[args.config],
+            "config": {"workload": args.config + (" exhaustive" if args.exhaustive else ""),
+                       "description": CONFIG_DOC[args.config],
                        "problems_per_gpu": len(problems), "pairs_per_gpu": len(hs.pair_problem),
                        "triangle_records_per_gpu": int(len(hs.tris)),
                        "l2": "flushed (256 MiB write) before every timed step",
@@ -390,6 +412,7 @@ def run_ours(args, rank, world, local_rank):
                          "screen_rows_exact_per_step": exact_rows / args.steps,
                          "note": "rows settled by the certified sphere cull are counted as tests in "
                                  "`value` (their decision is identical) but not in `achieved`"},
+            "roofline_distance_kernel": allpairs,
             "gpu_launches": launches,
             "breakdown_ms_per_step": {
                 "screen": screen_ms / args.steps,
@@ -417,6 +440,9 @@ def main(argv=None) -> int:
     ap.add_argument("--pairs", type=int, default=None, help="override the workload size")
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
     ap.add_argument("--cpu-workers", type=int, default=0)
+    ap.add_argument("--exhaustive", action="store_true",
+                    help="screen every fine x fine pair (ccd.py:387-388) instead of the multiscale walk")
+    ap.add_argument("--no-allpairs", action="store_true", help="skip the distance-kernel roofline leg")
     args = ap.parse_args(argv)
     rank, world, local_rank = _env_rank()
     if args.impl == "reference":

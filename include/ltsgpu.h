@@ -179,11 +179,10 @@ int ltsg_search(const ltsg_scene* scene, ltsg_result* out, ltsg_workspace* ws, v
 int ltsg_fuse_contacts(ltsg_result* io, int64_t n_raw, const uint64_t* group_key,
                        ltsg_workspace* ws, void* stream);
 
-/* Time one launch of the screen kernel over an implicit all-pairs frontier
- * of `n_pairs` pairs (exhaustive fine x fine, every candidate one sample at
- * tau = 0) -- the roofline microbenchmark of the 15-feature distance.
- * Returns the number of rows evaluated in *rows and the contacts in *hits. */
-int ltsg_exhaustive_rows(const ltsg_scene* scene, int64_t* rows, int64_t* hits,
+/* Roofline measurement of the 15-feature distance: every fine x fine row of
+ * every pair at tau = 0 evaluated exactly (no cull, no traversal).  Returns
+ * the row count, the rows within h + 1e-9 and the kernel's device time. */
+int ltsg_exhaustive_rows(const ltsg_scene* scene, int64_t* rows, int64_t* hits, double* ms,
                          ltsg_workspace* ws, void* stream);
 
 /* FP64 pipe microbenchmark: independent DFMA chains on every SM; reports

@@ -83,7 +83,7 @@ def lib():
             "ltsg_closest_feature": [P, P, I64, P, P, P, P],
             "ltsg_overlap_centroid": [P, P, P, I64, P, P, P],
             "ltsg_search": [C.POINTER(Scene), C.POINTER(Result), P, P],
-            "ltsg_exhaustive_rows": [C.POINTER(Scene), C.POINTER(I64), C.POINTER(I64), P, P],
+            "ltsg_exhaustive_rows": [C.POINTER(Scene), C.POINTER(I64), C.POINTER(I64), C.POINTER(F64), P, P],
             "ltsg_fuse_contacts": [C.POINTER(Result), I64, P, P, P],
             "ltsg_fp64_peak": [C.POINTER(F64), C.POINTER(F64), P],
         }.items():

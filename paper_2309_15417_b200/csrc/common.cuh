@@ -58,7 +58,7 @@ struct ltsg_workspace {
   size_t budget = 0;
   int device = 0;
   // sizes seen by earlier calls: the async traversal preallocates from them
-  size_t hint_front = 0, hint_rest = 0, hint_entries = 0, hint_cross = 0;
+  size_t hint_front = 0, hint_rest = 0, hint_entries = 0, hint_cross = 0, hint_seed = 0;
 
   int get(const char* name, size_t bytes, void** out, bool keep = false);
   ~ltsg_workspace();

@@ -809,13 +809,13 @@ __device__ __forceinline__ bool static_child_cull(const double* world, int32_t w
 __global__ void k_seed_static(const PairInfo* __restrict__ pairs, int64_t n_pairs,
                               const BodyInfo* __restrict__ bodies, const int64_t* __restrict__ woff,
                               const double* __restrict__ world, Cand* out, unsigned long long cap,
-                              Counters* ctr, unsigned long long* n_out) {
+                              Counters* ctr, unsigned long long* n_out, int exhaustive) {
   const int lane = threadIdx.x & 31;
   for (int64_t k = blockIdx.x; k < n_pairs; k += gridDim.x) {
     const PairInfo p = pairs[k];
     const BodyInfo& A = bodies[p.ba];
     const BodyInfo& B = bodies[p.bb];
-    const int la = A.n_levels - 1, lb = B.n_levels - 1;
+    const int la = exhaustive ? 0 : A.n_levels - 1, lb = exhaustive ? 0 : B.n_levels - 1;
     const int64_t na = A.level_size[la], nb = B.level_size[lb];
     const int64_t a0 = woff[p.ba] + A.level_off[la] - A.level_off[0];
     const int64_t b0 = woff[p.bb] + B.level_off[lb] - B.level_off[0];
@@ -1622,28 +1622,28 @@ __global__ void k_widen(const int32_t* a, int64_t* b, int64_t n) {
   if (i < n) b[i] = a[i];
 }
 
-// Exhaustive fine x fine screen of pair `k` at tau = 0 over an implicit
-// frontier (no candidate records): the roofline microbenchmark.
-__global__ void __launch_bounds__(128)
+// Exhaustive fine x fine rows of every pair at tau = 0 over an implicit
+// frontier: the exact 15-feature distance on every row, no cull -- the
+// roofline measurement of the distance kernel on real mesh rows.  Counts the
+// rows within h + 1e-9 (the resting test).
+__global__ void __launch_bounds__(32 * kStaticWarps, LTSG_STATIC_MINB)
 k_allpairs(const PairInfo* __restrict__ pairs, int64_t n_pairs, const BodyInfo* __restrict__ bodies,
-           const double* __restrict__ tris, unsigned long long* hits) {
-  __shared__ double s_stage[kStaged * 128];
-  const Staged<128> st{s_stage + threadIdx.x};
+           const double* __restrict__ world, const int64_t* __restrict__ woff, unsigned long long* hits) {
+  extern __shared__ double s_stage[];
+  const Staged<32 * kStaticWarps> st{s_stage + threadIdx.x};
   unsigned long long local = 0;
   for (int64_t k = blockIdx.y; k < n_pairs; k += gridDim.y) {
     const PairInfo p = pairs[k];
-    const BodyInfo& A = bodies[p.ba];
-    const BodyInfo& B = bodies[p.bb];
-    const int64_t na = A.level_size[0], nb = B.level_size[0];
-    const int64_t total = na * nb;
-    for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < total;
+    const int64_t na = bodies[p.ba].level_size[0], nb = bodies[p.bb].level_size[0];
+    const double* wa0 = world + (size_t)woff[p.ba] * kWorld;
+    const double* wb0 = world + (size_t)woff[p.bb] * kWorld;
+    for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < na * nb;
          j += (int64_t)gridDim.x * blockDim.x) {
-      const int ia = (int)(j / nb), ib = (int)(j % nb);
-      const double* ra = rec(tris, A, 0, ia);
-      const double* rb = rec(tris, B, 0, ib);
-      const double h = add(__ldg(ra + 9), __ldg(rb + 9));
-      const double d = row_distance(st, tris, A, B, 0, ia, 0, ib, 0.0);
-      if (d <= add(h, kRestSlop)) ++local;
+      const double* wa = wa0 + (size_t)(j / nb) * kWorld;
+      const double* wb = wb0 + (size_t)(j % nb) * kWorld;
+      const double h = add(__ldg(wa + 9), __ldg(wb + 9));
+      stage_pair(st, load_world(wa), load_world(wb));
+      if (__dsqrt_rn(staged_dist_sq(st)) <= add(h, kRestSlop)) ++local;
     }
   }
   for (int o = 16; o > 0; o >>= 1) local += __shfl_down_sync(0xffffffffu, local, o);
@@ -1683,6 +1683,7 @@ static int configure_kernels() {
     LTSG_CUDA(cudaFuncSetAttribute(k_screen, cudaFuncAttributeMaxDynamicSharedMemorySize, kScreenStageBytes));
     LTSG_CUDA(cudaFuncSetAttribute(k_screen_static, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                    kStaticStageBytes));
+    LTSG_CUDA(cudaFuncSetAttribute(k_allpairs, cudaFuncAttributeMaxDynamicSharedMemorySize, kStaticStageBytes));
     done = 1;
   }
   return LTSG_OK;
@@ -1786,7 +1787,7 @@ static int run_search(const ltsg_scene* sc, ltsg_result* out, ltsg_workspace* ws
   bool all_static = false;
   double* world = nullptr;
   int64_t* woff = nullptr;
-  if (!sc->exhaustive && sc->n_pairs > 0) {
+  if (sc->n_pairs > 0) {
     std::vector<double> hdt(np);
     LTSG_CUDA(cudaMemcpyAsync(hdt.data(), sc->problem_dt, sizeof(double) * np, cudaMemcpyDeviceToHost, st));
     LTSG_CUDA(cudaStreamSynchronize(st));
@@ -1890,11 +1891,17 @@ static int run_search(const ltsg_scene* sc, ltsg_result* out, ltsg_workspace* ws
     out->generations = 0;
     out->ms_screen = 0.0;
     if (sc->n_pairs == 0) return LTSG_OK;
-    const size_t cap_async = std::max<size_t>((size_t)(1.25 * (double)ws->hint_front) + 1024, (size_t)seed_total);
-    LTSG_TRY(ws_get(ws, "front0", async_mode ? cap_async : (size_t)seed_total, &front));
+    // static seeds are culled on the fly: size for the survivors (hint), grow on overflow
+    const size_t hint_cap = (size_t)(1.25 * (double)ws->hint_front) + 1024;
+    const size_t seed_cap = all_static ? std::min((size_t)seed_total, std::max(hint_cap, ws->hint_seed))
+                                       : (size_t)seed_total;
+    const size_t cap_async = std::max(hint_cap, seed_cap);
+    LTSG_TRY(ws_get(ws, "front0", async_mode ? cap_async : seed_cap, &front));
+    // the static seed kernel tests (and culls) the root rows: it is screen work
+    t_screen.start(st);
     if (all_static) {
       k_seed_static<<<(int)std::min<int64_t>(sc->n_pairs, 148 * 16), 128, 0, st>>>(
-          pr.pairs, sc->n_pairs, pr.bodies, woff, world, front, (unsigned long long)seed_total, d_ctr, gen_cnt);
+          pr.pairs, sc->n_pairs, pr.bodies, woff, world, front, seed_cap, d_ctr, gen_cnt, sc->exhaustive);
     } else {
       k_seed_fill<<<(int)std::min<int64_t>(sc->n_pairs, 148 * 16), 128, 0, st>>>(
           pr.pairs, sc->n_pairs, pr.bodies, sc->exhaustive, seed_off, front);
@@ -1905,7 +1912,6 @@ static int run_search(const ltsg_scene* sc, ltsg_result* out, ltsg_workspace* ws
       Cand* buf[2];
       buf[0] = front;
       LTSG_TRY(ws_get(ws, "front1", cap_async, &buf[1]));
-      t_screen.start(st);
       for (int g = 1; g <= kMaxGen; ++g)
         LTSG_TRY(launch_screen(buf[(g - 1) & 1], 0, gen_cnt + g - 1, buf[g & 1], cap_async, gen_cnt + g));
       t_screen.stop(st);
@@ -1913,8 +1919,9 @@ static int run_search(const ltsg_scene* sc, ltsg_result* out, ltsg_workspace* ws
       LTSG_CUDA(cudaMemcpyAsync(hg, gen_cnt, sizeof(hg), cudaMemcpyDeviceToHost, st));
       LTSG_TRY(read_ctr(d_ctr, &h, st));
       out->ms_screen = t_screen.ms();
+      if (hg[0] > seed_cap) ws->hint_seed = std::max(ws->hint_seed, (size_t)hg[0]);
       for (int g = 0; g <= kMaxGen; ++g) {
-        if (hg[g] > cap_async) *overflow = true;
+        if (hg[g] > (g == 0 ? seed_cap : cap_async)) *overflow = true;
         if (g < kMaxGen && hg[g] > 0) {
           out->candidates += (int64_t)hg[g];
           out->generations += 1;
@@ -1925,9 +1932,22 @@ static int run_search(const ltsg_scene* sc, ltsg_result* out, ltsg_workspace* ws
       return LTSG_OK;
     }
     // sync mode
+    t_screen.stop(st);
     unsigned long long n_first = 0;
     LTSG_CUDA(cudaMemcpyAsync(&n_first, gen_cnt, sizeof(n_first), cudaMemcpyDeviceToHost, st));
     LTSG_TRY(read_ctr(d_ctr, &h, st));
+    out->ms_screen += t_screen.ms();
+    if (n_first > seed_cap) {  // more seed survivors than room: size for them and seed again
+      ws->hint_seed = (size_t)n_first;
+      LTSG_CUDA(cudaMemsetAsync(d_ctr, 0, sizeof(Counters), st));
+      LTSG_CUDA(cudaMemsetAsync(gen_cnt, 0, sizeof(unsigned long long) * (kMaxGen + 1), st));
+      LTSG_TRY(ws_get(ws, "front0", (size_t)n_first, &front));
+      k_seed_static<<<(int)std::min<int64_t>(sc->n_pairs, 148 * 16), 128, 0, st>>>(
+          pr.pairs, sc->n_pairs, pr.bodies, woff, world, front, n_first, d_ctr, gen_cnt, sc->exhaustive);
+      LTSG_LAUNCHED();
+      LTSG_CUDA(cudaMemcpyAsync(&n_first, gen_cnt, sizeof(n_first), cudaMemcpyDeviceToHost, st));
+      LTSG_TRY(read_ctr(d_ctr, &h, st));
+    }
     int64_t n_front = (int64_t)n_first;
     int fsel = 0;
     const char* fname[2] = {"front0", "front1"};
@@ -2199,24 +2219,69 @@ static int fuse_stage(ltsg_workspace* ws, cudaStream_t st, Soa ro, unsigned long
   return LTSG_OK;
 }
 
-static int run_allpairs(const ltsg_scene* sc, int64_t* rows, int64_t* hits, ltsg_workspace* ws,
+static int build_world(const ltsg_scene* sc, const Prepared& pr, ltsg_workspace* ws, cudaStream_t st,
+                       double** world, int64_t** woff, int64_t* n_world, int* launches) {
+  int64_t* wcnt;
+  LTSG_TRY(ws_get(ws, "world_cnt", (size_t)sc->n_bodies + 1, &wcnt));
+  LTSG_TRY(ws_get(ws, "world_off", (size_t)sc->n_bodies + 1, woff));
+  k_world_count<<<grid_for(sc->n_bodies + 1, 128), 128, 0, st>>>(pr.bodies, sc->n_bodies, wcnt);
+  LTSG_CHECK_LAUNCH();
+  LTSG_TRY(scan_exclusive(ws, wcnt, *woff, sc->n_bodies + 1, st));
+  LTSG_CUDA(cudaMemcpyAsync(n_world, *woff + sc->n_bodies, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+  LTSG_CUDA(cudaStreamSynchronize(st));
+  if (*n_world >= (int64_t)1 << 31) {
+    *world = nullptr;
+    return LTSG_OK;
+  }
+  LTSG_TRY(ws_get(ws, "world", (size_t)std::max<int64_t>(*n_world, 1) * kWorld, world));
+  k_world_fill<<<(int)std::min<int64_t>(sc->n_bodies, 148 * 8), 128, 0, st>>>(pr.bodies, sc->n_bodies, *woff,
+                                                                              sc->tris, *world);
+  LTSG_CHECK_LAUNCH();
+  *launches += 2;
+  return LTSG_OK;
+}
+
+static int run_allpairs(const ltsg_scene* sc, int64_t* rows, int64_t* hits, double* ms, ltsg_workspace* ws,
                         cudaStream_t st) {
   LTSG_TRY(validate(sc));
+  LTSG_TRY(configure_kernels());
   Prepared pr{};
   LTSG_TRY(prepare(sc, ws, st, &pr));
   unsigned long long* d_hits;
   LTSG_TRY(ws_get(ws, "hits", 1, &d_hits));
   LTSG_CUDA(cudaMemsetAsync(d_hits, 0, sizeof(unsigned long long), st));
-  if (sc->n_pairs > 0) {
-    dim3 grid(148 * 4, (unsigned)std::min<int64_t>(sc->n_pairs, 65535));
-    k_allpairs<<<grid, 128, 0, st>>>(pr.pairs, sc->n_pairs, pr.bodies, sc->tris, d_hits);
+  *rows = 0;
+  *ms = 0.0;
+  if (sc->n_pairs > 0 && sc->n_bodies > 0) {
+    double* world;
+    int64_t* woff;
+    int64_t n_world = 0;
+    int launches = 0;
+    LTSG_TRY(build_world(sc, pr, ws, st, &world, &woff, &n_world, &launches));
+    if (!world) {
+      set_error("ltsg_exhaustive_rows: scene too large for the world cache");
+      return LTSG_ECAPACITY;
+    }
+    // rows = sum over pairs of fine sizes product (host-side from the level tables)
+    std::vector<int64_t> lev((size_t)sc->n_bodies * 18);
+    std::vector<int32_t> pb((size_t)sc->n_pairs * 2);
+    LTSG_CUDA(cudaMemcpyAsync(lev.data(), sc->body_levels, sizeof(int64_t) * lev.size(), cudaMemcpyDeviceToHost, st));
+    LTSG_CUDA(cudaMemcpyAsync(pb.data(), sc->pair_body, sizeof(int32_t) * pb.size(), cudaMemcpyDeviceToHost, st));
+    LTSG_CUDA(cudaStreamSynchronize(st));
+    for (int64_t k = 0; k < sc->n_pairs; ++k) *rows += lev[(size_t)pb[2 * k] * 18 + 10] * lev[(size_t)pb[2 * k + 1] * 18 + 10];
+    Timer t;
+    dim3 grid(148 * 8, (unsigned)std::min<int64_t>(sc->n_pairs, 65535));
+    t.start(st);
+    k_allpairs<<<grid, 32 * kStaticWarps, kStaticStageBytes, st>>>(pr.pairs, sc->n_pairs, pr.bodies, world, woff,
+                                                                   d_hits);
+    t.stop(st);
     LTSG_CHECK_LAUNCH();
+    *ms = t.ms();
   }
   unsigned long long h = 0;
   LTSG_CUDA(cudaMemcpyAsync(&h, d_hits, sizeof(h), cudaMemcpyDeviceToHost, st));
   LTSG_CUDA(cudaStreamSynchronize(st));
   *hits = (int64_t)h;
-  *rows = -1;  // computed by the caller from the tree sizes
   return LTSG_OK;
 }
 
@@ -2273,11 +2338,11 @@ extern "C" int ltsg_fuse_contacts(ltsg_result* io, int64_t n_raw, const uint64_t
   return rc;
 }
 
-extern "C" int ltsg_exhaustive_rows(const ltsg_scene* scene, int64_t* rows, int64_t* hits,
+extern "C" int ltsg_exhaustive_rows(const ltsg_scene* scene, int64_t* rows, int64_t* hits, double* ms,
                                     ltsg_workspace* ws, void* stream) {
-  if (!scene || !rows || !hits || !ws) {
+  if (!scene || !rows || !hits || !ms || !ws) {
     ltsg::set_error("ltsg_exhaustive_rows: null argument");
     return LTSG_EINVAL;
   }
-  return ltsg::run_allpairs(scene, rows, hits, ws, (cudaStream_t)stream);
+  return ltsg::run_allpairs(scene, rows, hits, ms, ws, (cudaStream_t)stream);
 }
