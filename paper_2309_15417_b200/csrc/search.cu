@@ -29,11 +29,11 @@ namespace ltsg {
 
 constexpr int kMaxLevels = 8;
 constexpr int kRecord = 16;  // doubles per triangle record
-constexpr int kWorld = 16;   // doubles per tau = 0 world record
+constexpr int kWorld = 20;   // doubles per tau = 0 world record
 // Relative slack of the certified culls: rows within this (times the
 // coordinate scale) of a threshold are always evaluated exactly.
 constexpr double kCullMargin = 1e-7;
-constexpr double kCullCond = 1e4;  // slivers (Lmax^2 > kCullCond * |e0 x e2|) are never culled
+// slivers (Lmax^2 > 1e4 |e0 x e2|, packing.CULL_COND) carry radius -1 and are never culled
 
 struct BodyInfo {
   Motion m;
@@ -483,13 +483,15 @@ k_screen(const Cand* __restrict__ front, int64_t n, const PairInfo* __restrict__
       me.cull_hi = 2.0 * p.dt + 1.0;
       if (__ldg(ra_ + 15) >= 0.0 && __ldg(rb_ + 15) >= 0.0) {
         const double T = fmax(me.thr, add(me.h, kRestSlop));
-        double sc0, sc1;
-        const double g0 = sphere_gap_at(bodies, p, ra_, rb_, c.w0, c.w0, p.dt, me.count, 0, pt, &sc0) -
-                          (T + kCullMargin * sc0);
-        const double g1 = p.dt > c.w0
-            ? sphere_gap_at(bodies, p, ra_, rb_, p.dt, c.w0, p.dt, me.count, me.count - 1, pt, &sc1) -
-                  (T + kCullMargin * sc1)
-            : g0;
+        double sc0 = 0.0, sc1 = 0.0;
+        // (the gap call sets the scale: evaluate it before reading sc0/sc1)
+        const double gap0 = sphere_gap_at(bodies, p, ra_, rb_, c.w0, c.w0, p.dt, me.count, 0, pt, &sc0);
+        const double g0 = gap0 - (T + kCullMargin * sc0);
+        double g1 = g0;
+        if (p.dt > c.w0) {
+          const double gap1 = sphere_gap_at(bodies, p, ra_, rb_, p.dt, c.w0, p.dt, me.count, me.count - 1, pt, &sc1);
+          g1 = gap1 - (T + kCullMargin * sc1);
+        }
         if (sp > 0.0) {
           me.cull_lo = c.w0 + g0 / sp;  // rows with tau < cull_lo are cleared
           me.cull_hi = p.dt - g1 / sp;  // rows with tau > cull_hi are cleared
@@ -670,12 +672,13 @@ k_screen(const Cand* __restrict__ front, int64_t n, const PairInfo* __restrict__
 
 // ---------------------------------------------------------------- static screen
 
-// World records at tau = 0 (the pose at the window start), 16 doubles each:
+// World records at tau = 0 (the pose at the window start), 20 doubles each:
 //   [0..8]  world corners x = base * local + x0 in the reference's einsum
 //           order -- exactly what rotation_at/position_at give at tau = 0
 //   [9] epsilon, [10] arm, [11] children (copied from the body record)
 //   [12..14] bounding-sphere centre (corner mean), [15] radius, or -1 when
-//           the triangle is a sliver (cond = Lmax^2 / |e0 x e2| > kCullCond)
+//           the triangle is a sliver (cond = Lmax^2 / |e0 x e2| > 1e4)
+//   [16..18] unit face normal n, [19] plane offset n . v0 (cull data only)
 
 __global__ void k_world_count(const BodyInfo* __restrict__ bodies, int n, int64_t* cnt) {
   const int b = blockIdx.x * blockDim.x + threadIdx.x;
@@ -695,6 +698,7 @@ __global__ void __launch_bounds__(128) k_world_fill(const BodyInfo* __restrict__
   // 128 records per block iteration, moved through shared memory so that both
   // the record loads and the world-record stores are fully coalesced.
   __shared__ double s_rec[128 * kRecord];
+  __shared__ double s_out[128 * kWorld];
   for (int b = blockIdx.x; b < n; b += gridDim.x) {
     const BodyInfo& B = bodies[b];
     const int64_t cnt = woff[b + 1] - woff[b];
@@ -713,7 +717,9 @@ __global__ void __launch_bounds__(128) k_world_fill(const BodyInfo* __restrict__
 #pragma unroll
         for (int k = 0; k < 9; ++k) L[k] = r[k];
         const Tri t = world_tri(B.m.base, pos, L);
-        double* w = r;  // in place: same 16-slot layout
+        double* w = s_out + threadIdx.x * kWorld;
+        w[9] = r[9];
+        w[10] = r[10];
 #pragma unroll
         for (int k = 0; k < 3; ++k) {
           w[3 * k] = t.v[k].x;
@@ -738,14 +744,26 @@ __global__ void __launch_bounds__(128) k_world_fill(const BodyInfo* __restrict__
           const V3 d = t.v[k] - c;
           r2 = fmax(r2, d.x * d.x + d.y * d.y + d.z * d.z);
         }
+        // unit face normal and plane offset for the separating-axis cull
+        const V3 e1{t.v[1].x - t.v[0].x, t.v[1].y - t.v[0].y, t.v[1].z - t.v[0].z};
+        const V3 e2{t.v[2].x - t.v[0].x, t.v[2].y - t.v[0].y, t.v[2].z - t.v[0].z};
+        const V3 nn{fma(e1.y, e2.z, -e1.z * e2.y), fma(e1.z, e2.x, -e1.x * e2.z), fma(e1.x, e2.y, -e1.y * e2.x)};
+        const double nl = sqrt(fma(nn.x, nn.x, fma(nn.y, nn.y, nn.z * nn.z)));
+        const double inv = nl > 0.0 ? 1.0 / nl : 0.0;
+        w[16] = nn.x * inv;
+        w[17] = nn.y * inv;
+        w[18] = nn.z * inv;
+        w[19] = fma(w[16], t.v[0].x, fma(w[17], t.v[0].y, w[18] * t.v[0].z));
         w[12] = c.x;
         w[13] = c.y;
         w[14] = c.z;
-        w[15] = rad >= 0.0 ? sqrt(r2) * (1.0 + 1e-12) : -1.0;  // sliver flag from the body record
+        // sliver flag from the body record; a zero-area triangle is never culled either
+        w[15] = rad >= 0.0 && nl > 0.0 ? sqrt(r2) * (1.0 + 1e-12) : -1.0;
       }
       __syncthreads();
       double2* dst = reinterpret_cast<double2*>(world + (size_t)(woff[b] + j0) * kWorld);
-      for (int k = threadIdx.x; k < m * kWorld / 2; k += blockDim.x) dst[k] = sm2[k];
+      const double2* so2 = reinterpret_cast<const double2*>(s_out);
+      for (int k = threadIdx.x; k < m * kWorld / 2; k += blockDim.x) dst[k] = so2[k];
       __syncthreads();
     }
   }
@@ -784,6 +802,55 @@ __device__ __forceinline__ bool sphere_cull(const double* wa, const double* wb, 
   return dx * dx + dy * dy + dz * dz > reach * reach;
 }
 
+// Certified separating-axis cull on static world records.  For any direction
+// u the gap between the projections of the two triangles onto u, divided by
+// |u|, is a lower bound of their distance; the axes are both face normals
+// (a triangle projects onto its own normal as the single value n . v0) and
+// the centroid direction.  The same rounding argument as sphere_cull applies
+// (the margin is far above the few-ulp error of these dot products), and
+// slivers or zero-area triangles (radius slot < 0) are never culled.  This is
+// cull arithmetic, not reference arithmetic: it may use FMA freely.
+__device__ __forceinline__ bool sat_cull(const double* wa, const double* wb, double thr) {
+  const double ra = __ldg(wa + 15), rb = __ldg(wb + 15);
+  if (ra < 0.0 || rb < 0.0) return false;
+  // loads are staged axis by axis (corners re-read from L1) to keep the
+  // register footprint low: the filter kernel runs at high occupancy
+  const double ca0 = __ldg(wa + 12), ca1 = __ldg(wa + 13), ca2 = __ldg(wa + 14);
+  const double cb0 = __ldg(wb + 12), cb1 = __ldg(wb + 13), cb2 = __ldg(wb + 14);
+  const double scale = 1.0 + fabs(ca0) + fabs(ca1) + fabs(ca2) + fabs(cb0) + fabs(cb1) + fabs(cb2) + ra + rb;
+  const double T = thr + kCullMargin * scale;
+  // a face normal against the other triangle's corners (the own triangle
+  // projects to the single value n . v0 stored in slot 19)
+  auto face_gap = [&](const double* w, const double* o) {
+    const double2 n01 = __ldg(reinterpret_cast<const double2*>(w + 16));
+    const double2 n2d = __ldg(reinterpret_cast<const double2*>(w + 18));
+    double lo = 0.0, hi = 0.0;
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+      const double x = fma(n01.x, __ldg(o + 3 * k), fma(n01.y, __ldg(o + 3 * k + 1), n2d.x * __ldg(o + 3 * k + 2)));
+      lo = k ? fmin(lo, x) : x;
+      hi = k ? fmax(hi, x) : x;
+    }
+    return fmax(lo - n2d.y, n2d.y - hi);
+  };
+  if (face_gap(wa, wb) > T) return true;
+  if (face_gap(wb, wa) > T) return true;
+  // centroid direction
+  const double u0 = cb0 - ca0, u1 = cb1 - ca1, u2 = cb2 - ca2;
+  const double len = sqrt(fma(u0, u0, fma(u1, u1, u2 * u2)));
+  double alo = 0.0, ahi = 0.0, blo = 0.0, bhi = 0.0;
+#pragma unroll
+  for (int k = 0; k < 3; ++k) {
+    const double x = fma(u0, __ldg(wa + 3 * k), fma(u1, __ldg(wa + 3 * k + 1), u2 * __ldg(wa + 3 * k + 2)));
+    const double y = fma(u0, __ldg(wb + 3 * k), fma(u1, __ldg(wb + 3 * k + 1), u2 * __ldg(wb + 3 * k + 2)));
+    alo = k ? fmin(alo, x) : x;
+    ahi = k ? fmax(ahi, x) : x;
+    blo = k ? fmin(blo, y) : y;
+    bhi = k ? fmax(bhi, y) : y;
+  }
+  return fmax(blo - ahi, alo - bhi) > T * len;
+}
+
 constexpr int kStaticWarps = 4;
 constexpr int kStaticStageBytes = kStaged * 32 * kStaticWarps * sizeof(double);
 #ifndef LTSG_STATIC_MINB
@@ -811,6 +878,7 @@ __global__ void k_seed_static(const PairInfo* __restrict__ pairs, int64_t n_pair
                               const double* __restrict__ world, Cand* out, unsigned long long cap,
                               Counters* ctr, unsigned long long* n_out, int exhaustive) {
   const int lane = threadIdx.x & 31;
+  unsigned long long culled = 0;
   for (int64_t k = blockIdx.x; k < n_pairs; k += gridDim.x) {
     const PairInfo p = pairs[k];
     const BodyInfo& A = bodies[p.ba];
@@ -830,11 +898,9 @@ __global__ void k_seed_static(const PairInfo* __restrict__ pairs, int64_t n_pair
       }
       const unsigned m = __ballot_sync(0xffffffffu, keep);
       const int nvalid = (int)min((int64_t)32, na * nb - j0);
+      culled += (unsigned long long)(nvalid - __popc(m));
       unsigned long long base = 0;
-      if (lane == 0) {
-        atomicAdd(&ctr->rows, (unsigned long long)(nvalid - __popc(m)));
-        if (m) base = atomicAdd(n_out, (unsigned long long)__popc(m));
-      }
+      if (lane == 0 && m) base = atomicAdd(n_out, (unsigned long long)__popc(m));
       base = __shfl_sync(0xffffffffu, base, 0);
       if (keep) {
         const unsigned long long dst = base + __popc(m & ((1u << lane) - 1u));
@@ -842,6 +908,27 @@ __global__ void k_seed_static(const PairInfo* __restrict__ pairs, int64_t n_pair
       }
     }
   }
+  if (lane == 0 && culled) atomicAdd(&ctr->rows, culled);
+}
+
+// Sphere data of one world record, pre-folded for the emission cull:
+// centre, and R = radius + epsilon (+ the margin share of this side).
+struct EmitSphere {
+  double x, y, z, r, e, s;  // centre, radius (-1: sliver), epsilon, |centre|_1
+};
+__device__ __forceinline__ EmitSphere emit_sphere(const double* w) {
+  const double2 c01 = __ldg(reinterpret_cast<const double2*>(w + 12));
+  const double2 c2r = __ldg(reinterpret_cast<const double2*>(w + 14));
+  return EmitSphere{c01.x, c01.y, c2r.x, c2r.y, __ldg(w + 9), fabs(c01.x) + fabs(c01.y) + fabs(c2r.x)};
+}
+// Same certified test as static_child_cull / sphere_cull (scale from A's centre).
+__device__ __forceinline__ bool emit_cull(const EmitSphere& a, const EmitSphere& b) {
+  if (a.r < 0.0 || b.r < 0.0) return false;
+  const double dx = a.x - b.x, dy = a.y - b.y, dz = a.z - b.z;
+  const double thr = add(add(a.e, b.e), kRestSlop);
+  const double scale = 1.0 + a.s + a.r + b.r;
+  const double reach = a.r + b.r + thr + kCullMargin * scale;
+  return fma(dx, dx, fma(dy, dy, dz * dz)) > reach * reach;
 }
 
 __global__ void __launch_bounds__(32 * kStaticWarps, LTSG_STATIC_MINB)
@@ -851,40 +938,21 @@ k_screen_static(const Cand* __restrict__ front, int64_t n, const PairInfo* __res
   if (out.n_in) n = (int64_t)min(*out.n_in, out.next_cap);
   extern __shared__ double s_stage[];  // kStaged x (32 * kStaticWarps)
   const Staged<32 * kStaticWarps> st{s_stage + threadIdx.x};
-  const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
-  // Child descriptors live in the first four stage rows of the warp's own
-  // columns once the rows are evaluated (no extra shared memory: five
-  // blocks fit per SM).
-  auto put_kid = [&](const ChildInfo& c) {
-    int2* col = reinterpret_cast<int2*>(s_stage + threadIdx.x);
-    col[0 * 32 * kStaticWarps] = make_int2(c.first, c.count);
-    col[1 * 32 * kStaticWarps] = make_int2(c.pair, c.ia0);
-    col[2 * 32 * kStaticWarps] = make_int2(c.ib0, c.nb);
-    col[3 * 32 * kStaticWarps] = make_int2(c.la, c.lb);
-  };
-  auto kid_first = [&](int o) { return reinterpret_cast<const int2*>(s_stage + warp * 32 + o)[0].x; };
-  auto get_kid = [&](int o) {
-    const int2* col = reinterpret_cast<const int2*>(s_stage + warp * 32 + o);
-    ChildInfo c;
-    const int2 a = col[0], b = col[1 * 32 * kStaticWarps], d = col[2 * 32 * kStaticWarps],
-               e = col[3 * 32 * kStaticWarps];
-    c.first = a.x;
-    c.count = a.y;
-    c.pair = b.x;
-    c.ia0 = b.y;
-    c.ib0 = d.x;
-    c.nb = d.y;
-    c.la = e.x;
-    c.lb = e.y;
-    c.w0 = 0.0;
-    return c;
-  };
+  const int warp = threadIdx.x >> 5;
+  // The frontier holds only rows that survived the certified culls (sphere
+  // at emission, separating axes in k_sat_filter): every row gets the exact
+  // 15-feature distance, one per lane.  A flagged coarse row is then
+  // expanded by its own lane: the na x nb children (ccd.py:418-427) are
+  // sphere-culled with the child spheres held in registers, counted, and
+  // the survivors written after one warp-wide scan and one atomic.
+  unsigned long long culled = 0;
+  if (blockIdx.x == 0 && threadIdx.x == 0) atomicAdd(&out.ctr->screen_exact, (unsigned long long)n);
   const int64_t n_warps = (n + 31) / 32;
   for (int64_t wi = blockIdx.x * (int64_t)kStaticWarps + warp; wi < n_warps;
        wi += (int64_t)gridDim.x * kStaticWarps) {
     const int64_t ci = wi * 32 + lane;
-    ChildInfo ch{};
+    int cnt = 0, na = 1, nb = 1, a0 = 0, b0 = 0, cla = 0, clb = 0, cpair = 0;
     if (ci < n) {
       const Cand c = front[ci];
       const double* wa = world + (size_t)c.ia * kWorld;
@@ -900,72 +968,114 @@ k_screen_static(const Cand* __restrict__ front, int64_t n, const PairInfo* __res
             out.resting[slot] = RestRec{c.pair, (int32_t)(c.ia - woff[p.ba]), (int32_t)(c.ib - woff[p.bb]), 0, h};
         }
       } else if (d <= h) {
-        int na = 1, nb = 1;
-        ch.ia0 = c.ia;
-        ch.ib0 = c.ib;
+        a0 = c.ia;
+        b0 = c.ib;
         if (c.la > 0) {
           const int2 cr = *reinterpret_cast<const int2*>(wa + 11);
-          ch.ia0 = cr.x;
+          a0 = cr.x;
           na = cr.y;
         }
         if (c.lb > 0) {
           const int2 cr = *reinterpret_cast<const int2*>(wb + 11);
-          ch.ib0 = cr.x;
+          b0 = cr.x;
           nb = cr.y;
         }
-        ch.pair = c.pair;
-        ch.nb = nb;
-        ch.count = na * nb;
-        ch.la = c.la > 0 ? c.la - 1 : 0;
-        ch.lb = c.lb > 0 ? c.lb - 1 : 0;
+        cpair = c.pair;
+        cnt = na * nb;
+        cla = c.la > 0 ? c.la - 1 : 0;
+        clb = c.lb > 0 ? c.lb - 1 : 0;
       }
     }
-    const int cincl = warp_incl_scan(ch.count, lane);
-    const int ctotal = __shfl_sync(0xffffffffu, cincl, 31);
-    if (lane == 0) {
-      const int64_t left = n - wi * 32;
-      atomicAdd(&out.ctr->rows, (unsigned long long)(left < 32 ? left : 32));
-      atomicAdd(&out.ctr->screen_exact, (unsigned long long)(left < 32 ? left : 32));
+    // children in chunks of 64 per lane (a fanout-4 parent pair has 16)
+    for (int c0 = 0; __any_sync(0xffffffffu, c0 < cnt); c0 += 64) {
+      const int m = cnt > c0 ? min(64, cnt - c0) : 0;
+      unsigned long long mask = 0;
+      int k0 = 0, l0 = 0;
+      if (m > 0) {
+        k0 = c0 / nb;
+        l0 = c0 - k0 * nb;
+        int k = k0, l = l0;
+        EmitSphere sa = emit_sphere(world + (size_t)(a0 + k) * kWorld);
+        for (int j = 0; j < m; ++j) {
+          const EmitSphere sb = emit_sphere(world + (size_t)(b0 + l) * kWorld);
+          if (!emit_cull(sa, sb)) mask |= 1ULL << j;
+          if (++l == nb) {
+            l = 0;
+            ++k;
+            if (j + 1 < m) sa = emit_sphere(world + (size_t)(a0 + k) * kWorld);
+          }
+        }
+      }
+      const int kept = __popcll(mask);
+      culled += (unsigned long long)(m - kept);
+      const int incl = warp_incl_scan(kept, lane);
+      const int tot = __shfl_sync(0xffffffffu, incl, 31);
+      unsigned long long base = 0;
+      if (lane == 31 && tot) base = atomicAdd(out.n_out, (unsigned long long)tot);
+      base = __shfl_sync(0xffffffffu, base, 31);
+      unsigned long long dst = base + (unsigned long long)(incl - kept);
+      int k = k0, l = l0;
+      for (int j = 0; j < m; ++j) {
+        if ((mask >> j) & 1ULL) {
+          if (dst < out.next_cap)
+            out.next[dst] = Cand{cpair, a0 + k, b0 + l, (int16_t)cla, (int16_t)clb, 0.0};
+          ++dst;
+        }
+        if (++l == nb) {
+          l = 0;
+          ++k;
+        }
+      }
     }
-    if (ctotal) {
-      ch.first = cincl - ch.count;
-      __syncwarp();  // every lane is done with its stage rows
-      put_kid(ch);
-      __syncwarp();
-      unsigned long long culled = 0;
-      for (int s0 = 0; s0 < ctotal; s0 += 32) {
-        const int s = s0 + lane;
-        bool keep = false;
-        Cand nc{};
-        if (s < ctotal) {
-          int o = 0;
+  }
+  for (int o = 16; o > 0; o >>= 1) culled += __shfl_xor_sync(0xffffffffu, culled, o);
+  if (lane == 0 && culled) atomicAdd(&out.ctr->rows, culled);  // children settled by the sphere cull
+}
+
+// Separating-axis filter between two static generations: every frontier row
+// is a test (counted here); rows the certified cull settles are dropped, the
+// rest are compacted (one atomic per block iteration) for k_screen_static.
+// Runs at full occupancy: it is load-latency bound, the exact kernel is not.
+constexpr int kSatThreads = 256;
+#ifndef LTSG_SAT_MINB
+#define LTSG_SAT_MINB 4
+#endif
+__global__ void __launch_bounds__(kSatThreads, LTSG_SAT_MINB)
+k_sat_filter(const Cand* __restrict__ in, int64_t n, const unsigned long long* n_in, unsigned long long in_cap,
+             const double* __restrict__ world, Cand* __restrict__ out, unsigned long long* n_out,
+             Counters* ctr) {
+  if (n_in) n = (int64_t)min(*n_in, in_cap);
+  __shared__ int s_cnt[kSatThreads / 32];
+  __shared__ unsigned long long s_base;
+  const int warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
+  if (blockIdx.x == 0 && threadIdx.x == 0 && n > 0) atomicAdd(&ctr->rows, (unsigned long long)n);
+  for (int64_t b0 = (int64_t)blockIdx.x * kSatThreads; b0 < n; b0 += (int64_t)gridDim.x * kSatThreads) {
+    const int64_t ci = b0 + threadIdx.x;
+    bool keep = false;
+    Cand c{};
+    if (ci < n) {
+      c = in[ci];
+      const double* wa = world + (size_t)c.ia * kWorld;
+      const double* wb = world + (size_t)c.ib * kWorld;
+      keep = !sat_cull(wa, wb, add(add(__ldg(wa + 9), __ldg(wb + 9)), kRestSlop));
+    }
+    const unsigned m = __ballot_sync(0xffffffffu, keep);
+    if (lane == 0) s_cnt[warp] = __popc(m);
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      int tot = 0;
 #pragma unroll
-          for (int step = 16; step > 0; step >>= 1)
-            if (kid_first(o + step) <= s) o += step;
-          const ChildInfo k = get_kid(o);
-          const int jj = s - k.first;
-          nc.pair = k.pair;
-          nc.ia = k.ia0 + jj / k.nb;
-          nc.ib = k.ib0 + jj % k.nb;
-          nc.la = (int16_t)k.la;
-          nc.lb = (int16_t)k.lb;
-          nc.w0 = 0.0;
-          keep = !static_child_cull(world, nc.ia, nc.ib);
-        }
-        const unsigned m = __ballot_sync(0xffffffffu, keep);
-        const int nvalid = ctotal - s0 < 32 ? ctotal - s0 : 32;
-        culled += (unsigned long long)(nvalid - __popc(m));
-        unsigned long long base = 0;
-        if (lane == 0 && m) base = atomicAdd(out.n_out, (unsigned long long)__popc(m));
-        base = __shfl_sync(0xffffffffu, base, 0);
-        if (keep) {
-          const unsigned long long dst = base + __popc(m & ((1u << lane) - 1u));
-          if (dst < out.next_cap) out.next[dst] = nc;
-        }
+      for (int w = 0; w < kSatThreads / 32; ++w) {
+        const int x = s_cnt[w];
+        s_cnt[w] = tot;
+        tot += x;
       }
-      if (lane == 0 && culled) atomicAdd(&out.ctr->rows, culled);
-      __syncwarp();
+      s_base = tot ? atomicAdd(n_out, (unsigned long long)tot) : 0ULL;
     }
+    __syncthreads();
+    if (keep) out[s_base + s_cnt[warp] + __popc(m & ((1u << lane) - 1u))] = c;
+    __syncthreads();
   }
 }
 
@@ -1851,8 +1961,9 @@ static int run_search(const ltsg_scene* sc, ltsg_result* out, ltsg_workspace* ws
     LTSG_CUDA(cudaStreamSynchronize(st));
   }
   constexpr int kMaxGen = 2 * kMaxLevels;
-  unsigned long long* gen_cnt;
+  unsigned long long *gen_cnt, *x_cnt;
   LTSG_TRY(ws_get(ws, "gen_cnt", kMaxGen + 1, &gen_cnt));
+  LTSG_TRY(ws_get(ws, "x_cnt", kMaxGen + 1, &x_cnt));  // static: survivors of k_sat_filter per generation
   const int64_t fan = (int64_t)sc->max_children * sc->max_children;
   size_t rest_cap = std::max<size_t>(1 << 16, ws->hint_rest), entry_cap = std::max<size_t>(1 << 14, ws->hint_entries),
          cross_cap = std::max<size_t>(1 << 14, ws->hint_cross);
@@ -1863,12 +1974,21 @@ static int run_search(const ltsg_scene* sc, ltsg_result* out, ltsg_workspace* ws
   Cand* front = nullptr;
 
   auto launch_screen = [&](const Cand* in, int64_t n, const unsigned long long* n_in, Cand* next,
-                           unsigned long long cap, unsigned long long* n_out) -> int {
+                           unsigned long long cap, unsigned long long* n_out, Cand* xbuf,
+                           unsigned long long* xcnt) -> int {
     ScreenOut so{next, cap, n_in, n_out, resting, rest_cap, entries, entry_cap, cross, cross_cap, d_ctr};
     if (all_static) {
+      // separating-axis filter into xbuf (count in xcnt), then the exact screen of the survivors
+      const int64_t sblocks = n_in ? 148LL * 8 : (n + kSatThreads - 1) / kSatThreads;
+      k_sat_filter<<<(int)std::max<int64_t>(1, std::min<int64_t>(sblocks, 148LL * 8)), kSatThreads, 0, st>>>(
+          in, n, n_in, cap, world, xbuf, xcnt, d_ctr);
+      LTSG_LAUNCHED();
+      in = xbuf;
+      so.n_in = xcnt;
       // async: the frontier size is unknown on the host; a generous grid lets
       // the block scheduler balance uneven rows (spare blocks exit at once)
       const int64_t blocks = n_in ? 148LL * 16 : (n + 32 * kStaticWarps - 1) / (32 * kStaticWarps);
+      n_in = xcnt;
       k_screen_static<<<(int)std::max<int64_t>(1, std::min<int64_t>(blocks, 148LL * 32)), 32 * kStaticWarps,
                         kStaticStageBytes, st>>>(in, n, pr.pairs, pr.bodies, world, woff, so);
     } else {
@@ -1884,6 +2004,7 @@ static int run_search(const ltsg_scene* sc, ltsg_result* out, ltsg_workspace* ws
     *overflow = false;
     LTSG_CUDA(cudaMemsetAsync(d_ctr, 0, sizeof(Counters), st));
     LTSG_CUDA(cudaMemsetAsync(gen_cnt, 0, sizeof(unsigned long long) * (kMaxGen + 1), st));
+    LTSG_CUDA(cudaMemsetAsync(x_cnt, 0, sizeof(unsigned long long) * (kMaxGen + 1), st));
     LTSG_TRY(ws_get(ws, "resting", rest_cap, &resting));
     LTSG_TRY(ws_get(ws, "entries", entry_cap, &entries));
     LTSG_TRY(ws_get(ws, "cross", cross_cap, &cross));
@@ -1912,8 +2033,11 @@ static int run_search(const ltsg_scene* sc, ltsg_result* out, ltsg_workspace* ws
       Cand* buf[2];
       buf[0] = front;
       LTSG_TRY(ws_get(ws, "front1", cap_async, &buf[1]));
+      Cand* xbuf = nullptr;
+      if (all_static) LTSG_TRY(ws_get(ws, "frontx", cap_async, &xbuf));
       for (int g = 1; g <= kMaxGen; ++g)
-        LTSG_TRY(launch_screen(buf[(g - 1) & 1], 0, gen_cnt + g - 1, buf[g & 1], cap_async, gen_cnt + g));
+        LTSG_TRY(launch_screen(buf[(g - 1) & 1], 0, gen_cnt + g - 1, buf[g & 1], cap_async, gen_cnt + g, xbuf,
+                               x_cnt + g));
       t_screen.stop(st);
       unsigned long long hg[kMaxGen + 1];
       LTSG_CUDA(cudaMemcpyAsync(hg, gen_cnt, sizeof(hg), cudaMemcpyDeviceToHost, st));
@@ -1955,12 +2079,16 @@ static int run_search(const ltsg_scene* sc, ltsg_result* out, ltsg_workspace* ws
     while (n_front > 0) {
       Cand* next;
       LTSG_TRY(ws_get(ws, fname[fsel ^ 1], (size_t)(n_front * fan), &next));
+      Cand* xbuf = nullptr;
+      if (all_static) LTSG_TRY(ws_get(ws, "frontx", (size_t)n_front, &xbuf));
       Counters before = h;
       for (;;) {
         LTSG_CUDA(cudaMemcpyAsync(d_ctr, &before, sizeof(Counters), cudaMemcpyHostToDevice, st));
         LTSG_CUDA(cudaMemsetAsync(gen_cnt + 1, 0, sizeof(unsigned long long), st));
+        LTSG_CUDA(cudaMemsetAsync(x_cnt, 0, sizeof(unsigned long long), st));
         t_screen.start(st);
-        LTSG_TRY(launch_screen(front, n_front, nullptr, next, (unsigned long long)(n_front * fan), gen_cnt + 1));
+        LTSG_TRY(launch_screen(front, n_front, nullptr, next, (unsigned long long)(n_front * fan), gen_cnt + 1, xbuf,
+                               x_cnt));
         t_screen.stop(st);
         LTSG_TRY(read_ctr(d_ctr, &h, st));
         out->ms_screen += t_screen.ms();
