@@ -389,7 +389,7 @@ def run_ours(args, rank, world, local_rank):
             "config": {"workload": args.config + (" exhaustive" if args.exhaustive else ""),
                        "description": CONFIG_DOC[args.config],
                        "problems_per_gpu": len(problems), "pairs_per_gpu": len(hs.pair_problem),
-                       "triangle_records_per_gpu": int(len(hs.tris)),
+                       "triangle_records_per_gpu": int(hs.n_tris),
                        "l2": "flushed (256 MiB write) before every timed step",
                        "parallelism": f"weak: {world} independent shards"},
             "contacts_per_s": contacts_all / (total_ms * 1e-3),

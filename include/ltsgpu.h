@@ -110,6 +110,43 @@ typedef struct {
   int32_t max_children;  /* max children per surrogate triangle (fanout) */
 } ltsg_scene;
 
+/* ---------------------------------------------------------------- compact tree upload
+ *
+ * The triangle records of `ltsg_scene.tris` rebuilt on the device from a
+ * compact host image (about 1/3 of the record bytes): the fine level as
+ * deduplicated vertices plus three vertex indices per triangle (the
+ * reference's level-0 corners are rows of the mesh vertex array,
+ * body.py:70-72 / surrogate.py:91, so the dedup is exact), the coarse
+ * levels as 9 corners, epsilon per record (or one value for a constant
+ * fine level, surrogate.py:89), and (first child, count) per coarse
+ * record.  The derived slots are computed on the device: arm with the
+ * reference's norm order (ccd._Motion.arm, ccd.py:108-114) and the cull
+ * sphere.  Replaces the host-side record build of the packer; the result is
+ * bit-identical to it in slots 0-11.
+ *
+ * Per tree (table row of 8 int64):
+ *   rec_off   first record of the tree in `tris_out`
+ *   n_fine    level-0 record count (records rec_off .. rec_off+n_fine-1)
+ *   n_coarse  coarse record count (the records after the fine ones)
+ *   vert_off  first vertex of the tree in `verts`
+ *   vidx_off  first fine record of the tree in `vidx` (3 int32 each; tree-local vertex ids)
+ *   coarse_off first coarse record of the tree in `coarse` (9 doubles each) and `kids` (2 int32 each)
+ *   eps_off   first epsilon of the tree in `eps`
+ *   eps_mode  1: one epsilon per record; 0: eps[eps_off] for every fine record,
+ *             then one per coarse record */
+typedef struct {
+  const double* verts;
+  const int32_t* vidx;
+  const double* coarse;
+  const double* eps;
+  const int32_t* kids;
+  const int64_t* table;
+  int32_t n_trees;
+  int32_t pad;
+} ltsg_tree_upload;
+
+int ltsg_unpack_trees(const ltsg_tree_upload* up, double* tris_out, void* stream);
+
 /* Per-problem results and the contact lists (device buffers, caller-owned).
  * Contacts are SoA; `fused_*` are the filter_contacts output grouped by
  * problem (problem p's fused contacts are [fused_offset[p], fused_offset[p+1]));

@@ -32,6 +32,14 @@ class Scene(C.Structure):
     ]
 
 
+class TreeUpload(C.Structure):
+    """ltsg_tree_upload: the compact tree image ltsg_unpack_trees expands."""
+    _fields_ = [
+        ("verts", P), ("vidx", P), ("coarse", P), ("eps", P), ("kids", P), ("table", P),
+        ("n_trees", I32), ("pad", I32),
+    ]
+
+
 class Result(C.Structure):
     _fields_ = [
         ("dt", P), ("first_contact", P), ("collision", P), ("fused_offset", P),
@@ -86,6 +94,7 @@ def lib():
             "ltsg_exhaustive_rows": [C.POINTER(Scene), C.POINTER(I64), C.POINTER(I64), C.POINTER(F64), P, P],
             "ltsg_fuse_contacts": [C.POINTER(Result), I64, P, P, P],
             "ltsg_fp64_peak": [C.POINTER(F64), C.POINTER(F64), P],
+            "ltsg_unpack_trees": [C.POINTER(TreeUpload), P, P],
         }.items():
             fn = getattr(h, name)
             fn.argtypes = args
@@ -105,6 +114,7 @@ EXPORTED = (
     "ltsg_segment_segment_closest", "ltsg_feature_distances", "ltsg_closest_feature",
     "ltsg_overlap_centroid", "ltsg_workspace_create", "ltsg_workspace_destroy",
     "ltsg_workspace_bytes", "ltsg_search", "ltsg_exhaustive_rows", "ltsg_fuse_contacts", "ltsg_fp64_peak",
+    "ltsg_unpack_trees",
 )
 
 

@@ -134,12 +134,21 @@ class DeviceScene:
             src = torch.from_numpy(np.ascontiguousarray(v))
             self.t[k] = src.to(dev, non_blocking=non_blocking)
         self.device = dev
+        # triangle records rebuilt on the device from the compact image
+        self.t["tris"] = torch.empty((max(hs.n_tris, 1), packing.RECORD), dtype=torch.float64, device=dev)
+        t = self.t
+        up = _lib.TreeUpload(verts=_ptr(t["up_verts"]), vidx=_ptr(t["up_vidx"]), coarse=_ptr(t["up_coarse"]),
+                             eps=_ptr(t["up_eps"]), kids=_ptr(t["up_kids"]), table=_ptr(t["up_table"]),
+                             n_trees=len(hs.up_table))
+        st = torch.cuda.current_stream(dev)
+        _lib.check(_lib.lib().ltsg_unpack_trees(C.byref(up), C.c_void_p(_ptr(t["tris"])),
+                                               C.c_void_p(st.cuda_stream)), "ltsg_unpack_trees")
 
     def struct(self, widen: float, exhaustive: bool) -> _lib.Scene:
         t = self.t
         hs = self.host
         return _lib.Scene(
-            tris=_ptr(t["tris"]), tri_orig=_ptr(t["tri_orig"]), n_tris=len(hs.tris),
+            tris=_ptr(t["tris"]), tri_orig=_ptr(t["tri_orig"]), n_tris=hs.n_tris,
             body_state=_ptr(t["body_state"]), body_levels=_ptr(t["body_levels"]),
             n_bodies=len(hs.body_state), n_problems=hs.n_problems,
             pair_body=_ptr(t["pair_body"]), pair_problem=_ptr(t["pair_problem"]),

@@ -36,11 +36,22 @@ CULL_COND = 1e4  # slivers (Lmax^2 > CULL_COND * |e0 x e2|) are never culled
 
 @dataclass
 class PackedTree:
-    records: np.ndarray      # (n, 12) float64
+    records: np.ndarray      # (n, 16) float64
     orig: np.ndarray         # (n,) int32
     level_off: np.ndarray    # (L,) int64, record offset of each level within the tree
     level_size: np.ndarray   # (L,) int64
     max_children: int
+    # compact upload image (ltsg_tree_upload): the device rebuilds `records`
+    verts: np.ndarray = None   # (nv, 3) float64 distinct fine-level corners (bitwise)
+    vidx: np.ndarray = None    # (n_fine, 3) int32 tree-local vertex ids, record order
+    coarse: np.ndarray = None  # (n - n_fine, 9) float64 coarse corners
+    eps: np.ndarray = None     # eps_mode 1: (n,); 0: [fine eps, coarse eps...]
+    eps_mode: int = 1
+    kids: np.ndarray = None    # (n - n_fine, 2) int32 (first child, count)
+
+    @property
+    def upload_nbytes(self) -> int:
+        return sum(a.nbytes for a in (self.verts, self.vidx, self.coarse, self.eps, self.kids, self.orig))
 
 
 _cache_lock = threading.Lock()
@@ -131,18 +142,46 @@ def _pack_tree(tree) -> PackedTree:
                     | (cn.astype(np.uint32).astype(np.uint64) << np.uint64(32)))
             recs[sl, 11] = pair.view(np.float64)
         orig[sl] = p.astype(np.int32)
-    return PackedTree(records=recs, orig=orig, level_off=offs, level_size=sizes,
-                      max_children=max_children)
+    return _with_upload(PackedTree(records=recs, orig=orig, level_off=offs, level_size=sizes,
+                                   max_children=max_children))
+
+
+def _with_upload(pt: PackedTree) -> PackedTree:
+    """Attach the compact upload image.  The fine level's corners are rows of
+    the mesh vertex array (body.py:70-72), so they are deduplicated on their
+    bit patterns (exact, -0.0 kept apart from 0.0)."""
+    n0 = int(pt.level_size[0])
+    fine = np.ascontiguousarray(pt.records[:n0, :9]).reshape(-1, 3)
+    bits = fine.view(np.uint64)
+    uniq, inv = np.unique(bits, axis=0, return_inverse=True)
+    pt.verts = np.ascontiguousarray(uniq).view(np.float64).reshape(-1, 3)
+    pt.vidx = inv.reshape(n0, 3).astype(np.int32)
+    pt.coarse = np.ascontiguousarray(pt.records[n0:, :9])
+    e = pt.records[:, 9]
+    e0 = e[:n0].view(np.uint64)
+    if n0 > 0 and np.all(e0 == e0[0]):
+        pt.eps_mode = 0
+        pt.eps = np.concatenate([e[:1], e[n0:]])
+    else:
+        pt.eps_mode = 1
+        pt.eps = e.copy()
+    pt.kids = np.ascontiguousarray(pt.records[n0:, 11]).view(np.int32).reshape(-1, 2).copy()
+    return pt
 
 
 def body_id(body) -> int:
     return int(body.pid) if hasattr(body, "timeline") else int(body.sid)
 
 
+UPLOAD_KEYS = ("up_verts", "up_vidx", "up_coarse", "up_eps", "up_kids", "up_table")
+
+
 @dataclass
 class HostScene:
-    """Packed scene in host (optionally pinned) memory."""
-    tris: np.ndarray
+    """Packed scene in host (optionally pinned) memory.  The triangle records
+    travel as the compact upload image (`up_*`, ltsg_tree_upload) and are
+    rebuilt on the device; `records()` assembles them on the host."""
+    n_tris: int
     tri_orig: np.ndarray
     body_state: np.ndarray
     body_levels: np.ndarray
@@ -154,15 +193,26 @@ class HostScene:
     max_children: int
     n_problems: int
     body_ids: np.ndarray
+    up_verts: np.ndarray
+    up_vidx: np.ndarray
+    up_coarse: np.ndarray
+    up_eps: np.ndarray
+    up_kids: np.ndarray
+    up_table: np.ndarray
+    trees: list  # the distinct PackedTrees, in table order
 
     def arrays(self):
         return {k: getattr(self, k) for k in (
-            "tris", "tri_orig", "body_state", "body_levels", "pair_body", "pair_problem",
-            "pair_group", "problem_dt", "problem_tbase")}
+            "tri_orig", "body_state", "body_levels", "pair_body", "pair_problem",
+            "pair_group", "problem_dt", "problem_tbase") + UPLOAD_KEYS}
 
     @property
     def nbytes(self) -> int:
         return sum(a.nbytes for a in self.arrays().values())
+
+    def records(self) -> np.ndarray:
+        """The (n_tris, 16) records the device rebuilds (host copy, for tests)."""
+        return np.concatenate([pt.records for pt in self.trees]) if self.trees else np.zeros((0, RECORD))
 
 
 def body_state_row(body) -> np.ndarray:
@@ -209,17 +259,25 @@ class Packer:
                                  np.asarray(pair_problem, dtype=np.int32),
                                  np.asarray(pair_group, dtype=np.int32))
             self._pair_key = skey
-        tris, orig, lev, max_children = self._static
-        state = _states(bodies, self.pinned)
-        ids = np.fromiter((body_id(b) for b in bodies), dtype=np.int64, count=len(bodies))
-        lev = lev.copy()
-        lev[:, 1] = ids
+        state = self._states(bodies)
         pb, pp, pg = self._pair_arrays
-        return HostScene(
-            tris=tris, tri_orig=orig, body_state=state, body_levels=lev,
-            pair_body=pb, pair_problem=pp, pair_group=pg,
-            problem_dt=dts, problem_tbase=tbs,
-            max_children=max_children, n_problems=len(dts), body_ids=ids)
+        return _scene(self._static, state, self._ids(bodies, skey), pb, pp, pg, dts, tbs)
+
+    def _ids(self, bodies, skey):
+        # body ids are fixed per body object; cached with the pair structure
+        if getattr(self, "_ids_key", None) is not skey:
+            self._ids_cache = np.fromiter((body_id(b) for b in bodies), dtype=np.int64, count=len(bodies))
+            self._ids_key = skey
+        return self._ids_cache
+
+    def _states(self, bodies):
+        # one pinned state buffer, re-used: every search call completes (its
+        # results are read back) before the next pack on this thread
+        buf = getattr(self, "_state_buf", None)
+        if buf is None or len(buf) != len(bodies):
+            buf = _pinned((len(bodies), 16), np.float64) if self.pinned else np.empty((len(bodies), 16))
+            self._state_buf = buf
+        return _states(bodies, out=buf)
 
 
     def pack_pairs(self, pairs, dts) -> HostScene:
@@ -251,23 +309,15 @@ class Packer:
             self._key = key
             self._trees = [b.tree for b in bodies]
         self._pair_arrays = (pb, pp, pg)
-        tris, orig, lev, max_children = self._static
-        state = _states(bodies, self.pinned)
-        ids = np.fromiter((body_id(b) for b in bodies), dtype=np.int64, count=len(bodies))
-        lev = lev.copy()
-        lev[:, 1] = ids
+        state = self._states(bodies)
         dts = np.array(np.broadcast_to(np.asarray(dts, dtype=np.float64), (len(pairs),)), copy=True)
-        return HostScene(
-            tris=tris, tri_orig=orig, body_state=state, body_levels=lev,
-            pair_body=pb, pair_problem=pp, pair_group=pg,
-            problem_dt=dts, problem_tbase=np.zeros(len(pairs)),
-            max_children=max_children, n_problems=len(pairs), body_ids=ids)
+        return _scene(self._static, state, self._ids(bodies, skey), pb, pp, pg, dts, np.zeros(len(pairs)))
 
 
-def _states(bodies, pinned):
+def _states(bodies, out):
     """Body snapshot rows (body_state_row for every body), vectorised."""
     n = len(bodies)
-    state = _pinned((n, 16), np.float64) if pinned else np.empty((n, 16))
+    state = out
     state.fill(0.0)
     dyn = [i for i, b in enumerate(bodies) if hasattr(b, "timeline")]
     if dyn:
@@ -318,8 +368,19 @@ def _tables(problems):
     return bodies, pair_body, pair_problem, pair_group, dts, tbs
 
 
-def _assemble_static(bodies, pinned):
-    """Concatenated tree records of the bodies' distinct trees + level table."""
+@dataclass
+class StaticBlock:
+    """The tree part of a scene: compact upload pools, tri_orig, level table."""
+    n_tris: int
+    orig: np.ndarray
+    lev: np.ndarray
+    max_children: int
+    pools: dict
+    trees: list
+
+
+def _assemble_static(bodies, pinned) -> StaticBlock:
+    """Upload image of the bodies' distinct trees + level table."""
     trees = {}
     order = []
     for b in bodies:
@@ -327,17 +388,36 @@ def _assemble_static(bodies, pinned):
         if k not in trees:
             trees[k] = pack_tree(b.tree)
             order.append(k)
+    pts = [trees[k] for k in order]
     tree_off = {}
     off = 0
     for k in order:
         tree_off[k] = off
         off += len(trees[k].records)
-    tris = _pinned((off, RECORD), np.float64) if pinned else np.empty((off, RECORD))
+    sizes = {"up_verts": (sum(len(p.verts) for p in pts), 3), "up_vidx": (sum(len(p.vidx) for p in pts), 3),
+             "up_coarse": (sum(len(p.coarse) for p in pts), 9), "up_eps": (sum(len(p.eps) for p in pts),),
+             "up_kids": (sum(len(p.kids) for p in pts), 2), "up_table": (len(pts), 8)}
+    dtypes = {"up_verts": np.float64, "up_vidx": np.int32, "up_coarse": np.float64, "up_eps": np.float64,
+              "up_kids": np.int32, "up_table": np.int64}
+    pools = {k: (_pinned(sizes[k], dtypes[k]) if pinned else np.empty(sizes[k], dtype=dtypes[k]))
+             for k in UPLOAD_KEYS}
     orig = _pinned((off,), np.int32) if pinned else np.empty(off, dtype=np.int32)
+    cur = dict.fromkeys(("v", "i", "c", "e"), 0)
     max_children = 1
-    for k in order:
+    for t, k in enumerate(order):
         pt = trees[k]
-        tris[tree_off[k]:tree_off[k] + len(pt.records)] = pt.records
+        n0 = int(pt.level_size[0])
+        nv, nc, ne = len(pt.verts), len(pt.coarse), len(pt.eps)
+        pools["up_table"][t] = (tree_off[k], n0, nc, cur["v"], cur["i"], cur["c"], cur["e"], pt.eps_mode)
+        pools["up_verts"][cur["v"]:cur["v"] + nv] = pt.verts
+        pools["up_vidx"][cur["i"]:cur["i"] + n0] = pt.vidx
+        pools["up_coarse"][cur["c"]:cur["c"] + nc] = pt.coarse
+        pools["up_kids"][cur["c"]:cur["c"] + nc] = pt.kids
+        pools["up_eps"][cur["e"]:cur["e"] + ne] = pt.eps
+        cur["v"] += nv
+        cur["i"] += n0
+        cur["c"] += nc
+        cur["e"] += ne
         orig[tree_off[k]:tree_off[k] + len(pt.records)] = pt.orig
         max_children = max(max_children, pt.max_children)
     lev = np.zeros((len(bodies), 18), dtype=np.int64)
@@ -347,7 +427,17 @@ def _assemble_static(bodies, pinned):
         lev[i, 0] = L
         lev[i, 2:2 + L] = tree_off[id(b.tree)] + pt.level_off
         lev[i, 10:10 + L] = pt.level_size
-    return tris, orig, lev, max_children
+    return StaticBlock(n_tris=off, orig=orig, lev=lev, max_children=max_children, pools=pools, trees=pts)
+
+
+def _scene(static: StaticBlock, state, ids, pair_body, pair_problem, pair_group, dts, tbs) -> HostScene:
+    lev = static.lev.copy()
+    lev[:, 1] = ids
+    return HostScene(
+        n_tris=static.n_tris, tri_orig=static.orig, body_state=state, body_levels=lev,
+        pair_body=pair_body, pair_problem=pair_problem, pair_group=pair_group,
+        problem_dt=dts, problem_tbase=tbs, max_children=static.max_children, n_problems=len(dts),
+        body_ids=ids, trees=static.trees, **static.pools)
 
 
 def pack(problems) -> HostScene:
@@ -384,43 +474,12 @@ def pack(problems) -> HostScene:
 
 
 def _assemble(bodies, pair_body, pair_problem, pair_group, dts, tbs) -> HostScene:
-    trees = {}
-    order = []
-    for b in bodies:
-        k = id(b.tree)
-        if k not in trees:
-            trees[k] = pack_tree(b.tree)
-            order.append(k)
-    tree_off = {}
-    off = 0
-    for k in order:
-        tree_off[k] = off
-        off += len(trees[k].records)
-    tris = np.empty((off, RECORD), dtype=np.float64)
-    orig = np.empty(off, dtype=np.int32)
-    max_children = 1
-    for k in order:
-        pt = trees[k]
-        tris[tree_off[k]:tree_off[k] + len(pt.records)] = pt.records
-        orig[tree_off[k]:tree_off[k] + len(pt.records)] = pt.orig
-        max_children = max(max_children, pt.max_children)
-    n_b = len(bodies)
-    state = np.empty((n_b, 16))
-    lev = np.zeros((n_b, 18), dtype=np.int64)
-    ids = np.empty(n_b, dtype=np.int64)
+    static = _assemble_static(bodies, pinned=False)
+    state = np.empty((len(bodies), 16))
     for i, b in enumerate(bodies):
-        pt = trees[id(b.tree)]
         state[i] = body_state_row(b)
-        L = len(pt.level_size)
-        lev[i, 0] = L
-        ids[i] = body_id(b)
-        lev[i, 1] = ids[i]
-        lev[i, 2:2 + L] = tree_off[id(b.tree)] + pt.level_off
-        lev[i, 10:10 + L] = pt.level_size
-    return HostScene(
-        tris=tris, tri_orig=orig, body_state=state, body_levels=lev,
-        pair_body=np.asarray(pair_body, dtype=np.int32).reshape(-1, 2),
-        pair_problem=np.asarray(pair_problem, dtype=np.int32),
-        pair_group=np.asarray(pair_group, dtype=np.int32),
-        problem_dt=np.asarray(dts, dtype=np.float64), problem_tbase=np.asarray(tbs, dtype=np.float64),
-        max_children=max_children, n_problems=len(dts), body_ids=ids)
+    ids = np.fromiter((body_id(b) for b in bodies), dtype=np.int64, count=len(bodies))
+    return _scene(static, state, ids,
+                  np.asarray(pair_body, dtype=np.int32).reshape(-1, 2),
+                  np.asarray(pair_problem, dtype=np.int32), np.asarray(pair_group, dtype=np.int32),
+                  np.asarray(dts, dtype=np.float64), np.asarray(tbs, dtype=np.float64))

@@ -42,6 +42,29 @@ def GK(G):
     return kernels
 
 
+# ---------------------------------------------------------------- compact tree upload
+
+def test_unpacked_records_match_host_build(G):
+    """ltsg_unpack_trees rebuilds the host's records: slots 0..11 bit for bit
+    (corners, epsilon, arm, children), the cull sphere conservatively."""
+    from paper_2309_15417_b200 import packing, scenes
+
+    sc = scenes.config3(n_rocks=40)
+    bodies = list(sc.particles.values())[:12]
+    sc1 = scenes.config1(n_pairs=3, subdiv=2)
+    bodies += list(sc1.particles.values())
+    hs = packing.pack([([(bodies[i], bodies[i + 1])], 0.0, 0.0) for i in range(0, len(bodies) - 1, 2)])
+    ds = G.DeviceScene(hs)
+    got = ds.t["tris"].cpu().numpy()[:hs.n_tris]
+    want = hs.records()
+    assert got[:, :12].view(np.uint64).tolist() == want[:, :12].view(np.uint64).tolist()
+    np.testing.assert_allclose(got[:, 12:15], want[:, 12:15], rtol=0, atol=1e-12)
+    sliver_g, sliver_w = got[:, 15] < 0, want[:, 15] < 0
+    assert (sliver_g == sliver_w).mean() > 0.999
+    ok = ~sliver_g & ~sliver_w
+    np.testing.assert_allclose(got[ok, 15], want[ok, 15], rtol=1e-12)
+
+
 # ---------------------------------------------------------------- row kernels
 
 def test_point_triangle_rows_bit_exact(GK):

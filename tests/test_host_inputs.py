@@ -71,7 +71,8 @@ def test_pack_groups_and_shared_bodies():
     s = B.StaticBody(-1, tree, 0.01)
     hs = packing.pack([([(a, b)], 0.0, 0.0), ([(b, c), (a, c), (c, s), (a, c)], 0.5, 1.0)])
     assert len(hs.body_state) == 4          # shared objects packed once
-    assert len(hs.tris) == sum(l.size for l in tree.levels)  # one tree copy
+    assert hs.n_tris == sum(l.size for l in tree.levels)  # one tree copy
+    assert len(hs.up_table) == 1
     assert hs.pair_problem.tolist() == [0, 1, 1, 1, 1]
     # groups rank the distinct (id_a, id_b) pairs of each problem
     assert hs.pair_group.tolist() == [0, 1, 0, 2, 0]
@@ -113,3 +114,44 @@ def test_batched_particles_match_single_builds():
                 assert len(a.children) == len(b.children)
                 for x, y in zip(a.children, b.children):
                     np.testing.assert_array_equal(x, y)
+
+
+def _expand_upload(hs):
+    """Host restatement of ltsg_unpack_trees for slots 0..11."""
+    out = np.zeros((hs.n_tris, 12))
+    for rec_off, n0, nc, vo, io, co, eo, mode in hs.up_table:
+        vidx = hs.up_vidx[io:io + n0]
+        out[rec_off:rec_off + n0, :9] = hs.up_verts[vo + vidx].reshape(n0, 9)
+        out[rec_off + n0:rec_off + n0 + nc, :9] = hs.up_coarse[co:co + nc]
+        if mode:
+            out[rec_off:rec_off + n0 + nc, 9] = hs.up_eps[eo:eo + n0 + nc]
+        else:
+            out[rec_off:rec_off + n0, 9] = hs.up_eps[eo]
+            out[rec_off + n0:rec_off + n0 + nc, 9] = hs.up_eps[eo + 1:eo + 1 + nc]
+        kids = np.zeros((n0 + nc, 2), dtype=np.int32)
+        kids[n0:] = hs.up_kids[co:co + nc]
+        out[rec_off:rec_off + n0 + nc, 11] = kids.view(np.float64).reshape(-1)
+    return out
+
+
+def test_compact_upload_image_rebuilds_records():
+    trees = [_tree_of(1), _tree_of(2)]
+    bodies = [B.Particle(i, t, 0.01, 1.0, B.timeline(B.state((2.0 * i, 0, 0)))) for i, t in enumerate(trees)]
+    hs = packing.pack([([(bodies[0], bodies[1])], 0.0, 0.0)])
+    rec = hs.records()
+    got = _expand_upload(hs)
+    keep = [k for k in range(12) if k != 10]  # slot 10 (arm) is derived on the device
+    assert got[:, keep].view(np.uint64).tolist() == rec[:, keep].view(np.uint64).tolist()
+    # the fine level is shared-vertex compressed
+    n0 = sum(int(pt.level_size[0]) for pt in hs.trees)
+    assert len(hs.up_verts) < 3 * n0 / 2
+    assert hs.nbytes < 0.6 * (rec.nbytes + hs.tri_orig.nbytes)
+
+
+def test_compact_upload_keeps_signed_zero_apart():
+    corners = np.array([[[0.0, 0.0, 0.0], [1.0, 0.0, 0.0], [0.0, 1.0, 0.0]],
+                        [[-0.0, 0.0, 0.0], [1.0, 0.0, 0.0], [0.0, 0.0, 1.0]]])
+    tree = build_surrogate_tree(corners, 0.01)
+    pt = packing._pack_tree(tree)
+    rebuilt = pt.verts[pt.vidx].reshape(-1, 9)
+    assert rebuilt.view(np.uint64).tolist() == pt.records[:2, :9].view(np.uint64).tolist()
