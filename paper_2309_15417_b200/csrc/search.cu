@@ -23,6 +23,7 @@
 
 #include <algorithm>
 #include <cstdlib>
+#include <ctime>
 #include <vector>
 
 namespace ltsg {
@@ -388,15 +389,15 @@ __device__ __forceinline__ double sphere_gap_at(const BodyInfo* bodies, const Pa
     double R[9], pos[3];
     pose_at(bodies[b], b, tau, w0, dt, n, i, pt, R, pos);
     const double x = __ldg(r + 12), y = __ldg(r + 13), z = __ldg(r + 14);
-    const double cx = R[0] * x + R[1] * y + R[2] * z + pos[0];
-    const double cy = R[3] * x + R[4] * y + R[5] * z + pos[1];
-    const double cz = R[6] * x + R[7] * y + R[8] * z + pos[2];
+    const double cx = fma(R[0], x, fma(R[1], y, fma(R[2], z, pos[0])));  // cull arithmetic: FMA is fine
+    const double cy = fma(R[3], x, fma(R[4], y, fma(R[5], z, pos[1])));
+    const double cz = fma(R[6], x, fma(R[7], y, fma(R[8], z, pos[2])));
     if (side) { bx = cx; by = cy; bz = cz; } else { ax = cx; ay = cy; az = cz; }
   }
   const double dx = ax - bx, dy = ay - by, dz = az - bz;
   const double rA = __ldg(ra + 15), rB = __ldg(rb + 15);
   *scale = 1.0 + fabs(ax) + fabs(ay) + fabs(az) + fabs(bx) + fabs(by) + fabs(bz) + rA + rB;
-  return sqrt(dx * dx + dy * dy + dz * dz) - (rA + rB);
+  return sqrt(fma(dx, dx, fma(dy, dy, dz * dz))) - (rA + rB);
 }
 
 // Exact 15-feature distance of one row, triangles posed at sample i.
@@ -423,6 +424,67 @@ __device__ __forceinline__ double row_distance_posed(const Staged<kStride>& st, 
     }
   }
   return __dsqrt_rn(staged_dist_sq_lite(st));
+}
+
+// Separating-axis cull of one moving row (same certificate as sat_cull on
+// static records): world corners at the row's pose (FMA arithmetic -- cull
+// data, not reference arithmetic), axes = both face normals and the
+// centroid direction, compared without normalising (gap > T |u|).
+__device__ __forceinline__ void world_corners_fast(const double R[9], const double pos[3], const double* r,
+                                                   double w[9]) {
+#pragma unroll
+  for (int k = 0; k < 3; ++k) {
+    const double x = __ldg(r + 3 * k), y = __ldg(r + 3 * k + 1), z = __ldg(r + 3 * k + 2);
+    w[3 * k] = fma(R[0], x, fma(R[1], y, fma(R[2], z, pos[0])));
+    w[3 * k + 1] = fma(R[3], x, fma(R[4], y, fma(R[5], z, pos[1])));
+    w[3 * k + 2] = fma(R[6], x, fma(R[7], y, fma(R[8], z, pos[2])));
+  }
+}
+
+__device__ __forceinline__ double axis_gap(double ux, double uy, double uz, const double a[9], const double b[9]) {
+  double alo = 0.0, ahi = 0.0, blo = 0.0, bhi = 0.0;
+#pragma unroll
+  for (int k = 0; k < 3; ++k) {
+    const double x = fma(ux, a[3 * k], fma(uy, a[3 * k + 1], uz * a[3 * k + 2]));
+    const double y = fma(ux, b[3 * k], fma(uy, b[3 * k + 1], uz * b[3 * k + 2]));
+    alo = k ? fmin(alo, x) : x;
+    ahi = k ? fmax(ahi, x) : x;
+    blo = k ? fmin(blo, y) : y;
+    bhi = k ? fmax(bhi, y) : y;
+  }
+  return fmax(blo - ahi, alo - bhi);
+}
+
+__device__ __forceinline__ bool sat_cull_posed(const BodyInfo* bodies, const PairInfo& p, const double* ra,
+                                               const double* rb, double tau, double w0, double dt, int n, int i,
+                                               const PoseTable& pt, double thr) {
+  if (__ldg(ra + 15) < 0.0 || __ldg(rb + 15) < 0.0) return false;  // slivers are never culled
+  double a[9], b[9];
+  {
+    double R[9], pos[3];
+    pose_at(bodies[p.ba], p.ba, tau, w0, dt, n, i, pt, R, pos);
+    world_corners_fast(R, pos, ra, a);
+    pose_at(bodies[p.bb], p.bb, tau, w0, dt, n, i, pt, R, pos);
+    world_corners_fast(R, pos, rb, b);
+  }
+  double scale = 1.0 + __ldg(ra + 15) + __ldg(rb + 15);
+#pragma unroll
+  for (int k = 0; k < 3; ++k) scale += fabs(a[k]) + fabs(b[k]);
+  const double T = thr + kCullMargin * scale;
+  auto normal_gap = [&](const double* x, const double* y) {  // x's face normal
+    const double e1x = x[3] - x[0], e1y = x[4] - x[1], e1z = x[5] - x[2];
+    const double e2x = x[6] - x[0], e2y = x[7] - x[1], e2z = x[8] - x[2];
+    const double nx = fma(e1y, e2z, -e1z * e2y), ny = fma(e1z, e2x, -e1x * e2z), nz = fma(e1x, e2y, -e1y * e2x);
+    const double len = sqrt(fma(nx, nx, fma(ny, ny, nz * nz)));
+    return axis_gap(nx, ny, nz, x, y) - T * len;
+  };
+  if (normal_gap(a, b) > 0.0) return true;
+  if (normal_gap(b, a) > 0.0) return true;
+  const double ux = (b[0] + b[3] + b[6]) - (a[0] + a[3] + a[6]);
+  const double uy = (b[1] + b[4] + b[7]) - (a[1] + a[4] + a[7]);
+  const double uz = (b[2] + b[5] + b[8]) - (a[2] + a[5] + a[8]);
+  const double len = sqrt(fma(ux, ux, fma(uy, uy, uz * uz)));
+  return axis_gap(ux, uy, uz, a, b) > T * len;
 }
 
 // Screen one frontier (one generation): every candidate is sampled over
@@ -549,6 +611,39 @@ k_screen(const Cand* __restrict__ front, int64_t n, const PairInfo* __restrict__
       const unsigned m = __ballot_sync(0xffffffffu, keep);
       if (keep) queue[nq + __popc(m & ((1u << lane) - 1u))] = (int16_t)r;
       nq += __popc(m);
+    }
+    __syncwarp();
+    // (b1) separating-axis cull of the sphere survivors, densely; survivors
+    // are compacted in place (a chunk is read before any lane writes)
+    {
+      int nq2 = 0;
+      for (int q0 = 0; q0 < nq; q0 += 32) {
+        const int q = q0 + lane;
+        bool keep = false;
+        int r = 0;
+        if (q < nq) {
+          r = queue[q];
+          int o = 0;
+#pragma unroll
+          for (int step = 16; step > 0; step >>= 1)
+            if (info[o + step].first <= r) o += step;
+          while (info[o].culled || info[o].count == 0) --o;
+          const CandInfo& c = info[o];
+          const int i = r - c.first;
+          const double tau = linspace_at(c.w0, c.dt, c.count, i);
+          const PairInfo p = pairs[c.pair];
+          const double* ra_ = rec(tris, bodies[p.ba], c.la, c.ia);
+          const double* rb_ = rec(tris, bodies[p.bb], c.lb, c.ib);
+          keep = !sat_cull_posed(bodies, p, ra_, rb_, tau, c.w0, c.dt, c.count, i, pt,
+                                 fmax(c.thr, add(c.h, kRestSlop)));
+          if (!keep) bits[r] = 0;
+        }
+        const unsigned m = __ballot_sync(0xffffffffu, keep);
+        __syncwarp();
+        if (keep) queue[nq2 + __popc(m & ((1u << lane) - 1u))] = (int16_t)r;
+        nq2 += __popc(m);
+      }
+      nq = nq2;
     }
     __syncwarp();
     // (b) exact 15-feature distance of the surviving rows, densely
@@ -1862,6 +1957,45 @@ struct Timer {
   }
 };
 
+// Optional phase trace (env LTSG_TRACE=1): device time and host wall time
+// between consecutive marks of one call, printed to stderr.  Diagnostic only.
+struct Trace {
+  bool on = false;
+  cudaStream_t st = nullptr;
+  std::vector<const char*> name;
+  std::vector<cudaEvent_t> ev;
+  std::vector<double> host_us;
+  explicit Trace(cudaStream_t s) : st(s) {
+    const char* e = getenv("LTSG_TRACE");
+    on = e && e[0] == '1';
+  }
+  static double now_us() {
+    timespec t;
+    clock_gettime(CLOCK_MONOTONIC, &t);
+    return 1e6 * (double)t.tv_sec + 1e-3 * (double)t.tv_nsec;
+  }
+  void mark(const char* n) {
+    if (!on) return;
+    cudaEvent_t e;
+    cudaEventCreate(&e);
+    cudaEventRecord(e, st);
+    name.push_back(n);
+    ev.push_back(e);
+    host_us.push_back(now_us());
+  }
+  ~Trace() {
+    if (!on || ev.empty()) return;
+    cudaEventSynchronize(ev.back());
+    fprintf(stderr, "[ltsg trace] %-14s %10s %10s\n", "phase", "device_ms", "host_ms");
+    for (size_t i = 1; i < ev.size(); ++i) {
+      float m = 0.f;
+      cudaEventElapsedTime(&m, ev[i - 1], ev[i]);
+      fprintf(stderr, "[ltsg trace] %-14s %10.3f %10.3f\n", name[i], m, 1e-3 * (host_us[i] - host_us[i - 1]));
+    }
+    for (auto e : ev) cudaEventDestroy(e);
+  }
+};
+
 #define LTSG_LAUNCHED() \
   do {                  \
     LTSG_CHECK_LAUNCH(); \
@@ -1881,9 +2015,12 @@ static int run_search(const ltsg_scene* sc, ltsg_result* out, ltsg_workspace* ws
   out->rows_screen_exact = 0;
   if (np == 0) return LTSG_OK;
 
+  Trace tr(st);
+  tr.mark("start");
   Prepared pr{};
   LTSG_TRY(prepare(sc, ws, st, &pr));
   out->launches += 2;
+  tr.mark("prepare");
   Timer t_screen, t_refine, t_contacts;
   Counters* d_ctr;
   LTSG_TRY(ws_get(ws, "ctr", 1, &d_ctr));
@@ -1925,6 +2062,7 @@ static int run_search(const ltsg_scene* sc, ltsg_result* out, ltsg_workspace* ws
     }
   }
 
+  tr.mark("world");
   // ---- pose tables for moving batches
   PoseTable poses{nullptr, nullptr};
   if (!all_static && sc->n_pairs > 0 && sc->n_bodies > 0 && !getenv("LTSG_NO_POSES")) {
@@ -1960,6 +2098,7 @@ static int run_search(const ltsg_scene* sc, ltsg_result* out, ltsg_workspace* ws
     LTSG_CUDA(cudaMemcpyAsync(&seed_total, seed_off + sc->n_pairs, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
     LTSG_CUDA(cudaStreamSynchronize(st));
   }
+  tr.mark("poses+seedcnt");
   constexpr int kMaxGen = 2 * kMaxLevels;
   unsigned long long *gen_cnt, *x_cnt;
   LTSG_TRY(ws_get(ws, "gen_cnt", kMaxGen + 1, &gen_cnt));
@@ -2137,6 +2276,7 @@ static int run_search(const ltsg_scene* sc, ltsg_result* out, ltsg_workspace* ws
   ws->hint_entries = std::max(ws->hint_entries, (size_t)h.entries);
   ws->hint_cross = std::max(ws->hint_cross, (size_t)h.cross);
 
+  tr.mark("traverse");
   // ---- certified zoom + bisection
   t_refine.start(st);
   const int64_t n_entries = (int64_t)h.entries;
@@ -2169,6 +2309,7 @@ static int run_search(const ltsg_scene* sc, ltsg_result* out, ltsg_workspace* ws
   }
   const int64_t n_cross = (int64_t)h.cross + n_br;
   t_refine.stop(st);
+  tr.mark("refine");
   t_contacts.start(st);
   k_finalize<<<grid_for(np, 128), 128, 0, st>>>(tau_min, sc->problem_dt, np, sc->widen, out->dt,
                                                 out->first_contact, out->collision);
@@ -2185,6 +2326,7 @@ static int run_search(const ltsg_scene* sc, ltsg_result* out, ltsg_workspace* ws
     LTSG_LAUNCHED();
   }
   LTSG_TRY(read_ctr(d_ctr, &h, st));
+  tr.mark("collect");
   const int64_t n_rec = (int64_t)h.records;
   out->rows_screen = (int64_t)h.rows;
   out->rows_zoom = (int64_t)h.zoom_rows;
@@ -2230,8 +2372,9 @@ static int run_search(const ltsg_scene* sc, ltsg_result* out, ltsg_workspace* ws
   k_contacts<<<grid_for(n_rec, 64), 64, 0, st>>>(recs, n_rec, pr.pairs, pr.bodies, sc->tris, sc->tri_orig,
                                                  sc->problem_tbase, ro, key);
   LTSG_LAUNCHED();
-
+  tr.mark("contacts");
   LTSG_TRY(fuse_stage(ws, st, ro, key, n_rec, np, prob_count, prob_count64, out));
+  tr.mark("fuse");
   t_contacts.stop(st);
   out->ms_refine = t_refine.ms();
   out->ms_contacts = t_contacts.ms();

@@ -25,6 +25,8 @@ from __future__ import annotations
 
 import threading
 import weakref
+from itertools import chain
+from operator import is_not
 from dataclasses import dataclass
 
 import numpy as np
@@ -264,28 +266,38 @@ class Packer:
         return _scene(self._static, state, self._ids(bodies, skey), pb, pp, pg, dts, tbs)
 
     def _ids(self, bodies, skey):
-        # body ids are fixed per body object; cached with the pair structure
-        if getattr(self, "_ids_key", None) is not skey:
+        # body ids and kinds are fixed per body object: cached with the
+        # structure (keyed on the body list object, rebuilt with it)
+        if getattr(self, "_ids_for", None) is not bodies:
             self._ids_cache = np.fromiter((body_id(b) for b in bodies), dtype=np.int64, count=len(bodies))
-            self._ids_key = skey
+            self._dyn_cache = np.flatnonzero(np.fromiter((hasattr(b, "timeline") for b in bodies), dtype=bool,
+                                                         count=len(bodies)))
+            self._ids_for = bodies
         return self._ids_cache
 
     def _states(self, bodies):
         # one pinned state buffer, re-used: every search call completes (its
-        # results are read back) before the next pack on this thread
+        # results are read back) before the next pack on this thread, so a
+        # HostScene from a Packer is valid until the Packer's next pack call
         buf = getattr(self, "_state_buf", None)
         if buf is None or len(buf) != len(bodies):
             buf = _pinned((len(bodies), 16), np.float64) if self.pinned else np.empty((len(bodies), 16))
             self._state_buf = buf
-        return _states(bodies, out=buf)
+        self._ids(bodies, None)
+        return _states(bodies, out=buf, dyn=self._dyn_cache)
 
 
     def pack_pairs(self, pairs, dts) -> HostScene:
         """Fast path for pair-mode batches (one body pair per problem, as
         `pair_earliest_contact`): no per-problem Python tuples, one fusion
         group per problem, t_base 0."""
-        skey = ("pairs", tuple(map(id, (x for ab in pairs for x in ab))))
-        if skey != getattr(self, "_skey", None):
+        flat = list(chain.from_iterable(pairs))
+        prev = getattr(self, "_flat", None)
+        same = (prev is not None and len(prev) == len(flat) and getattr(self, "_skey", None) == "pairs"
+                and not any(map(is_not, flat, prev)))
+        skey = "pairs"
+        if not same:
+            self._flat = flat
             slot_of = {}
             bodies = []
             pb = np.empty((len(pairs), 2), dtype=np.int32)
@@ -314,18 +326,21 @@ class Packer:
         return _scene(self._static, state, self._ids(bodies, skey), pb, pp, pg, dts, np.zeros(len(pairs)))
 
 
-def _states(bodies, out):
-    """Body snapshot rows (body_state_row for every body), vectorised."""
+def _states(bodies, out, dyn=None):
+    """Body snapshot rows (body_state_row for every body), vectorised.
+    `dyn`: indices of the dynamic bodies (computed when not given)."""
     n = len(bodies)
     state = out
     state.fill(0.0)
-    dyn = [i for i, b in enumerate(bodies) if hasattr(b, "timeline")]
-    if dyn:
-        cur = [bodies[i].timeline.current for i in dyn]
-        state[dyn, 0:3] = np.array([c.position for c in cur], dtype=np.float64)
-        state[dyn, 3:6] = np.array([c.velocity for c in cur], dtype=np.float64)
-        state[dyn, 6:10] = np.array([c.rotation for c in cur], dtype=np.float64)
-        state[dyn, 10:13] = np.array([c.angular_velocity for c in cur], dtype=np.float64)
+    if dyn is None:
+        dyn = np.flatnonzero(np.fromiter((hasattr(b, "timeline") for b in bodies), dtype=bool, count=n))
+    if len(dyn):
+        sel = slice(None) if len(dyn) == n else dyn
+        cur = [b.timeline.current for b in bodies] if len(dyn) == n else [bodies[i].timeline.current for i in dyn]
+        state[sel, 0:3] = np.array([c.position for c in cur], dtype=np.float64)
+        state[sel, 3:6] = np.array([c.velocity for c in cur], dtype=np.float64)
+        state[sel, 6:10] = np.array([c.rotation for c in cur], dtype=np.float64)
+        state[sel, 10:13] = np.array([c.angular_velocity for c in cur], dtype=np.float64)
     if len(dyn) < n:
         stat = np.ones(n, dtype=bool)
         stat[dyn] = False
