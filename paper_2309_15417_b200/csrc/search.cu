@@ -249,9 +249,14 @@ __device__ __forceinline__ double row_distance_lite(const Staged<kStride>& st, c
 
 // ---------------------------------------------------------------- screen
 
+// Per-candidate data the lanes evaluating its rows need (shared memory):
+// everything a row needs is one shared-memory read away, no dependent
+// global loads (pair -> body -> level table -> record).
 struct CandInfo {
-  double w0, dt, h, speed, thr, cull_lo, cull_hi;
-  int32_t pair, ia, ib, la, lb, count, first, culled;
+  double w0, dt, h, thr, cull_lo, cull_hi;
+  int64_t off_a, off_b;  // record indices of the two triangles (tris + off * kRecord)
+  int32_t ba, bb, count, first, culled;
+  int32_t tab;  // bit 0 / bit 1: the pose table covers side a / b (w0 == 0 and the body's table dt == dt)
 };
 
 struct ChildInfo {
@@ -355,9 +360,9 @@ __global__ void k_pose_fill(const BodyInfo* __restrict__ bodies, int n_bodies, c
 }
 
 // Pose of body slot `b` at sample i of linspace(w0, dt, n) (= tau).
-__device__ __forceinline__ void pose_at(const BodyInfo& B, int b, double tau, double w0, double dt, int n, int i,
+__device__ __forceinline__ void pose_at(const BodyInfo& B, int b, double tau, bool use_tab, int n, int i,
                                         const PoseTable& pt, double R[9], double pos[3]) {
-  if (pt.tab != nullptr && w0 == 0.0 && pt.tdt[b] == dt) {
+  if (use_tab) {
     const double2* e = reinterpret_cast<const double2*>(pt.tab + ((size_t)b * kPoseEntries + grid_entry(n, i)) * kPose);
     double v[12];
 #pragma unroll
@@ -378,16 +383,16 @@ __device__ __forceinline__ void pose_at(const BodyInfo& B, int b, double tau, do
 
 // Bounding-sphere gap (centre distance minus radii, approximate arithmetic;
 // the cull margins cover it) of the candidate's two triangles at sample i.
-__device__ __forceinline__ double sphere_gap_at(const BodyInfo* bodies, const PairInfo& p, const double* ra,
-                                                const double* rb, double tau, double w0, double dt, int n, int i,
+__device__ __forceinline__ double sphere_gap_at(const BodyInfo* bodies, int ba, int bb, const double* ra,
+                                                const double* rb, double tau, int tab, int n, int i,
                                                 const PoseTable& pt, double* scale) {
   double ax = 0.0, ay = 0.0, az = 0.0, bx = 0.0, by = 0.0, bz = 0.0;
 #pragma unroll 1
   for (int side = 0; side < 2; ++side) {
-    const int b = side ? p.bb : p.ba;
+    const int b = side ? bb : ba;
     const double* r = side ? rb : ra;
     double R[9], pos[3];
-    pose_at(bodies[b], b, tau, w0, dt, n, i, pt, R, pos);
+    pose_at(bodies[b], b, tau, (tab >> side) & 1, n, i, pt, R, pos);
     const double x = __ldg(r + 12), y = __ldg(r + 13), z = __ldg(r + 14);
     const double cx = fma(R[0], x, fma(R[1], y, fma(R[2], z, pos[0])));  // cull arithmetic: FMA is fine
     const double cy = fma(R[3], x, fma(R[4], y, fma(R[5], z, pos[1])));
@@ -402,17 +407,16 @@ __device__ __forceinline__ double sphere_gap_at(const BodyInfo* bodies, const Pa
 
 // Exact 15-feature distance of one row, triangles posed at sample i.
 template <int kStride>
-__device__ __forceinline__ double row_distance_posed(const Staged<kStride>& st, const double* tris,
-                                                     const BodyInfo* bodies, const PairInfo& p, int la, int ia,
-                                                     int lb, int ib, double tau, double w0, double dt, int n,
-                                                     int i, const PoseTable& pt) {
+__device__ __forceinline__ double row_distance_posed(const Staged<kStride>& st, const BodyInfo* bodies, int ba,
+                                                     int bb, const double* ra, const double* rb, double tau,
+                                                     int tab, int n, int i, const PoseTable& pt) {
 #pragma unroll 1
   for (int side = 0; side < 2; ++side) {
-    const int b = side ? p.bb : p.ba;
+    const int b = side ? bb : ba;
     const BodyInfo& B = bodies[b];
     double R[9], pos[3], L[9];
-    pose_at(B, b, tau, w0, dt, n, i, pt, R, pos);
-    load_local(rec(tris, B, side ? lb : la, side ? ib : ia), L);
+    pose_at(B, b, tau, (tab >> side) & 1, n, i, pt, R, pos);
+    load_local(side ? rb : ra, L);
     const Tri t = world_tri(R, pos, L);
     const int base = side ? kLiteB : kLiteA;
 #pragma unroll
@@ -455,16 +459,16 @@ __device__ __forceinline__ double axis_gap(double ux, double uy, double uz, cons
   return fmax(blo - ahi, alo - bhi);
 }
 
-__device__ __forceinline__ bool sat_cull_posed(const BodyInfo* bodies, const PairInfo& p, const double* ra,
-                                               const double* rb, double tau, double w0, double dt, int n, int i,
+__device__ __forceinline__ bool sat_cull_posed(const BodyInfo* bodies, int ba, int bb, const double* ra,
+                                               const double* rb, double tau, int tab, int n, int i,
                                                const PoseTable& pt, double thr) {
   if (__ldg(ra + 15) < 0.0 || __ldg(rb + 15) < 0.0) return false;  // slivers are never culled
   double a[9], b[9];
   {
     double R[9], pos[3];
-    pose_at(bodies[p.ba], p.ba, tau, w0, dt, n, i, pt, R, pos);
+    pose_at(bodies[ba], ba, tau, tab & 1, n, i, pt, R, pos);
     world_corners_fast(R, pos, ra, a);
-    pose_at(bodies[p.bb], p.bb, tau, w0, dt, n, i, pt, R, pos);
+    pose_at(bodies[bb], bb, tau, (tab >> 1) & 1, n, i, pt, R, pos);
     world_corners_fast(R, pos, rb, b);
   }
   double scale = 1.0 + __ldg(ra + 15) + __ldg(rb + 15);
@@ -510,25 +514,35 @@ k_screen(const Cand* __restrict__ front, int64_t n, const PairInfo* __restrict__
   ChildInfo* kid = s_u[warp].child;
   uint8_t* bits = s_bits[warp];
   int16_t* queue = s_queue[warp];
+  unsigned long long acc_rows = 0, acc_exact = 0;
 
   for (int64_t wi = blockIdx.x * (int64_t)kScreenWarps + warp; wi < n_warps;
        wi += (int64_t)gridDim.x * kScreenWarps) {
     const int64_t ci = wi * 32 + lane;
     const bool valid = ci < n;
     CandInfo me{};
+    Cand own{};        // the candidate itself (this lane's, for the decisions)
+    double speed = 0;  // its Lipschitz speed (entries carry it)
     if (valid) {
       const Cand c = front[ci];
+      own = c;
       const PairInfo p = pairs[c.pair];
       const BodyInfo& A = bodies[p.ba];
       const BodyInfo& B = bodies[p.bb];
-      const double* ra_ = rec(tris, A, c.la, c.ia);
-      const double* rb_ = rec(tris, B, c.lb, c.ib);
+      me.ba = p.ba;
+      me.bb = p.bb;
+      me.off_a = A.level_off[c.la] + c.ia;
+      me.off_b = B.level_off[c.lb] + c.ib;
+      const double* ra_ = tris + me.off_a * kRecord;
+      const double* rb_ = tris + me.off_b * kRecord;
       me.h = add(__ldg(ra_ + 9), __ldg(rb_ + 9));  // ccd.py:339
       double sp = p.speed0;                        // ccd.py:340-345
       if (A.m.omega > 0.0) sp = add(sp, mul(A.m.omega, __ldg(ra_ + 10)));
       if (B.m.omega > 0.0) sp = add(sp, mul(B.m.omega, __ldg(rb_ + 10)));
-      me.speed = sp;
+      speed = sp;
       me.w0 = c.w0;
+      me.tab = (pt.tab != nullptr && c.w0 == 0.0)
+          ? ((pt.tdt[p.ba] == p.dt ? 1 : 0) | (pt.tdt[p.bb] == p.dt ? 2 : 0)) : 0;
       me.dt = p.dt;
       const double span = fmax(sub(p.dt, c.w0), 0.0);
       me.count = sample_count(span, sp, me.h);
@@ -547,11 +561,12 @@ k_screen(const Cand* __restrict__ front, int64_t n, const PairInfo* __restrict__
         const double T = fmax(me.thr, add(me.h, kRestSlop));
         double sc0 = 0.0, sc1 = 0.0;
         // (the gap call sets the scale: evaluate it before reading sc0/sc1)
-        const double gap0 = sphere_gap_at(bodies, p, ra_, rb_, c.w0, c.w0, p.dt, me.count, 0, pt, &sc0);
+        const double gap0 = sphere_gap_at(bodies, p.ba, p.bb, ra_, rb_, c.w0, me.tab, me.count, 0, pt, &sc0);
         const double g0 = gap0 - (T + kCullMargin * sc0);
         double g1 = g0;
         if (p.dt > c.w0) {
-          const double gap1 = sphere_gap_at(bodies, p, ra_, rb_, p.dt, c.w0, p.dt, me.count, me.count - 1, pt, &sc1);
+          const double gap1 = sphere_gap_at(bodies, p.ba, p.bb, ra_, rb_, p.dt, me.tab, me.count, me.count - 1, pt,
+                                            &sc1);
           g1 = gap1 - (T + kCullMargin * sc1);
         }
         if (sp > 0.0) {
@@ -563,11 +578,6 @@ k_screen(const Cand* __restrict__ front, int64_t n, const PairInfo* __restrict__
         // every sample cleared?
         me.culled = me.cull_lo > p.dt || me.cull_hi < c.w0 || me.cull_lo > me.cull_hi;
       }
-      me.pair = c.pair;
-      me.ia = c.ia;
-      me.ib = c.ib;
-      me.la = c.la;
-      me.lb = c.lb;
     }
     // rows of culled candidates are decided (all flags false) without being evaluated
     const int nrows = me.culled ? 0 : me.count;
@@ -597,13 +607,12 @@ k_screen(const Cand* __restrict__ front, int64_t n, const PairInfo* __restrict__
         const CandInfo& c = info[o];
         const int i = r - c.first;
         const double tau = linspace_at(c.w0, c.dt, c.count, i);
-        const PairInfo p = pairs[c.pair];
-        const double* ra_ = rec(tris, bodies[p.ba], c.la, c.ia);
-        const double* rb_ = rec(tris, bodies[p.bb], c.lb, c.ib);
+        const double* ra_ = tris + c.off_a * kRecord;
+        const double* rb_ = tris + c.off_b * kRecord;
         keep = !(tau < c.cull_lo || tau > c.cull_hi);
         if (keep && __ldg(ra_ + 15) >= 0.0 && __ldg(rb_ + 15) >= 0.0) {
           double scale;
-          const double gap = sphere_gap_at(bodies, p, ra_, rb_, tau, c.w0, c.dt, c.count, i, pt, &scale);
+          const double gap = sphere_gap_at(bodies, c.ba, c.bb, ra_, rb_, tau, c.tab, c.count, i, pt, &scale);
           keep = !(gap > fmax(c.thr, add(c.h, kRestSlop)) + kCullMargin * scale);
         }
         if (!keep) bits[r] = 0;
@@ -631,11 +640,8 @@ k_screen(const Cand* __restrict__ front, int64_t n, const PairInfo* __restrict__
           const CandInfo& c = info[o];
           const int i = r - c.first;
           const double tau = linspace_at(c.w0, c.dt, c.count, i);
-          const PairInfo p = pairs[c.pair];
-          const double* ra_ = rec(tris, bodies[p.ba], c.la, c.ia);
-          const double* rb_ = rec(tris, bodies[p.bb], c.lb, c.ib);
-          keep = !sat_cull_posed(bodies, p, ra_, rb_, tau, c.w0, c.dt, c.count, i, pt,
-                                 fmax(c.thr, add(c.h, kRestSlop)));
+          keep = !sat_cull_posed(bodies, c.ba, c.bb, tris + c.off_a * kRecord, tris + c.off_b * kRecord, tau, c.tab,
+                                 c.count, i, pt, fmax(c.thr, add(c.h, kRestSlop)));
           if (!keep) bits[r] = 0;
         }
         const unsigned m = __ballot_sync(0xffffffffu, keep);
@@ -657,8 +663,8 @@ k_screen(const Cand* __restrict__ front, int64_t n, const PairInfo* __restrict__
       const CandInfo& c = info[o];
       const int i = r - c.first;
       const double tau = linspace_at(c.w0, c.dt, c.count, i);
-      const PairInfo p = pairs[c.pair];
-      const double d = row_distance_posed(st, tris, bodies, p, c.la, c.ia, c.lb, c.ib, tau, c.w0, c.dt, c.count, i, pt);
+      const double d = row_distance_posed(st, bodies, c.ba, c.bb, tris + c.off_a * kRecord, tris + c.off_b * kRecord,
+                                          tau, c.tab, c.count, i, pt);
       uint8_t b = 0;
       if (d <= c.thr) b |= 1;                  // screen flag
       if (d <= c.h) b |= 2;                    // at or below touching distance
@@ -671,35 +677,34 @@ k_screen(const Cand* __restrict__ front, int64_t n, const PairInfo* __restrict__
     ChildInfo ch{};
     if (valid && !me.culled) {
       const uint8_t* cb = bits + me.first;
-      const bool fine = me.la == 0 && me.lb == 0;
+      const bool fine = own.la == 0 && own.lb == 0;
       if (fine && me.w0 == 0.0 && (cb[0] & 4)) {
         const unsigned long long slot = atomicAdd(&out.ctr->resting, 1ULL);
-        if (slot < out.rest_cap) out.resting[slot] = RestRec{me.pair, me.ia, me.ib, 0, me.h};
+        if (slot < out.rest_cap) out.resting[slot] = RestRec{own.pair, own.ia, own.ib, 0, me.h};
       } else {
         int k0 = -1;
         for (int k = 0; k < me.count; ++k)
           if (cb[k] & 1) { k0 = k; break; }
         if (k0 >= 0 && !fine) {  // ccd.py:414-428
-          const PairInfo p = pairs[me.pair];
           ch.w0 = linspace_at(me.w0, me.dt, me.count, k0 > 0 ? k0 - 1 : 0);
-          ch.pair = me.pair;
+          ch.pair = own.pair;
           int na = 1, nb = 1;
-          ch.ia0 = me.ia;
-          ch.ib0 = me.ib;
-          if (me.la > 0) {
-            const int2 cr = *reinterpret_cast<const int2*>(rec(tris, bodies[p.ba], me.la, me.ia) + 11);
+          ch.ia0 = own.ia;
+          ch.ib0 = own.ib;
+          if (own.la > 0) {
+            const int2 cr = *reinterpret_cast<const int2*>(tris + me.off_a * kRecord + 11);
             ch.ia0 = cr.x;
             na = cr.y;
           }
-          if (me.lb > 0) {
-            const int2 cr = *reinterpret_cast<const int2*>(rec(tris, bodies[p.bb], me.lb, me.ib) + 11);
+          if (own.lb > 0) {
+            const int2 cr = *reinterpret_cast<const int2*>(tris + me.off_b * kRecord + 11);
             ch.ib0 = cr.x;
             nb = cr.y;
           }
           ch.nb = nb;
           ch.count = na * nb;
-          ch.la = me.la > 0 ? me.la - 1 : 0;
-          ch.lb = me.lb > 0 ? me.lb - 1 : 0;
+          ch.la = own.la > 0 ? own.la - 1 : 0;
+          ch.lb = own.lb > 0 ? own.lb - 1 : 0;
         } else if (k0 >= 0) {  // fine: flagged runs (ccd.py:429-446)
           int k = k0;
           while (k < me.count) {
@@ -711,14 +716,14 @@ k_screen(const Cand* __restrict__ front, int64_t n, const PairInfo* __restrict__
             if (cb[lo_i] & 2) {
               const unsigned long long slot = atomicAdd(&out.ctr->cross, 1ULL);
               if (slot < out.cross_cap)
-                out.cross[slot] = Cross{me.pair, me.ia, me.ib, 0,
+                out.cross[slot] = Cross{own.pair, own.ia, own.ib, 0,
                                         linspace_at(me.w0, me.dt, me.count, lo_i), me.h};
             } else if (hi_i > lo_i) {
               const unsigned long long slot = atomicAdd(&out.ctr->entries, 1ULL);
               if (slot < out.entry_cap)
-                out.entries[slot] = Entry{me.pair, me.ia, me.ib, 0,
+                out.entries[slot] = Entry{own.pair, own.ia, own.ib, 0,
                                           linspace_at(me.w0, me.dt, me.count, lo_i),
-                                          linspace_at(me.w0, me.dt, me.count, hi_i), me.h, me.speed};
+                                          linspace_at(me.w0, me.dt, me.count, hi_i), me.h, speed};
             }
             k = ke + 1;
           }
@@ -729,11 +734,9 @@ k_screen(const Cand* __restrict__ front, int64_t n, const PairInfo* __restrict__
     const int cincl = warp_incl_scan(ch.count, lane);
     const int ctotal = __shfl_sync(0xffffffffu, cincl, 31);
     unsigned long long cbase = 0;
-    if (lane == 0) {
-      atomicAdd(&out.ctr->rows, (unsigned long long)all_rows);
-      atomicAdd(&out.ctr->screen_exact, (unsigned long long)nq);
-      if (ctotal) cbase = atomicAdd(out.n_out, (unsigned long long)ctotal);
-    }
+    acc_rows += (unsigned long long)all_rows;  // warp-uniform; flushed once per warp
+    acc_exact += (unsigned long long)nq;
+    if (lane == 0 && ctotal) cbase = atomicAdd(out.n_out, (unsigned long long)ctotal);
     cbase = __shfl_sync(0xffffffffu, cbase, 0);
     if (ctotal) {
       ch.first = cincl - ch.count;
@@ -761,6 +764,10 @@ k_screen(const Cand* __restrict__ front, int64_t n, const PairInfo* __restrict__
       }
     }
     __syncwarp();
+  }
+  if (lane == 0) {
+    if (acc_rows) atomicAdd(&out.ctr->rows, acc_rows);
+    if (acc_exact) atomicAdd(&out.ctr->screen_exact, acc_exact);
   }
 }
 
