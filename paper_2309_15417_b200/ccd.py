@@ -201,17 +201,30 @@ class DeviceResult:
         return res
 
     def to_host(self, st: _lib.Result) -> BatchResult:
+        """All outputs in one pass: async copies into pinned host tensors
+        (torch's caching host allocator), one stream synchronisation."""
+        import torch
+
         n = self.n_problems
         nf, nr = int(st.n_fused), int(st.n_raw)
-        fused = {k: v[:nf].cpu().numpy() for k, v in self.f.items()}
-        raw = {k: v[:nr].cpu().numpy() for k, v in self.r.items()} if self.r else None
+        stream = torch.cuda.current_stream(self.dt.device)
+
+        def d2h(v):
+            h = torch.empty(v.shape, dtype=v.dtype, pin_memory=True)
+            h.copy_(v, non_blocking=True)
+            return h
+
+        fused = {k: d2h(v[:nf]) for k, v in self.f.items()}
+        raw = {k: d2h(v[:nr]) for k, v in self.r.items()} if self.r else None
+        dt, coll, first, off = d2h(self.dt[:n]), d2h(self.coll[:n]), d2h(self.first[:n]), d2h(self.off)
+        stream.synchronize()
         stats = {k: int(getattr(st, k)) for k in (
             "rows_screen", "rows_zoom", "rows_bisect", "rows_executed", "candidates",
             "generations", "n_raw", "n_fused", "launches", "rows_screen_exact")}
         stats.update({k: float(getattr(st, k)) for k in ("ms_screen", "ms_refine", "ms_contacts")})
-        return BatchResult(dt=self.dt[:n].cpu().numpy(), collision=self.coll[:n].cpu().numpy() != 0,
-                           first_contact=self.first[:n].cpu().numpy(),
-                           fused_offset=self.off.cpu().numpy(), contacts=fused, raw=raw, stats=stats)
+        return BatchResult(dt=dt.numpy(), collision=coll.numpy() != 0, first_contact=first.numpy(),
+                           fused_offset=off.numpy(), contacts={k: v.numpy() for k, v in fused.items()},
+                           raw={k: v.numpy() for k, v in raw.items()} if raw is not None else None, stats=stats)
 
 
 _capacity_hint = [1 << 12]

@@ -31,6 +31,7 @@ namespace ltsg {
 constexpr int kMaxLevels = 8;
 constexpr int kRecord = 16;  // doubles per triangle record
 constexpr int kWorld = 20;   // doubles per tau = 0 world record
+constexpr int kSph = 4;      // doubles per compact cull sphere (after the world records)
 // Relative slack of the certified culls: rows within this (times the
 // coordinate scale) of a threshold are always evaluated exactly.
 constexpr double kCullMargin = 1e-7;
@@ -796,78 +797,108 @@ __global__ void k_world_count(const BodyInfo* __restrict__ bodies, int n, int64_
 
 __global__ void __launch_bounds__(128) k_world_fill(const BodyInfo* __restrict__ bodies, int n,
                                                     const int64_t* __restrict__ woff,
-                                                    const double* __restrict__ tris, double* __restrict__ world) {
-  // 128 records per block iteration, moved through shared memory so that both
-  // the record loads and the world-record stores are fully coalesced.
+                                                    const double* __restrict__ tris, double* __restrict__ world,
+                                                    double* __restrict__ wsph) {
+  // Chunks of 128 consecutive world records (any body boundaries inside),
+  // moved through shared memory so that both the record loads and the
+  // world-record stores are coalesced.  Grid-stride over all chunks keeps
+  // every SM busy whatever the body sizes.
   __shared__ double s_rec[128 * kRecord];
   __shared__ double s_out[128 * kWorld];
-  for (int b = blockIdx.x; b < n; b += gridDim.x) {
-    const BodyInfo& B = bodies[b];
-    const int64_t cnt = woff[b + 1] - woff[b];
-    double pos[3];
-    position_at(B.m, 0.0, pos);
-    for (int64_t j0 = 0; j0 < cnt; j0 += 128) {
-      const int m = (int)min((int64_t)128, cnt - j0);
-      const double2* src = reinterpret_cast<const double2*>(tris + (size_t)(B.level_off[0] + j0) * kRecord);
-      double2* sm2 = reinterpret_cast<double2*>(s_rec);
-      for (int k = threadIdx.x; k < m * kRecord / 2; k += blockDim.x) sm2[k] = __ldg(src + k);
-      __syncthreads();
-      if (threadIdx.x < m) {
-        const int64_t j = j0 + threadIdx.x;
-        double* r = s_rec + threadIdx.x * kRecord;
-        double L[9];
-#pragma unroll
-        for (int k = 0; k < 9; ++k) L[k] = r[k];
-        const Tri t = world_tri(B.m.base, pos, L);
-        double* w = s_out + threadIdx.x * kWorld;
-        w[9] = r[9];
-        w[10] = r[10];
-#pragma unroll
-        for (int k = 0; k < 3; ++k) {
-          w[3 * k] = t.v[k].x;
-          w[3 * k + 1] = t.v[k].y;
-          w[3 * k + 2] = t.v[k].z;
-        }
-        {  // first child as an absolute world index (children are contiguous)
-          int lvl = 0;
-          while (lvl + 1 < B.n_levels && B.level_off[0] + j >= B.level_off[lvl + 1]) ++lvl;
-          int2 ch = *reinterpret_cast<const int2*>(r + 11);
-          if (lvl > 0) ch.x = (int32_t)(woff[b] + B.level_off[lvl - 1] - B.level_off[0] + ch.x);
-          *reinterpret_cast<int2*>(w + 11) = ch;
-        }
-        // bounding sphere in world coordinates (approximate; the cull margin absorbs it)
-        const double rad = r[15];
-        constexpr double kThird = 1.0 / 3.0;
-        const V3 c{(t.v[0].x + t.v[1].x + t.v[2].x) * kThird, (t.v[0].y + t.v[1].y + t.v[2].y) * kThird,
-                   (t.v[0].z + t.v[1].z + t.v[2].z) * kThird};
-        double r2 = 0.0;
-#pragma unroll
-        for (int k = 0; k < 3; ++k) {
-          const V3 d = t.v[k] - c;
-          r2 = fmax(r2, d.x * d.x + d.y * d.y + d.z * d.z);
-        }
-        // unit face normal and plane offset for the separating-axis cull
-        const V3 e1{t.v[1].x - t.v[0].x, t.v[1].y - t.v[0].y, t.v[1].z - t.v[0].z};
-        const V3 e2{t.v[2].x - t.v[0].x, t.v[2].y - t.v[0].y, t.v[2].z - t.v[0].z};
-        const V3 nn{fma(e1.y, e2.z, -e1.z * e2.y), fma(e1.z, e2.x, -e1.x * e2.z), fma(e1.x, e2.y, -e1.y * e2.x)};
-        const double nl = sqrt(fma(nn.x, nn.x, fma(nn.y, nn.y, nn.z * nn.z)));
-        const double inv = nl > 0.0 ? 1.0 / nl : 0.0;
-        w[16] = nn.x * inv;
-        w[17] = nn.y * inv;
-        w[18] = nn.z * inv;
-        w[19] = fma(w[16], t.v[0].x, fma(w[17], t.v[0].y, w[18] * t.v[0].z));
-        w[12] = c.x;
-        w[13] = c.y;
-        w[14] = c.z;
-        // sliver flag from the body record; a zero-area triangle is never culled either
-        w[15] = rad >= 0.0 && nl > 0.0 ? sqrt(r2) * (1.0 + 1e-12) : -1.0;
+  __shared__ const double* s_src[128];
+  const int64_t n_world = woff[n];
+  for (int64_t w0 = (int64_t)blockIdx.x * 128; w0 < n_world; w0 += (int64_t)gridDim.x * 128) {
+    const int m = (int)min((int64_t)128, n_world - w0);
+    const int64_t w = w0 + threadIdx.x;
+    int b = 0;
+    int64_t j = 0;
+    if (threadIdx.x < m) {
+      int lo = 0, hi = n;  // body of world record w: last b with woff[b] <= w
+      while (hi - lo > 1) {
+        const int mid = (lo + hi) >> 1;
+        if (__ldg(woff + mid) <= w) lo = mid; else hi = mid;
       }
-      __syncthreads();
-      double2* dst = reinterpret_cast<double2*>(world + (size_t)(woff[b] + j0) * kWorld);
-      const double2* so2 = reinterpret_cast<const double2*>(s_out);
-      for (int k = threadIdx.x; k < m * kWorld / 2; k += blockDim.x) dst[k] = so2[k];
-      __syncthreads();
+      b = lo;
+      j = w - woff[b];
+      s_src[threadIdx.x] = tris + (size_t)(bodies[b].level_off[0] + j) * kRecord;
     }
+    __syncthreads();
+    double2* sm2 = reinterpret_cast<double2*>(s_rec);
+    {  // all loads in flight before the first shared-memory store
+      constexpr int kPer = kRecord / 2;  // 8 double2 per record, 8 per thread
+      double2 v[kPer];
+#pragma unroll
+      for (int u = 0; u < kPer; ++u) {
+        const int k = threadIdx.x + u * 128;
+        if (k < m * kPer) v[u] = __ldg(reinterpret_cast<const double2*>(s_src[k / kPer]) + k % kPer);
+      }
+#pragma unroll
+      for (int u = 0; u < kPer; ++u) {
+        const int k = threadIdx.x + u * 128;
+        if (k < m * kPer) sm2[k] = v[u];
+      }
+    }
+    __syncthreads();
+    if (threadIdx.x < m) {
+      const BodyInfo& B = bodies[b];
+      double pos[3];
+      position_at(B.m, 0.0, pos);
+      double* r = s_rec + threadIdx.x * kRecord;
+      double L[9];
+#pragma unroll
+      for (int k = 0; k < 9; ++k) L[k] = r[k];
+      const Tri t = world_tri(B.m.base, pos, L);
+      double* wr = s_out + threadIdx.x * kWorld;
+      wr[9] = r[9];
+      wr[10] = r[10];
+#pragma unroll
+      for (int k = 0; k < 3; ++k) {
+        wr[3 * k] = t.v[k].x;
+        wr[3 * k + 1] = t.v[k].y;
+        wr[3 * k + 2] = t.v[k].z;
+      }
+      {  // first child as an absolute world index (children are contiguous)
+        int lvl = 0;
+        while (lvl + 1 < B.n_levels && B.level_off[0] + j >= B.level_off[lvl + 1]) ++lvl;
+        int2 ch = *reinterpret_cast<const int2*>(r + 11);
+        if (lvl > 0) ch.x = (int32_t)(woff[b] + B.level_off[lvl - 1] - B.level_off[0] + ch.x);
+        *reinterpret_cast<int2*>(wr + 11) = ch;
+      }
+      // bounding sphere in world coordinates (approximate; the cull margin absorbs it)
+      const double rad = r[15];
+      constexpr double kThird = 1.0 / 3.0;
+      const V3 c{(t.v[0].x + t.v[1].x + t.v[2].x) * kThird, (t.v[0].y + t.v[1].y + t.v[2].y) * kThird,
+                 (t.v[0].z + t.v[1].z + t.v[2].z) * kThird};
+      double r2 = 0.0;
+#pragma unroll
+      for (int k = 0; k < 3; ++k) {
+        const V3 d = t.v[k] - c;
+        r2 = fmax(r2, fma(d.x, d.x, fma(d.y, d.y, d.z * d.z)));
+      }
+      // unit face normal and plane offset for the separating-axis cull
+      const V3 e1{t.v[1].x - t.v[0].x, t.v[1].y - t.v[0].y, t.v[1].z - t.v[0].z};
+      const V3 e2{t.v[2].x - t.v[0].x, t.v[2].y - t.v[0].y, t.v[2].z - t.v[0].z};
+      const V3 nn{fma(e1.y, e2.z, -e1.z * e2.y), fma(e1.z, e2.x, -e1.x * e2.z), fma(e1.x, e2.y, -e1.y * e2.x)};
+      const double nl = sqrt(fma(nn.x, nn.x, fma(nn.y, nn.y, nn.z * nn.z)));
+      const double inv = nl > 0.0 ? 1.0 / nl : 0.0;
+      wr[16] = nn.x * inv;
+      wr[17] = nn.y * inv;
+      wr[18] = nn.z * inv;
+      wr[19] = fma(wr[16], t.v[0].x, fma(wr[17], t.v[0].y, wr[18] * t.v[0].z));
+      wr[12] = c.x;
+      wr[13] = c.y;
+      wr[14] = c.z;
+      // sliver flag from the body record; a zero-area triangle is never culled either
+      wr[15] = rad >= 0.0 && nl > 0.0 ? sqrt(r2) * (1.0 + 1e-12) : -1.0;
+      double2* sp = reinterpret_cast<double2*>(wsph + (size_t)w * kSph);
+      sp[0] = make_double2(c.x, c.y);
+      sp[1] = make_double2(c.z, wr[15] < 0.0 ? -1.0 : wr[15] + r[9]);
+    }
+    __syncthreads();
+    double2* dst = reinterpret_cast<double2*>(world + (size_t)w0 * kWorld);
+    const double2* so2 = reinterpret_cast<const double2*>(s_out);
+    for (int k = threadIdx.x; k < m * kWorld / 2; k += blockDim.x) dst[k] = so2[k];
+    __syncthreads();
   }
 }
 
@@ -967,18 +998,28 @@ constexpr int kStaticStageBytes = kStaged * 32 * kStaticWarps * sizeof(double);
 // certified sphere cull the moment it is emitted: a culled child is a
 // decided row (not flagged, not resting) and is only counted, so the next
 // frontier holds exactly the rows that need the 15-feature distance.
-__device__ __forceinline__ bool static_child_cull(const double* world, int32_t wa, int32_t wb) {
-  const double* pa = world + (size_t)wa * kWorld;
-  const double* pb = world + (size_t)wb * kWorld;
-  const double h = add(__ldg(pa + 9), __ldg(pb + 9));
-  return sphere_cull(pa, pb, add(h, kRestSlop));
+// Compact cull spheres of the world records, one 32-B sector each:
+// (centre, R = radius + epsilon), R = -1 for slivers.  The sphere test of a
+// child pair reads two sectors instead of four, and the whole array of a
+// c1 batch (112 MB) stays L2-resident.
+__device__ __forceinline__ bool static_child_cull(const double* __restrict__ wsph, int32_t wa, int32_t wb) {
+  const double2* pa = reinterpret_cast<const double2*>(wsph + (size_t)wa * kSph);
+  const double2* pb = reinterpret_cast<const double2*>(wsph + (size_t)wb * kSph);
+  const double2 a01 = __ldg(pa), a2r = __ldg(pa + 1), b01 = __ldg(pb), b2r = __ldg(pb + 1);
+  if (a2r.y < 0.0 || b2r.y < 0.0) return false;  // slivers are never culled
+  const double dx = a01.x - b01.x, dy = a01.y - b01.y, dz = a2r.x - b2r.x;
+  // same certificate as sphere_cull with thr = eps_a + eps_b + 1e-9 folded into R
+  const double scale = 1.0 + fabs(a01.x) + fabs(a01.y) + fabs(a2r.x) + a2r.y + b2r.y;
+  const double reach = a2r.y + b2r.y + kRestSlop + kCullMargin * scale;
+  return fma(dx, dx, fma(dy, dy, dz * dz)) > reach * reach;
 }
 
-// Seeds (roots x roots per pair, ccd.py:385-391) in world indices, culled.
+// Seeds (roots x roots per pair, ccd.py:385-391) in world indices, culled
+// (sphere, then separating axes): the frontier holds only exact rows.
 __global__ void k_seed_static(const PairInfo* __restrict__ pairs, int64_t n_pairs,
                               const BodyInfo* __restrict__ bodies, const int64_t* __restrict__ woff,
-                              const double* __restrict__ world, Cand* out, unsigned long long cap,
-                              Counters* ctr, unsigned long long* n_out, int exhaustive) {
+                              const double* __restrict__ world, const double* __restrict__ wsph, Cand* out,
+                              unsigned long long cap, Counters* ctr, unsigned long long* n_out, int exhaustive) {
   const int lane = threadIdx.x & 31;
   unsigned long long culled = 0;
   for (int64_t k = blockIdx.x; k < n_pairs; k += gridDim.x) {
@@ -996,11 +1037,16 @@ __global__ void k_seed_static(const PairInfo* __restrict__ pairs, int64_t n_pair
       if (j < na * nb) {
         wa = (int32_t)(a0 + j / nb);
         wb = (int32_t)(b0 + j % nb);
-        keep = !static_child_cull(world, wa, wb);
+        keep = !static_child_cull(wsph, wa, wb);
+        if (keep) {
+          const double* pa = world + (size_t)wa * kWorld;
+          const double* pb = world + (size_t)wb * kWorld;
+          keep = !sat_cull(pa, pb, add(add(__ldg(pa + 9), __ldg(pb + 9)), kRestSlop));
+        }
       }
       const unsigned m = __ballot_sync(0xffffffffu, keep);
       const int nvalid = (int)min((int64_t)32, na * nb - j0);
-      culled += (unsigned long long)(nvalid - __popc(m));
+      culled += (unsigned long long)nvalid;  // every seed is a test; survivors go to the exact pass
       unsigned long long base = 0;
       if (lane == 0 && m) base = atomicAdd(n_out, (unsigned long long)__popc(m));
       base = __shfl_sync(0xffffffffu, base, 0);
@@ -1013,48 +1059,38 @@ __global__ void k_seed_static(const PairInfo* __restrict__ pairs, int64_t n_pair
   if (lane == 0 && culled) atomicAdd(&ctr->rows, culled);
 }
 
-// Sphere data of one world record, pre-folded for the emission cull:
-// centre, and R = radius + epsilon (+ the margin share of this side).
-struct EmitSphere {
-  double x, y, z, r, e, s;  // centre, radius (-1: sliver), epsilon, |centre|_1
+// A flagged coarse row of a static generation: its na x nb children
+// (ccd.py:418-427) in absolute world indices.
+struct Parent {
+  int32_t pair, a0, b0;
+  uint8_t na, nb, la, lb;
 };
-__device__ __forceinline__ EmitSphere emit_sphere(const double* w) {
-  const double2 c01 = __ldg(reinterpret_cast<const double2*>(w + 12));
-  const double2 c2r = __ldg(reinterpret_cast<const double2*>(w + 14));
-  return EmitSphere{c01.x, c01.y, c2r.x, c2r.y, __ldg(w + 9), fabs(c01.x) + fabs(c01.y) + fabs(c2r.x)};
-}
-// Same certified test as static_child_cull / sphere_cull (scale from A's centre).
-__device__ __forceinline__ bool emit_cull(const EmitSphere& a, const EmitSphere& b) {
-  if (a.r < 0.0 || b.r < 0.0) return false;
-  const double dx = a.x - b.x, dy = a.y - b.y, dz = a.z - b.z;
-  const double thr = add(add(a.e, b.e), kRestSlop);
-  const double scale = 1.0 + a.s + a.r + b.r;
-  const double reach = a.r + b.r + thr + kCullMargin * scale;
-  return fma(dx, dx, fma(dy, dy, dz * dz)) > reach * reach;
-}
+static_assert(sizeof(Parent) == 16, "Parent layout");
+static_assert(sizeof(Parent) <= sizeof(Cand), "parents are stored in a candidate buffer");
 
+// Exact pass of a static generation.  The frontier holds only rows that
+// survived the certified culls, so every row gets the exact 15-feature
+// distance, one per lane, from shared-memory staging.  Fine rows apply the
+// resting test (ccd.py:407-409); a flagged coarse row (ccd.py:410-411)
+// becomes a Parent, appended with one atomic per block iteration.  The
+// children are generated and culled by k_expand_filter at full occupancy.
 __global__ void __launch_bounds__(32 * kStaticWarps, LTSG_STATIC_MINB)
 k_screen_static(const Cand* __restrict__ front, int64_t n, const PairInfo* __restrict__ pairs,
                 const BodyInfo* __restrict__ bodies, const double* __restrict__ world,
-                const int64_t* __restrict__ woff, ScreenOut out) {
+                const int64_t* __restrict__ woff, ScreenOut out, Parent* __restrict__ par,
+                unsigned long long* n_par) {
   if (out.n_in) n = (int64_t)min(*out.n_in, out.next_cap);
   extern __shared__ double s_stage[];  // kStaged x (32 * kStaticWarps)
   const Staged<32 * kStaticWarps> st{s_stage + threadIdx.x};
   const int lane = threadIdx.x & 31;
   const int warp = threadIdx.x >> 5;
-  // The frontier holds only rows that survived the certified culls (sphere
-  // at emission, separating axes in k_sat_filter): every row gets the exact
-  // 15-feature distance, one per lane.  A flagged coarse row is then
-  // expanded by its own lane: the na x nb children (ccd.py:418-427) are
-  // sphere-culled with the child spheres held in registers, counted, and
-  // the survivors written after one warp-wide scan and one atomic.
-  unsigned long long culled = 0;
-  if (blockIdx.x == 0 && threadIdx.x == 0) atomicAdd(&out.ctr->screen_exact, (unsigned long long)n);
+  if (blockIdx.x == 0 && threadIdx.x == 0 && n > 0) atomicAdd(&out.ctr->screen_exact, (unsigned long long)n);
   const int64_t n_warps = (n + 31) / 32;
   for (int64_t wi = blockIdx.x * (int64_t)kStaticWarps + warp; wi < n_warps;
        wi += (int64_t)gridDim.x * kStaticWarps) {
     const int64_t ci = wi * 32 + lane;
-    int cnt = 0, na = 1, nb = 1, a0 = 0, b0 = 0, cla = 0, clb = 0, cpair = 0;
+    bool flagged = false;
+    Parent P{};
     if (ci < n) {
       const Cand c = front[ci];
       const double* wa = world + (size_t)c.ia * kWorld;
@@ -1070,8 +1106,7 @@ k_screen_static(const Cand* __restrict__ front, int64_t n, const PairInfo* __res
             out.resting[slot] = RestRec{c.pair, (int32_t)(c.ia - woff[p.ba]), (int32_t)(c.ib - woff[p.bb]), 0, h};
         }
       } else if (d <= h) {
-        a0 = c.ia;
-        b0 = c.ib;
+        int a0 = c.ia, b0c = c.ib, na = 1, nb = 1;
         if (c.la > 0) {
           const int2 cr = *reinterpret_cast<const int2*>(wa + 11);
           a0 = cr.x;
@@ -1079,106 +1114,106 @@ k_screen_static(const Cand* __restrict__ front, int64_t n, const PairInfo* __res
         }
         if (c.lb > 0) {
           const int2 cr = *reinterpret_cast<const int2*>(wb + 11);
-          b0 = cr.x;
+          b0c = cr.x;
           nb = cr.y;
         }
-        cpair = c.pair;
-        cnt = na * nb;
-        cla = c.la > 0 ? c.la - 1 : 0;
-        clb = c.lb > 0 ? c.lb - 1 : 0;
+        P = Parent{c.pair, a0, b0c, (uint8_t)na, (uint8_t)nb, (uint8_t)(c.la > 0 ? c.la - 1 : 0),
+                   (uint8_t)(c.lb > 0 ? c.lb - 1 : 0)};
+        flagged = true;
       }
     }
-    // children in chunks of 64 per lane (a fanout-4 parent pair has 16)
-    for (int c0 = 0; __any_sync(0xffffffffu, c0 < cnt); c0 += 64) {
-      const int m = cnt > c0 ? min(64, cnt - c0) : 0;
-      unsigned long long mask = 0;
-      int k0 = 0, l0 = 0;
-      if (m > 0) {
-        k0 = c0 / nb;
-        l0 = c0 - k0 * nb;
-        int k = k0, l = l0;
-        EmitSphere sa = emit_sphere(world + (size_t)(a0 + k) * kWorld);
-        for (int j = 0; j < m; ++j) {
-          const EmitSphere sb = emit_sphere(world + (size_t)(b0 + l) * kWorld);
-          if (!emit_cull(sa, sb)) mask |= 1ULL << j;
-          if (++l == nb) {
-            l = 0;
-            ++k;
-            if (j + 1 < m) sa = emit_sphere(world + (size_t)(a0 + k) * kWorld);
-          }
-        }
-      }
-      const int kept = __popcll(mask);
-      culled += (unsigned long long)(m - kept);
-      const int incl = warp_incl_scan(kept, lane);
-      const int tot = __shfl_sync(0xffffffffu, incl, 31);
-      unsigned long long base = 0;
-      if (lane == 31 && tot) base = atomicAdd(out.n_out, (unsigned long long)tot);
-      base = __shfl_sync(0xffffffffu, base, 31);
-      unsigned long long dst = base + (unsigned long long)(incl - kept);
-      int k = k0, l = l0;
-      for (int j = 0; j < m; ++j) {
-        if ((mask >> j) & 1ULL) {
-          if (dst < out.next_cap)
-            out.next[dst] = Cand{cpair, a0 + k, b0 + l, (int16_t)cla, (int16_t)clb, 0.0};
-          ++dst;
-        }
-        if (++l == nb) {
-          l = 0;
-          ++k;
-        }
-      }
-    }
+    // per-warp append: only this warp waits for the atomic
+    const unsigned m = __ballot_sync(0xffffffffu, flagged);
+    unsigned long long base = 0;
+    if (lane == 0 && m) base = atomicAdd(n_par, (unsigned long long)__popc(m));
+    base = __shfl_sync(0xffffffffu, base, 0);
+    if (flagged) par[base + __popc(m & ((1u << lane) - 1u))] = P;
   }
-  for (int o = 16; o > 0; o >>= 1) culled += __shfl_xor_sync(0xffffffffu, culled, o);
-  if (lane == 0 && culled) atomicAdd(&out.ctr->rows, culled);  // children settled by the sphere cull
 }
 
-// Separating-axis filter between two static generations: every frontier row
-// is a test (counted here); rows the certified cull settles are dropped, the
-// rest are compacted (one atomic per block iteration) for k_screen_static.
-// Runs at full occupancy: it is load-latency bound, the exact kernel is not.
-constexpr int kSatThreads = 256;
-#ifndef LTSG_SAT_MINB
-#define LTSG_SAT_MINB 4
-#endif
-__global__ void __launch_bounds__(kSatThreads, LTSG_SAT_MINB)
-k_sat_filter(const Cand* __restrict__ in, int64_t n, const unsigned long long* n_in, unsigned long long in_cap,
-             const double* __restrict__ world, Cand* __restrict__ out, unsigned long long* n_out,
-             Counters* ctr) {
-  if (n_in) n = (int64_t)min(*n_in, in_cap);
-  __shared__ int s_cnt[kSatThreads / 32];
-  __shared__ unsigned long long s_base;
-  const int warp = threadIdx.x >> 5;
+// Children of the flagged rows of one static generation (ccd.py:418-427),
+// one thread per child slot (fan = max_children^2 slots per parent): every
+// child is a test (counted here); the certified sphere cull, then the
+// separating-axis cull on the block-compacted sphere survivors, settle
+// most of them, and the rest are appended (one atomic per block
+// iteration) as the next generation's exact frontier.
+constexpr int kExpThreads = 256;
+constexpr int kExpWarps = kExpThreads / 32;
+// Each warp works alone (no block barriers, so the load latency of one warp
+// overlaps the work of the others): 32 child slots per step through the
+// sphere cull into a per-warp queue; every 32 queued rows get the SAT cull
+// with all lanes busy; survivors collect in a per-warp output buffer that
+// is flushed 64 at a time with one atomic.
+__global__ void __launch_bounds__(kExpThreads, 4)
+k_expand_filter(const Parent* __restrict__ par, const unsigned long long* n_par, unsigned long long par_cap,
+                int fan, const double* __restrict__ world, const double* __restrict__ wsph, Cand* __restrict__ next,
+                unsigned long long next_cap, unsigned long long* n_out, Counters* ctr) {
+  const int64_t npar = (int64_t)min(*n_par, par_cap);
+  const int64_t total = npar * fan;
+  __shared__ Cand s_q[kExpWarps][64];
+  __shared__ Cand s_o[kExpWarps][96];
   const int lane = threadIdx.x & 31;
-  if (blockIdx.x == 0 && threadIdx.x == 0 && n > 0) atomicAdd(&ctr->rows, (unsigned long long)n);
-  for (int64_t b0 = (int64_t)blockIdx.x * kSatThreads; b0 < n; b0 += (int64_t)gridDim.x * kSatThreads) {
-    const int64_t ci = b0 + threadIdx.x;
+  const int warp = threadIdx.x >> 5;
+  Cand* q = s_q[warp];
+  Cand* o = s_o[warp];
+  const unsigned lt = (1u << lane) - 1u;
+  int nq = 0, no = 0;
+  unsigned long long rows = 0;
+  auto flush = [&](int cnt) {  // warp-uniform: write the first cnt buffered rows
+    unsigned long long base = 0;
+    if (lane == 0 && cnt) base = atomicAdd(n_out, (unsigned long long)cnt);
+    base = __shfl_sync(0xffffffffu, base, 0);
+    for (int k = lane; k < cnt; k += 32)
+      if (base + k < next_cap) next[base + k] = o[k];
+    __syncwarp();
+    for (int k = cnt + lane; k < no; k += 32) o[k - cnt] = o[k];  // keep the rest (no - cnt < 32)
+    __syncwarp();
+    no -= cnt;
+  };
+  auto sat_step = [&](int m) {  // SAT cull of the top m queued rows, survivors to the output buffer
     bool keep = false;
     Cand c{};
-    if (ci < n) {
-      c = in[ci];
-      const double* wa = world + (size_t)c.ia * kWorld;
-      const double* wb = world + (size_t)c.ib * kWorld;
-      keep = !sat_cull(wa, wb, add(add(__ldg(wa + 9), __ldg(wb + 9)), kRestSlop));
+    if (lane < m) {
+      c = q[nq - m + lane];
+      const double* pa = world + (size_t)c.ia * kWorld;
+      const double* pb = world + (size_t)c.ib * kWorld;
+      keep = !sat_cull(pa, pb, add(add(__ldg(pa + 9), __ldg(pb + 9)), kRestSlop));
     }
-    const unsigned m = __ballot_sync(0xffffffffu, keep);
-    if (lane == 0) s_cnt[warp] = __popc(m);
-    __syncthreads();
-    if (threadIdx.x == 0) {
-      int tot = 0;
-#pragma unroll
-      for (int w = 0; w < kSatThreads / 32; ++w) {
-        const int x = s_cnt[w];
-        s_cnt[w] = tot;
-        tot += x;
+    const unsigned mk = __ballot_sync(0xffffffffu, keep);
+    __syncwarp();
+    if (keep) o[no + __popc(mk & lt)] = c;
+    __syncwarp();
+    nq -= m;
+    no += __popc(mk);
+    if (no >= 64) flush(64);
+  };
+  for (int64_t t0 = ((int64_t)blockIdx.x * kExpWarps + warp) * 32; t0 < total;
+       t0 += (int64_t)gridDim.x * kExpThreads) {
+    const int64_t t = t0 + lane;
+    bool keep = false;
+    Cand c{};
+    if (t < total) {
+      const int64_t pi = t / fan;
+      const int j = (int)(t - pi * fan);
+      const Parent P = par[pi];
+      if (j < (int)P.na * (int)P.nb) {
+        ++rows;
+        const int k = j / P.nb;
+        c = Cand{P.pair, P.a0 + k, P.b0 + (j - k * P.nb), (int16_t)P.la, (int16_t)P.lb, 0.0};
+        keep = !static_child_cull(wsph, c.ia, c.ib);
       }
-      s_base = tot ? atomicAdd(n_out, (unsigned long long)tot) : 0ULL;
     }
-    __syncthreads();
-    if (keep) out[s_base + s_cnt[warp] + __popc(m & ((1u << lane) - 1u))] = c;
-    __syncthreads();
+    const unsigned mk = __ballot_sync(0xffffffffu, keep);
+    if (keep) q[nq + __popc(mk & lt)] = c;
+    __syncwarp();
+    nq += __popc(mk);
+    if (nq >= 32) sat_step(32);
   }
+  if (nq > 0) sat_step(nq);
+  if (no > 0) flush(no);
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) rows += __shfl_xor_sync(0xffffffffu, rows, off);
+  if (lane == 0 && rows) atomicAdd(&ctr->rows, rows);
 }
 
 // ---------------------------------------------------------------- zoom
@@ -2040,12 +2075,14 @@ static int run_search(const ltsg_scene* sc, ltsg_result* out, ltsg_workspace* ws
   // ---- static batches: tau = 0 world records, sphere data, culled seeds
   bool all_static = false;
   double* world = nullptr;
+  double* wsph = nullptr;
   int64_t* woff = nullptr;
   if (sc->n_pairs > 0) {
     std::vector<double> hdt(np);
     LTSG_CUDA(cudaMemcpyAsync(hdt.data(), sc->problem_dt, sizeof(double) * np, cudaMemcpyDeviceToHost, st));
     LTSG_CUDA(cudaStreamSynchronize(st));
     all_static = std::all_of(hdt.begin(), hdt.end(), [](double d) { return d == 0.0; });
+    if (sc->max_children > 255) all_static = false;  // static parents hold 8-bit child counts
     const char* env = getenv("LTSG_NO_STATIC");
     if (env && env[0] == '1') all_static = false;
   }
@@ -2062,9 +2099,10 @@ static int run_search(const ltsg_scene* sc, ltsg_result* out, ltsg_workspace* ws
     if (n_world >= (int64_t)1 << 31) {
       all_static = false;  // world indices are int32 in the candidates
     } else {
-      LTSG_TRY(ws_get(ws, "world", (size_t)std::max<int64_t>(n_world, 1) * kWorld, &world));
-      k_world_fill<<<(int)std::min<int64_t>(sc->n_bodies, 148 * 8), 128, 0, st>>>(pr.bodies, sc->n_bodies,
-                                                                                  woff, sc->tris, world);
+      LTSG_TRY(ws_get(ws, "world", (size_t)std::max<int64_t>(n_world, 1) * (kWorld + kSph), &world));
+      wsph = world + (size_t)std::max<int64_t>(n_world, 1) * kWorld;
+      k_world_fill<<<(int)std::max<int64_t>(1, std::min<int64_t>((n_world + 127) / 128, 148 * 12)), 128, 0, st>>>(
+          pr.bodies, sc->n_bodies, woff, sc->tris, world, wsph);
       LTSG_LAUNCHED();
     }
   }
@@ -2109,7 +2147,7 @@ static int run_search(const ltsg_scene* sc, ltsg_result* out, ltsg_workspace* ws
   constexpr int kMaxGen = 2 * kMaxLevels;
   unsigned long long *gen_cnt, *x_cnt;
   LTSG_TRY(ws_get(ws, "gen_cnt", kMaxGen + 1, &gen_cnt));
-  LTSG_TRY(ws_get(ws, "x_cnt", kMaxGen + 1, &x_cnt));  // static: survivors of k_sat_filter per generation
+  LTSG_TRY(ws_get(ws, "x_cnt", kMaxGen + 1, &x_cnt));  // static: flagged parents per generation
   const int64_t fan = (int64_t)sc->max_children * sc->max_children;
   size_t rest_cap = std::max<size_t>(1 << 16, ws->hint_rest), entry_cap = std::max<size_t>(1 << 14, ws->hint_entries),
          cross_cap = std::max<size_t>(1 << 14, ws->hint_cross);
@@ -2124,19 +2162,15 @@ static int run_search(const ltsg_scene* sc, ltsg_result* out, ltsg_workspace* ws
                            unsigned long long* xcnt) -> int {
     ScreenOut so{next, cap, n_in, n_out, resting, rest_cap, entries, entry_cap, cross, cross_cap, d_ctr};
     if (all_static) {
-      // separating-axis filter into xbuf (count in xcnt), then the exact screen of the survivors
-      const int64_t sblocks = n_in ? 148LL * 8 : (n + kSatThreads - 1) / kSatThreads;
-      k_sat_filter<<<(int)std::max<int64_t>(1, std::min<int64_t>(sblocks, 148LL * 8)), kSatThreads, 0, st>>>(
-          in, n, n_in, cap, world, xbuf, xcnt, d_ctr);
+      // exact pass of the frontier (parents into xbuf, count in xcnt), then
+      // the culled expansion of the parents into the next frontier
+      const int64_t blocks = n_in ? 148LL * 20 : (n + 32 * kStaticWarps - 1) / (32 * kStaticWarps);
+      k_screen_static<<<(int)std::max<int64_t>(1, std::min<int64_t>(blocks, 148LL * 20)), 32 * kStaticWarps,
+                        kStaticStageBytes, st>>>(in, n, pr.pairs, pr.bodies, world, woff, so,
+                                                 reinterpret_cast<Parent*>(xbuf), xcnt);
       LTSG_LAUNCHED();
-      in = xbuf;
-      so.n_in = xcnt;
-      // async: the frontier size is unknown on the host; a generous grid lets
-      // the block scheduler balance uneven rows (spare blocks exit at once)
-      const int64_t blocks = n_in ? 148LL * 16 : (n + 32 * kStaticWarps - 1) / (32 * kStaticWarps);
-      n_in = xcnt;
-      k_screen_static<<<(int)std::max<int64_t>(1, std::min<int64_t>(blocks, 148LL * 32)), 32 * kStaticWarps,
-                        kStaticStageBytes, st>>>(in, n, pr.pairs, pr.bodies, world, woff, so);
+      k_expand_filter<<<148 * 8, kExpThreads, 0, st>>>(reinterpret_cast<const Parent*>(xbuf), xcnt, cap, (int)fan,
+                                                       world, wsph, next, cap, n_out, d_ctr);
     } else {
       const int grid = n_in ? 148 * 32 : screen_grid(n);
       k_screen<<<grid, 32 * kScreenWarps, kScreenStageBytes, st>>>(in, n, pr.pairs, pr.bodies, sc->tris, so,
@@ -2168,7 +2202,7 @@ static int run_search(const ltsg_scene* sc, ltsg_result* out, ltsg_workspace* ws
     t_screen.start(st);
     if (all_static) {
       k_seed_static<<<(int)std::min<int64_t>(sc->n_pairs, 148 * 16), 128, 0, st>>>(
-          pr.pairs, sc->n_pairs, pr.bodies, woff, world, front, seed_cap, d_ctr, gen_cnt, sc->exhaustive);
+          pr.pairs, sc->n_pairs, pr.bodies, woff, world, wsph, front, seed_cap, d_ctr, gen_cnt, sc->exhaustive);
     } else {
       k_seed_fill<<<(int)std::min<int64_t>(sc->n_pairs, 148 * 16), 128, 0, st>>>(
           pr.pairs, sc->n_pairs, pr.bodies, sc->exhaustive, seed_off, front);
@@ -2213,7 +2247,7 @@ static int run_search(const ltsg_scene* sc, ltsg_result* out, ltsg_workspace* ws
       LTSG_CUDA(cudaMemsetAsync(gen_cnt, 0, sizeof(unsigned long long) * (kMaxGen + 1), st));
       LTSG_TRY(ws_get(ws, "front0", (size_t)n_first, &front));
       k_seed_static<<<(int)std::min<int64_t>(sc->n_pairs, 148 * 16), 128, 0, st>>>(
-          pr.pairs, sc->n_pairs, pr.bodies, woff, world, front, n_first, d_ctr, gen_cnt, sc->exhaustive);
+          pr.pairs, sc->n_pairs, pr.bodies, woff, world, wsph, front, n_first, d_ctr, gen_cnt, sc->exhaustive);
       LTSG_LAUNCHED();
       LTSG_CUDA(cudaMemcpyAsync(&n_first, gen_cnt, sizeof(n_first), cudaMemcpyDeviceToHost, st));
       LTSG_TRY(read_ctr(d_ctr, &h, st));
@@ -2511,9 +2545,11 @@ static int build_world(const ltsg_scene* sc, const Prepared& pr, ltsg_workspace*
     *world = nullptr;
     return LTSG_OK;
   }
-  LTSG_TRY(ws_get(ws, "world", (size_t)std::max<int64_t>(*n_world, 1) * kWorld, world));
-  k_world_fill<<<(int)std::min<int64_t>(sc->n_bodies, 148 * 8), 128, 0, st>>>(pr.bodies, sc->n_bodies, *woff,
-                                                                              sc->tris, *world);
+  LTSG_TRY(ws_get(ws, "world", (size_t)std::max<int64_t>(*n_world, 1) * (kWorld + kSph), world));
+  k_world_fill<<<(int)std::max<int64_t>(1, std::min<int64_t>((*n_world + 127) / 128, 148 * 12)), 128, 0, st>>>(
+      pr.bodies, sc->n_bodies, *woff,
+                                                                              sc->tris, *world,
+                                                                              *world + (size_t)std::max<int64_t>(*n_world, 1) * kWorld);
   LTSG_CHECK_LAUNCH();
   *launches += 2;
   return LTSG_OK;
