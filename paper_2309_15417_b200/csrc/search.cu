@@ -799,106 +799,88 @@ __global__ void __launch_bounds__(128) k_world_fill(const BodyInfo* __restrict__
                                                     const int64_t* __restrict__ woff,
                                                     const double* __restrict__ tris, double* __restrict__ world,
                                                     double* __restrict__ wsph) {
-  // Chunks of 128 consecutive world records (any body boundaries inside),
-  // moved through shared memory so that both the record loads and the
-  // world-record stores are coalesced.  Grid-stride over all chunks keeps
-  // every SM busy whatever the body sizes.
-  __shared__ double s_rec[128 * kRecord];
-  __shared__ double s_out[128 * kWorld];
-  __shared__ const double* s_src[128];
+  // One world record per lane, warps independent (no block barriers): the
+  // 8 record loads of a lane are all in flight at once.  A warp covers 32
+  // consecutive world records; their bodies are found by one binary search
+  // (lane 0) and a short forward walk per lane.
+  const int lane = threadIdx.x & 31;
   const int64_t n_world = woff[n];
-  for (int64_t w0 = (int64_t)blockIdx.x * 128; w0 < n_world; w0 += (int64_t)gridDim.x * 128) {
-    const int m = (int)min((int64_t)128, n_world - w0);
-    const int64_t w = w0 + threadIdx.x;
-    int b = 0;
-    int64_t j = 0;
-    if (threadIdx.x < m) {
-      int lo = 0, hi = n;  // body of world record w: last b with woff[b] <= w
+  for (int64_t w0 = ((int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5)) * 32; w0 < n_world;
+       w0 += (int64_t)gridDim.x * blockDim.x) {
+    int b0 = 0;
+    if (lane == 0) {
+      int lo = 0, hi = n;  // last b with woff[b] <= w0
       while (hi - lo > 1) {
         const int mid = (lo + hi) >> 1;
-        if (__ldg(woff + mid) <= w) lo = mid; else hi = mid;
+        if (__ldg(woff + mid) <= w0) lo = mid; else hi = mid;
       }
-      b = lo;
-      j = w - woff[b];
-      s_src[threadIdx.x] = tris + (size_t)(bodies[b].level_off[0] + j) * kRecord;
+      b0 = lo;
     }
-    __syncthreads();
-    double2* sm2 = reinterpret_cast<double2*>(s_rec);
-    {  // all loads in flight before the first shared-memory store
-      constexpr int kPer = kRecord / 2;  // 8 double2 per record, 8 per thread
-      double2 v[kPer];
+    b0 = __shfl_sync(0xffffffffu, b0, 0);
+    const int64_t w = w0 + lane;
+    if (w >= n_world) continue;
+    int b = b0;
+    while (__ldg(woff + b + 1) <= w) ++b;
+    const int64_t j = w - woff[b];
+    const BodyInfo& B = bodies[b];
+    const double2* src = reinterpret_cast<const double2*>(tris + (size_t)(B.level_off[0] + j) * kRecord);
+    double r[kRecord];
 #pragma unroll
-      for (int u = 0; u < kPer; ++u) {
-        const int k = threadIdx.x + u * 128;
-        if (k < m * kPer) v[u] = __ldg(reinterpret_cast<const double2*>(s_src[k / kPer]) + k % kPer);
-      }
-#pragma unroll
-      for (int u = 0; u < kPer; ++u) {
-        const int k = threadIdx.x + u * 128;
-        if (k < m * kPer) sm2[k] = v[u];
-      }
+    for (int k = 0; k < kRecord / 2; ++k) {
+      const double2 v = __ldg(src + k);
+      r[2 * k] = v.x;
+      r[2 * k + 1] = v.y;
     }
-    __syncthreads();
-    if (threadIdx.x < m) {
-      const BodyInfo& B = bodies[b];
-      double pos[3];
-      position_at(B.m, 0.0, pos);
-      double* r = s_rec + threadIdx.x * kRecord;
-      double L[9];
+    double pos[3];
+    position_at(B.m, 0.0, pos);
+    const Tri t = world_tri(B.m.base, pos, r);
+    double wr[kWorld];
 #pragma unroll
-      for (int k = 0; k < 9; ++k) L[k] = r[k];
-      const Tri t = world_tri(B.m.base, pos, L);
-      double* wr = s_out + threadIdx.x * kWorld;
-      wr[9] = r[9];
-      wr[10] = r[10];
-#pragma unroll
-      for (int k = 0; k < 3; ++k) {
-        wr[3 * k] = t.v[k].x;
-        wr[3 * k + 1] = t.v[k].y;
-        wr[3 * k + 2] = t.v[k].z;
-      }
-      {  // first child as an absolute world index (children are contiguous)
-        int lvl = 0;
-        while (lvl + 1 < B.n_levels && B.level_off[0] + j >= B.level_off[lvl + 1]) ++lvl;
-        int2 ch = *reinterpret_cast<const int2*>(r + 11);
-        if (lvl > 0) ch.x = (int32_t)(woff[b] + B.level_off[lvl - 1] - B.level_off[0] + ch.x);
-        *reinterpret_cast<int2*>(wr + 11) = ch;
-      }
-      // bounding sphere in world coordinates (approximate; the cull margin absorbs it)
-      const double rad = r[15];
-      constexpr double kThird = 1.0 / 3.0;
-      const V3 c{(t.v[0].x + t.v[1].x + t.v[2].x) * kThird, (t.v[0].y + t.v[1].y + t.v[2].y) * kThird,
-                 (t.v[0].z + t.v[1].z + t.v[2].z) * kThird};
-      double r2 = 0.0;
-#pragma unroll
-      for (int k = 0; k < 3; ++k) {
-        const V3 d = t.v[k] - c;
-        r2 = fmax(r2, fma(d.x, d.x, fma(d.y, d.y, d.z * d.z)));
-      }
-      // unit face normal and plane offset for the separating-axis cull
-      const V3 e1{t.v[1].x - t.v[0].x, t.v[1].y - t.v[0].y, t.v[1].z - t.v[0].z};
-      const V3 e2{t.v[2].x - t.v[0].x, t.v[2].y - t.v[0].y, t.v[2].z - t.v[0].z};
-      const V3 nn{fma(e1.y, e2.z, -e1.z * e2.y), fma(e1.z, e2.x, -e1.x * e2.z), fma(e1.x, e2.y, -e1.y * e2.x)};
-      const double nl = sqrt(fma(nn.x, nn.x, fma(nn.y, nn.y, nn.z * nn.z)));
-      const double inv = nl > 0.0 ? 1.0 / nl : 0.0;
-      wr[16] = nn.x * inv;
-      wr[17] = nn.y * inv;
-      wr[18] = nn.z * inv;
-      wr[19] = fma(wr[16], t.v[0].x, fma(wr[17], t.v[0].y, wr[18] * t.v[0].z));
-      wr[12] = c.x;
-      wr[13] = c.y;
-      wr[14] = c.z;
-      // sliver flag from the body record; a zero-area triangle is never culled either
-      wr[15] = rad >= 0.0 && nl > 0.0 ? sqrt(r2) * (1.0 + 1e-12) : -1.0;
-      double2* sp = reinterpret_cast<double2*>(wsph + (size_t)w * kSph);
-      sp[0] = make_double2(c.x, c.y);
-      sp[1] = make_double2(c.z, wr[15] < 0.0 ? -1.0 : wr[15] + r[9]);
+    for (int k = 0; k < 3; ++k) {
+      wr[3 * k] = t.v[k].x;
+      wr[3 * k + 1] = t.v[k].y;
+      wr[3 * k + 2] = t.v[k].z;
     }
-    __syncthreads();
-    double2* dst = reinterpret_cast<double2*>(world + (size_t)w0 * kWorld);
-    const double2* so2 = reinterpret_cast<const double2*>(s_out);
-    for (int k = threadIdx.x; k < m * kWorld / 2; k += blockDim.x) dst[k] = so2[k];
-    __syncthreads();
+    wr[9] = r[9];
+    wr[10] = r[10];
+    {  // first child as an absolute world index (children are contiguous)
+      int lvl = 0;
+      while (lvl + 1 < B.n_levels && B.level_off[0] + j >= B.level_off[lvl + 1]) ++lvl;
+      int2 ch = *reinterpret_cast<const int2*>(r + 11);
+      if (lvl > 0) ch.x = (int32_t)(woff[b] + B.level_off[lvl - 1] - B.level_off[0] + ch.x);
+      *reinterpret_cast<int2*>(wr + 11) = ch;
+    }
+    // bounding sphere in world coordinates (approximate; the cull margin absorbs it)
+    constexpr double kThird = 1.0 / 3.0;
+    const V3 c{(t.v[0].x + t.v[1].x + t.v[2].x) * kThird, (t.v[0].y + t.v[1].y + t.v[2].y) * kThird,
+               (t.v[0].z + t.v[1].z + t.v[2].z) * kThird};
+    double r2 = 0.0;
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+      const V3 d = t.v[k] - c;
+      r2 = fmax(r2, fma(d.x, d.x, fma(d.y, d.y, d.z * d.z)));
+    }
+    // unit face normal and plane offset for the separating-axis cull
+    const V3 e1{t.v[1].x - t.v[0].x, t.v[1].y - t.v[0].y, t.v[1].z - t.v[0].z};
+    const V3 e2{t.v[2].x - t.v[0].x, t.v[2].y - t.v[0].y, t.v[2].z - t.v[0].z};
+    const V3 nn{fma(e1.y, e2.z, -e1.z * e2.y), fma(e1.z, e2.x, -e1.x * e2.z), fma(e1.x, e2.y, -e1.y * e2.x)};
+    const double nl = sqrt(fma(nn.x, nn.x, fma(nn.y, nn.y, nn.z * nn.z)));
+    const double inv = nl > 0.0 ? 1.0 / nl : 0.0;
+    wr[16] = nn.x * inv;
+    wr[17] = nn.y * inv;
+    wr[18] = nn.z * inv;
+    wr[19] = fma(wr[16], t.v[0].x, fma(wr[17], t.v[0].y, wr[18] * t.v[0].z));
+    wr[12] = c.x;
+    wr[13] = c.y;
+    wr[14] = c.z;
+    // sliver flag from the body record; a zero-area triangle is never culled either
+    wr[15] = r[15] >= 0.0 && nl > 0.0 ? sqrt(r2) * (1.0 + 1e-12) : -1.0;
+    double2* dst = reinterpret_cast<double2*>(world + (size_t)w * kWorld);
+#pragma unroll
+    for (int k = 0; k < kWorld / 2; ++k) dst[k] = make_double2(wr[2 * k], wr[2 * k + 1]);
+    double2* sp = reinterpret_cast<double2*>(wsph + (size_t)w * kSph);
+    sp[0] = make_double2(c.x, c.y);
+    sp[1] = make_double2(c.z, wr[15] < 0.0 ? -1.0 : wr[15] + r[9]);
   }
 }
 
@@ -2101,7 +2083,7 @@ static int run_search(const ltsg_scene* sc, ltsg_result* out, ltsg_workspace* ws
     } else {
       LTSG_TRY(ws_get(ws, "world", (size_t)std::max<int64_t>(n_world, 1) * (kWorld + kSph), &world));
       wsph = world + (size_t)std::max<int64_t>(n_world, 1) * kWorld;
-      k_world_fill<<<(int)std::max<int64_t>(1, std::min<int64_t>((n_world + 127) / 128, 148 * 12)), 128, 0, st>>>(
+      k_world_fill<<<(int)std::max<int64_t>(1, std::min<int64_t>((n_world + 127) / 128, 148 * 16)), 128, 0, st>>>(
           pr.bodies, sc->n_bodies, woff, sc->tris, world, wsph);
       LTSG_LAUNCHED();
     }
@@ -2546,7 +2528,7 @@ static int build_world(const ltsg_scene* sc, const Prepared& pr, ltsg_workspace*
     return LTSG_OK;
   }
   LTSG_TRY(ws_get(ws, "world", (size_t)std::max<int64_t>(*n_world, 1) * (kWorld + kSph), world));
-  k_world_fill<<<(int)std::max<int64_t>(1, std::min<int64_t>((*n_world + 127) / 128, 148 * 12)), 128, 0, st>>>(
+  k_world_fill<<<(int)std::max<int64_t>(1, std::min<int64_t>((*n_world + 127) / 128, 148 * 16)), 128, 0, st>>>(
       pr.bodies, sc->n_bodies, *woff,
                                                                               sc->tris, *world,
                                                                               *world + (size_t)std::max<int64_t>(*n_world, 1) * kWorld);
