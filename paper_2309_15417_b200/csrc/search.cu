@@ -1475,7 +1475,22 @@ __device__ __forceinline__ bool key_less(const Soa& o, int64_t a, int64_t b) {
 // the output order -- are identical.  Larger groups go to k_fuse_large.
 constexpr int kFuseCap = 256;
 constexpr int kFuseWords = kFuseCap / 32;
-constexpr int kFuseThreads = 128;
+constexpr int kFuseThreads = 256;
+
+// norm_blas(w) <= r, decided exactly: fl(sqrt(s)) <= r  <=>  s <= r*r up to a
+// few ulps, so the square root is only evaluated inside that band.
+// Outside it: s < fl(r*r)(1 - 2^-49) implies s < r^2, hence sqrt(s) < r;
+// s > fl(r*r)(1 + 2^-49) implies sqrt(s) > r (1 + 2^-52) >= r + ulp(r)/2,
+// which rounds above r.
+__device__ __forceinline__ bool norm_le(V3 w, double r) {
+  const double s = dot_blas(w, w);
+  const double p = r * r;
+  if (p > 1e-290 && p < 1e290) {
+    if (s < p * (1.0 - 0x1p-49)) return true;
+    if (s > p * (1.0 + 0x1p-49)) return false;
+  }
+  return __dsqrt_rn(s) <= r;
+}
 
 struct FuseKey {
   double t, r0, r1, r2;
@@ -1491,7 +1506,7 @@ __device__ __forceinline__ bool fkey_less(const FuseKey& a, const FuseKey& b) {
   return a.tb < b.tb;
 }
 
-__global__ void __launch_bounds__(kFuseThreads)
+__global__ void __launch_bounds__(kFuseThreads, 4)
 k_fuse_block(Soa o, int64_t* __restrict__ idx, const int64_t* __restrict__ g_off, int64_t n_groups,
              int64_t n_total, Soa f, int64_t* g_fused, int32_t* prob_count, int32_t* big_list,
              int32_t* big_count) {
@@ -1562,7 +1577,7 @@ k_fuse_block(Soa o, int64_t* __restrict__ idx, const int64_t* __restrict__ g_off
         const int j = word * 32 + b;
         if (j <= row || j >= n) continue;
         const V3 pj{s_p[0][j], s_p[1][j], s_p[2][j]};
-        if (norm_blas(pi - pj) <= fmax(ti, s_thr[j])) bits |= 1u << b;
+        if (norm_le(pi - pj, fmax(ti, s_thr[j]))) bits |= 1u << b;
       }
       s_adj[row * kFuseWords + word] = bits;
     }
@@ -1727,7 +1742,7 @@ k_fuse_large(Soa o, int64_t* __restrict__ idx, const int64_t* __restrict__ g_off
       const int j = word * 32 + b;
       if (j <= row || j >= n) continue;
       const V3 pj{px[3 * j], px[3 * j + 1], px[3 * j + 2]};
-      if (norm_blas(pi - pj) <= fmax(ti, th[j])) bits |= 1u << b;
+      if (norm_le(pi - pj, fmax(ti, th[j]))) bits |= 1u << b;
     }
     adj[(int64_t)row * words + word] = bits;
   }
