@@ -14,7 +14,8 @@ scenes (no dataset exists for this path).  Rank 0 prints ONE JSON line.
   e2e      the same metric through the public batched API
            (`ccd.earliest_contacts`) from host bodies: packing, H2D copies,
            the search and the D2H copy of every result inside the timed region
-  roofline the dominant kernel (k_screen): 984 FP64 flops per test over its
+  roofline the exact-distance kernel (k_screen_static for static batches,
+           k_screen for moving ones): 984 FP64 flops per exact row over its
            CUDA-event time, against the FP64 DFMA peak measured in this run
   cpu_baseline  the CPU oracle (numpy restatement of the reference) on a
            bounded sample of the same workload, on this host's cores
@@ -78,6 +79,21 @@ def scene_problems(scene):
         probs.append(([(scene.body(scene.pairs[i][0]), scene.body(scene.pairs[i][1])) for i in sel],
                       float(scene.dt[p]), float(scene.t_base[p])))
     return probs
+
+
+def committed_traffic(config: str, kernel: str) -> dict:
+    """DRAM bytes of the dominant kernel from the newest committed ncu summary
+    (profiles/rNN_traffic_<config>.json, written by tools/traffic.py)."""
+    import glob
+
+    for path in sorted(glob.glob(os.path.join(REPO, "profiles", f"r*_traffic_{config}.json")), reverse=True):
+        try:
+            d = json.load(open(path))
+        except (OSError, ValueError):
+            continue
+        if d.get("kernel") == kernel:
+            return d
+    return {}
 
 
 # ------------------------------------------------------------------ clocks
@@ -338,6 +354,8 @@ def run_ours(args, rank, world, local_rank):
     screen_ms = sum(s.get("ms_screen", 0.0) for s in stats)
     screen_rows = sum(s["rows_screen"] for s in stats)
     exact_rows = sum(s.get("rows_screen_exact", s["rows_screen"]) for s in stats)
+    exact_ms = sum(s.get("ms_exact", 0.0) for s in stats)
+    expand_ms = sum(s.get("ms_expand", 0.0) for s in stats)
     launches = sum(s.get("launches", 0) for s in stats)
 
     # ---- end to end through the public API from host bodies
@@ -380,7 +398,11 @@ def run_ours(args, rank, world, local_rank):
     if rank == 0:
         value = tests_all / (total_ms * 1e-3)
         # flops of the rows that actually ran the exact 15-feature distance
-        achieved = exact_rows * FLOPS_PER_TEST / (screen_ms * 1e-3) / 1e12 if screen_ms > 0 else 0.0
+        # static batches time the exact kernel alone; moving batches run the
+        # culls and the exact distance in one kernel (k_screen)
+        kern_ms = exact_ms if exact_ms > 0 else screen_ms
+        traffic = committed_traffic(args.config, "k_screen_static" if exact_ms > 0 else "k_screen")
+        achieved = exact_rows * FLOPS_PER_TEST / (kern_ms * 1e-3) / 1e12 if kern_ms > 0 else 0.0
         line = {
             "metric": METRIC, "value": value, "unit": "tests/s", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": total_ms / args.steps,
@@ -400,18 +422,25 @@ def run_ours(args, rank, world, local_rank):
                     "ms_per_step": e2e_total / args.steps,
                     "path": "ccd.earliest_contacts(host bodies) -> pack -> H2D -> ltsg_search -> D2H",
                     "phases_ms_per_step": {k: sum(v) / len(v) for k, v in phases.items()}},
-            "roofline": {"bound": "fp64", "kernel": "k_screen", "achieved": achieved,
+            "roofline": {"bound": "fp64", "kernel": "k_screen_static" if exact_ms > 0 else "k_screen",
+                         "achieved": achieved,
                          "peak": peak_tflops.value, "unit": "TFLOP/s",
                          "frac": achieved / peak_tflops.value if peak_tflops.value else None,
-                         "traffic": None,
+                         "traffic": traffic.get("dram_bytes_per_step"),
+                         "traffic_unit": "DRAM bytes per step (sum over the kernel's launches of one search)",
+                         "traffic_source": traffic.get("source"),
                          "peak_source": "in-run DFMA microbenchmark (ltsg_fp64_peak); "
                                         "MEASURED_PEAKS.json has no FP64 entry",
                          "flops_per_test": FLOPS_PER_TEST,
+                         "kernel_ms_per_step": kern_ms / args.steps,
                          "screen_ms_per_step": screen_ms / args.steps,
+                         "expand_ms_per_step": expand_ms / args.steps,
                          "screen_rows_per_step": screen_rows / args.steps,
                          "screen_rows_exact_per_step": exact_rows / args.steps,
-                         "note": "rows settled by the certified sphere cull are counted as tests in "
-                                 "`value` (their decision is identical) but not in `achieved`"},
+                         "note": "rows settled by the certified culls (sphere, separating axes) are "
+                                 "counted as tests in `value` (their decision is identical) but not in "
+                                 "`achieved`; screen_ms also covers the seeds and the child expansion "
+                                 "with its culls (expand_ms)"},
             "roofline_distance_kernel": allpairs,
             "gpu_launches": launches,
             "breakdown_ms_per_step": {

@@ -192,7 +192,9 @@ typedef struct {
   double ms_refine;       /* zoom + bisection */
   double ms_contacts;     /* records, contacts, fusion */
   int64_t rows_screen_exact; /* screen rows that ran the exact 15-feature distance
-                                (the rest were settled by the certified sphere cull) */
+                                (the rest were settled by the certified culls) */
+  double ms_exact;        /* static batches: device time of the exact-distance kernel alone */
+  double ms_expand;       /* static batches: device time of the child expansion + culls */
 } ltsg_result;
 
 typedef struct ltsg_workspace ltsg_workspace;

@@ -221,7 +221,8 @@ class DeviceResult:
         stats = {k: int(getattr(st, k)) for k in (
             "rows_screen", "rows_zoom", "rows_bisect", "rows_executed", "candidates",
             "generations", "n_raw", "n_fused", "launches", "rows_screen_exact")}
-        stats.update({k: float(getattr(st, k)) for k in ("ms_screen", "ms_refine", "ms_contacts")})
+        stats.update({k: float(getattr(st, k)) for k in ("ms_screen", "ms_refine", "ms_contacts", "ms_exact",
+                                                           "ms_expand")})
         return BatchResult(dt=dt.numpy(), collision=coll.numpy() != 0, first_contact=first.numpy(),
                            fused_offset=off.numpy(), contacts={k: v.numpy() for k, v in fused.items()},
                            raw={k: v.numpy() for k, v in raw.items()} if raw is not None else None, stats=stats)

@@ -8,6 +8,7 @@
 #include <cstdio>
 #include <string>
 #include <unordered_map>
+#include <vector>
 
 #include "../../include/ltsgpu.h"
 
@@ -59,7 +60,18 @@ struct ltsg_workspace {
   int device = 0;
   // sizes seen by earlier calls: the async traversal preallocates from them
   size_t hint_front = 0, hint_rest = 0, hint_entries = 0, hint_cross = 0, hint_seed = 0;
+  int hint_gens = 0;  // deepest traversal seen: async mode launches one generation more
 
   int get(const char* name, size_t bytes, void** out, bool keep = false);
+  // CUDA events for per-kernel timing, created on first use and reused
+  std::vector<cudaEvent_t> events;
+  cudaEvent_t event(size_t i) {
+    while (events.size() <= i) {
+      cudaEvent_t e = nullptr;
+      cudaEventCreate(&e);
+      events.push_back(e);
+    }
+    return events[i];
+  }
   ~ltsg_workspace();
 };

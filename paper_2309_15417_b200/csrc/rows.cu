@@ -271,4 +271,6 @@ int ltsg_workspace::get(const char* name, size_t bytes, void** out, bool keep) {
 ltsg_workspace::~ltsg_workspace() {
   for (auto& kv : bufs)
     if (kv.second.ptr) cudaFree(kv.second.ptr);
+  for (auto e : events)
+    if (e) cudaEventDestroy(e);
 }

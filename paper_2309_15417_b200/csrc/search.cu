@@ -2052,6 +2052,7 @@ static int run_search(const ltsg_scene* sc, ltsg_result* out, ltsg_workspace* ws
   out->launches = 0;
   out->ms_screen = out->ms_refine = out->ms_contacts = 0.0;
   out->rows_screen_exact = 0;
+  out->ms_exact = out->ms_expand = 0.0;
   if (np == 0) return LTSG_OK;
 
   Trace tr(st);
@@ -2154,6 +2155,19 @@ static int run_search(const ltsg_scene* sc, ltsg_result* out, ltsg_workspace* ws
   Counters h{};
   Cand* front = nullptr;
 
+  size_t n_timed = 0;  // static generations timed with event triples (exact, expand)
+  auto static_times = [&]() -> int {  // call once the stream has passed every recorded event
+    out->ms_exact = out->ms_expand = 0.0;
+    for (size_t g = 0; g < n_timed; ++g) {
+      float a = 0.f, b = 0.f;
+      LTSG_CUDA(cudaEventSynchronize(ws->event(3 * g + 2)));
+      LTSG_CUDA(cudaEventElapsedTime(&a, ws->event(3 * g), ws->event(3 * g + 1)));
+      LTSG_CUDA(cudaEventElapsedTime(&b, ws->event(3 * g + 1), ws->event(3 * g + 2)));
+      out->ms_exact += a;
+      out->ms_expand += b;
+    }
+    return LTSG_OK;
+  };
   auto launch_screen = [&](const Cand* in, int64_t n, const unsigned long long* n_in, Cand* next,
                            unsigned long long cap, unsigned long long* n_out, Cand* xbuf,
                            unsigned long long* xcnt) -> int {
@@ -2162,12 +2176,18 @@ static int run_search(const ltsg_scene* sc, ltsg_result* out, ltsg_workspace* ws
       // exact pass of the frontier (parents into xbuf, count in xcnt), then
       // the culled expansion of the parents into the next frontier
       const int64_t blocks = n_in ? 148LL * 20 : (n + 32 * kStaticWarps - 1) / (32 * kStaticWarps);
+      const size_t e = 3 * n_timed++;
+      LTSG_CUDA(cudaEventRecord(ws->event(e), st));
       k_screen_static<<<(int)std::max<int64_t>(1, std::min<int64_t>(blocks, 148LL * 20)), 32 * kStaticWarps,
                         kStaticStageBytes, st>>>(in, n, pr.pairs, pr.bodies, world, woff, so,
                                                  reinterpret_cast<Parent*>(xbuf), xcnt);
       LTSG_LAUNCHED();
+      LTSG_CUDA(cudaEventRecord(ws->event(e + 1), st));
       k_expand_filter<<<148 * 8, kExpThreads, 0, st>>>(reinterpret_cast<const Parent*>(xbuf), xcnt, cap, (int)fan,
                                                        world, wsph, next, cap, n_out, d_ctr);
+      LTSG_LAUNCHED();
+      LTSG_CUDA(cudaEventRecord(ws->event(e + 2), st));
+      return LTSG_OK;
     } else {
       const int grid = n_in ? 148 * 32 : screen_grid(n);
       k_screen<<<grid, 32 * kScreenWarps, kScreenStageBytes, st>>>(in, n, pr.pairs, pr.bodies, sc->tris, so,
@@ -2179,6 +2199,7 @@ static int run_search(const ltsg_scene* sc, ltsg_result* out, ltsg_workspace* ws
 
   auto traverse = [&](bool async_mode, bool* overflow) -> int {
     *overflow = false;
+    n_timed = 0;
     LTSG_CUDA(cudaMemsetAsync(d_ctr, 0, sizeof(Counters), st));
     LTSG_CUDA(cudaMemsetAsync(gen_cnt, 0, sizeof(unsigned long long) * (kMaxGen + 1), st));
     LTSG_CUDA(cudaMemsetAsync(x_cnt, 0, sizeof(unsigned long long) * (kMaxGen + 1), st));
@@ -2212,7 +2233,10 @@ static int run_search(const ltsg_scene* sc, ltsg_result* out, ltsg_workspace* ws
       LTSG_TRY(ws_get(ws, "front1", cap_async, &buf[1]));
       Cand* xbuf = nullptr;
       if (all_static) LTSG_TRY(ws_get(ws, "frontx", cap_async, &xbuf));
-      for (int g = 1; g <= kMaxGen; ++g)
+      // one generation more than the deepest traversal seen: a non-empty
+      // frontier after the last one means the budget was short (re-run sync)
+      const int n_gen = std::min(kMaxGen, std::max(1, ws->hint_gens) + 1);
+      for (int g = 1; g <= n_gen; ++g)
         LTSG_TRY(launch_screen(buf[(g - 1) & 1], 0, gen_cnt + g - 1, buf[g & 1], cap_async, gen_cnt + g, xbuf,
                                x_cnt + g));
       t_screen.stop(st);
@@ -2228,7 +2252,7 @@ static int run_search(const ltsg_scene* sc, ltsg_result* out, ltsg_workspace* ws
           out->generations += 1;
         }
       }
-      if (hg[kMaxGen] > 0) *overflow = true;  // deeper than the generation budget
+      if (hg[n_gen] > 0) *overflow = true;  // deeper than the generation budget
       if (h.resting > rest_cap || h.entries > entry_cap || h.cross > cross_cap) *overflow = true;
       return LTSG_OK;
     }
@@ -2259,7 +2283,9 @@ static int run_search(const ltsg_scene* sc, ltsg_result* out, ltsg_workspace* ws
       Cand* xbuf = nullptr;
       if (all_static) LTSG_TRY(ws_get(ws, "frontx", (size_t)n_front, &xbuf));
       Counters before = h;
+      const size_t timed_before = n_timed;
       for (;;) {
+        n_timed = timed_before;  // a retried generation replaces its timing
         LTSG_CUDA(cudaMemcpyAsync(d_ctr, &before, sizeof(Counters), cudaMemcpyHostToDevice, st));
         LTSG_CUDA(cudaMemsetAsync(gen_cnt + 1, 0, sizeof(unsigned long long), st));
         LTSG_CUDA(cudaMemsetAsync(x_cnt, 0, sizeof(unsigned long long), st));
@@ -2298,6 +2324,7 @@ static int run_search(const ltsg_scene* sc, ltsg_result* out, ltsg_workspace* ws
       front = next;
     }
     ws->hint_front = std::max(ws->hint_front, max_front);
+    ws->hint_gens = std::max(ws->hint_gens, (int)out->generations);
     return LTSG_OK;
   };
 
@@ -2310,6 +2337,7 @@ static int run_search(const ltsg_scene* sc, ltsg_result* out, ltsg_workspace* ws
     cross_cap = std::max(cross_cap, (size_t)h.cross * 2);
     LTSG_TRY(traverse(false, &overflow));
   }
+  if (all_static) LTSG_TRY(static_times());
   ws->hint_rest = std::max(ws->hint_rest, (size_t)h.resting);
   ws->hint_entries = std::max(ws->hint_entries, (size_t)h.entries);
   ws->hint_cross = std::max(ws->hint_cross, (size_t)h.cross);
