@@ -224,6 +224,15 @@ int ltsg_fuse_contacts(ltsg_result* io, int64_t n_raw, const uint64_t* group_key
 int ltsg_exhaustive_rows(const ltsg_scene* scene, int64_t* rows, int64_t* hits, double* ms,
                          ltsg_workspace* ws, void* stream);
 
+/* The same rows with every distance written out: out_dist (device, float64)
+ * receives, pair after pair, the na x nb fine rows of each pair row-major in
+ * world-record order (record i of body a, record j of body b; tri_orig maps
+ * records to reference triangle indices).  Each value is
+ * ccd._feature_distances (ccd.py:135-153) of that row at tau = 0.  *rows
+ * receives the total row count.  Parity/validation entry point. */
+int ltsg_exhaustive_distances(const ltsg_scene* scene, double* out_dist, int64_t* rows,
+                              ltsg_workspace* ws, void* stream);
+
 /* FP64 pipe microbenchmark: independent DFMA chains on every SM; reports
  * the achieved FP64 FLOP/s (2 per DFMA) -- the roofline denominator. */
 int ltsg_fp64_peak(double* tflops, double* ms, void* stream);

@@ -92,6 +92,7 @@ def lib():
             "ltsg_overlap_centroid": [P, P, P, I64, P, P, P],
             "ltsg_search": [C.POINTER(Scene), C.POINTER(Result), P, P],
             "ltsg_exhaustive_rows": [C.POINTER(Scene), C.POINTER(I64), C.POINTER(I64), C.POINTER(F64), P, P],
+            "ltsg_exhaustive_distances": [C.POINTER(Scene), P, C.POINTER(I64), P, P],
             "ltsg_fuse_contacts": [C.POINTER(Result), I64, P, P, P],
             "ltsg_fp64_peak": [C.POINTER(F64), C.POINTER(F64), P],
             "ltsg_unpack_trees": [C.POINTER(TreeUpload), P, P],
@@ -113,7 +114,7 @@ EXPORTED = (
     "ltsg_last_error", "ltsg_version", "ltsg_point_triangle_closest",
     "ltsg_segment_segment_closest", "ltsg_feature_distances", "ltsg_closest_feature",
     "ltsg_overlap_centroid", "ltsg_workspace_create", "ltsg_workspace_destroy",
-    "ltsg_workspace_bytes", "ltsg_search", "ltsg_exhaustive_rows", "ltsg_fuse_contacts", "ltsg_fp64_peak",
+    "ltsg_workspace_bytes", "ltsg_search", "ltsg_exhaustive_rows", "ltsg_exhaustive_distances", "ltsg_fuse_contacts", "ltsg_fp64_peak",
     "ltsg_unpack_trees",
 )
 

@@ -18,6 +18,7 @@
 #include "common.cuh"
 #include "geom.cuh"
 #include "dist_staged.cuh"
+#include "dist_tile.cuh"
 
 #include <cub/cub.cuh>
 
@@ -1894,6 +1895,79 @@ k_allpairs(const PairInfo* __restrict__ pairs, int64_t n_pairs, const BodyInfo* 
   if ((threadIdx.x & 31) == 0 && local) atomicAdd(hits, local);
 }
 
+// Exhaustive fine x fine rows as register x broadcast tiles (the roofline
+// kernel; ccd._search with exhaustive=True evaluates the same rows,
+// ccd.py:385-391).  A work item is (pair, tile of kTileA fine triangles of
+// body a, tile of kTileB fine triangles of body b).  Each lane holds one A
+// triangle with its per-triangle constants in registers; the B tile is
+// staged once in shared memory and every lane of a warp walks it in the
+// same order, so each B operand is one broadcast load.  Work items are
+// distributed over a persistent grid from a per-pair prefix of item counts.
+constexpr int kTileA = 128;
+constexpr int kTileB = 32;
+#ifndef LTSG_TILE_MINB
+#define LTSG_TILE_MINB 5
+#endif
+
+#ifndef LTSG_TILE_ASMEM
+#define LTSG_TILE_ASMEM 1
+#endif
+constexpr int kTileSmemBytes = (kTileB * kTilePre + (LTSG_TILE_ASMEM ? kTileA * kTilePre : 0)) * 8;
+
+__global__ void __launch_bounds__(kTileA, LTSG_TILE_MINB)
+k_allpairs_tile(const PairInfo* __restrict__ pairs, int64_t n_pairs, const BodyInfo* __restrict__ bodies,
+                const double* __restrict__ world, const int64_t* __restrict__ woff,
+                const int64_t* __restrict__ item_start, const int64_t* __restrict__ row_start,
+                unsigned long long* hits, double* __restrict__ out_dist) {
+  extern __shared__ __align__(16) double s_tile[];
+  double* sB = s_tile;                       // [kTileB][kTilePre], broadcast reads
+  double* sA = s_tile + kTileB * kTilePre;   // [kTilePre][kTileA], one column per lane
+  unsigned long long local = 0;
+  const int64_t n_items = item_start[n_pairs];
+  for (int64_t item = blockIdx.x; item < n_items; item += gridDim.x) {
+    int64_t lo = 0, hi = n_pairs;  // last pair k with item_start[k] <= item
+    while (hi - lo > 1) {
+      const int64_t mid = (lo + hi) >> 1;
+      if (__ldg(item_start + mid) <= item) lo = mid; else hi = mid;
+    }
+    const PairInfo p = pairs[lo];
+    const int na = bodies[p.ba].level_size[0], nb = bodies[p.bb].level_size[0];
+    const int tiles_b = (nb + kTileB - 1) / kTileB;
+    const int64_t local_item = item - item_start[lo];
+    const int ta = (int)(local_item / tiles_b), tb = (int)(local_item - (int64_t)ta * tiles_b);
+    const int jb0 = tb * kTileB, nbt = min(kTileB, nb - jb0);
+    __syncthreads();  // the previous item's tiles are no longer read
+    if (threadIdx.x < nbt) {
+      const double* wb = world + (size_t)(woff[p.bb] + jb0 + threadIdx.x) * kWorld;
+      tri_store(sB + threadIdx.x * kTilePre, tri_reg(load_world(wb), __ldg(wb + 9)));
+    }
+    const int i = ta * kTileA + threadIdx.x;
+    const bool valid = i < na;
+    const double* wa = world + (size_t)(woff[p.ba] + (valid ? i : na - 1)) * kWorld;
+#if LTSG_TILE_ASMEM
+    const double eps_a = __ldg(wa + 9);
+    tri_store_soa<kTileA>(sA + threadIdx.x, tri_reg(load_world(wa), eps_a));
+    __syncthreads();
+    const SmemTri<kTileA> A{sA + threadIdx.x};
+#else
+    __syncthreads();
+    const TriReg AR = tri_reg(load_world(wa), __ldg(wa + 9));
+    const double eps_a = AR.eps;
+    const RegA A{AR};
+#endif
+    double* od = out_dist ? out_dist + row_start[lo] + (int64_t)(valid ? i : 0) * nb + jb0 : nullptr;
+#pragma unroll 1
+    for (int j = 0; j < nbt; ++j) {
+      const double* t = sB + j * kTilePre;
+      const double d = __dsqrt_rn(tile_dist_sq(A, t));
+      if (valid && d <= add(add(eps_a, t[kTpEps]), kRestSlop)) ++local;
+      if (od && valid) od[j] = d;
+    }
+  }
+  for (int o = 16; o > 0; o >>= 1) local += __shfl_down_sync(0xffffffffu, local, o);
+  if ((threadIdx.x & 31) == 0 && local) atomicAdd(hits, local);
+}
+
 // ---------------------------------------------------------------- host side
 
 template <typename T>
@@ -1928,6 +2002,7 @@ static int configure_kernels() {
     LTSG_CUDA(cudaFuncSetAttribute(k_screen_static, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                    kStaticStageBytes));
     LTSG_CUDA(cudaFuncSetAttribute(k_allpairs, cudaFuncAttributeMaxDynamicSharedMemorySize, kStaticStageBytes));
+    LTSG_CUDA(cudaFuncSetAttribute(k_allpairs_tile, cudaFuncAttributeMaxDynamicSharedMemorySize, kTileSmemBytes));
     done = 1;
   }
   return LTSG_OK;
@@ -2580,8 +2655,8 @@ static int build_world(const ltsg_scene* sc, const Prepared& pr, ltsg_workspace*
   return LTSG_OK;
 }
 
-static int run_allpairs(const ltsg_scene* sc, int64_t* rows, int64_t* hits, double* ms, ltsg_workspace* ws,
-                        cudaStream_t st) {
+static int run_allpairs(const ltsg_scene* sc, int64_t* rows, int64_t* hits, double* ms, double* out_dist,
+                        ltsg_workspace* ws, cudaStream_t st) {
   LTSG_TRY(validate(sc));
   LTSG_TRY(configure_kernels());
   Prepared pr{};
@@ -2608,11 +2683,30 @@ static int run_allpairs(const ltsg_scene* sc, int64_t* rows, int64_t* hits, doub
     LTSG_CUDA(cudaMemcpyAsync(pb.data(), sc->pair_body, sizeof(int32_t) * pb.size(), cudaMemcpyDeviceToHost, st));
     LTSG_CUDA(cudaStreamSynchronize(st));
     for (int64_t k = 0; k < sc->n_pairs; ++k) *rows += lev[(size_t)pb[2 * k] * 18 + 10] * lev[(size_t)pb[2 * k + 1] * 18 + 10];
+    // per-pair prefixes of tile items and of rows (row-major na x nb per pair)
+    std::vector<int64_t> items((size_t)sc->n_pairs + 1, 0), rowv((size_t)sc->n_pairs + 1, 0);
+    for (int64_t k = 0; k < sc->n_pairs; ++k) {
+      const int64_t na = lev[(size_t)pb[2 * k] * 18 + 10], nb = lev[(size_t)pb[2 * k + 1] * 18 + 10];
+      items[k + 1] = items[k] + ((na + kTileA - 1) / kTileA) * ((nb + kTileB - 1) / kTileB);
+      rowv[k + 1] = rowv[k] + na * nb;
+    }
+    int64_t *d_items, *d_rows;
+    LTSG_TRY(ws_get(ws, "tile_items", items.size(), &d_items));
+    LTSG_TRY(ws_get(ws, "tile_rows", rowv.size(), &d_rows));
+    LTSG_CUDA(cudaMemcpyAsync(d_items, items.data(), sizeof(int64_t) * items.size(), cudaMemcpyHostToDevice, st));
+    LTSG_CUDA(cudaMemcpyAsync(d_rows, rowv.data(), sizeof(int64_t) * rowv.size(), cudaMemcpyHostToDevice, st));
+    const char* legacy = getenv("LTSG_ALLPAIRS_STAGED");
     Timer t;
-    dim3 grid(148 * 8, (unsigned)std::min<int64_t>(sc->n_pairs, 65535));
     t.start(st);
-    k_allpairs<<<grid, 32 * kStaticWarps, kStaticStageBytes, st>>>(pr.pairs, sc->n_pairs, pr.bodies, world, woff,
-                                                                   d_hits);
+    if (legacy && legacy[0] == '1' && !out_dist) {
+      dim3 grid(148 * 8, (unsigned)std::min<int64_t>(sc->n_pairs, 65535));
+      k_allpairs<<<grid, 32 * kStaticWarps, kStaticStageBytes, st>>>(pr.pairs, sc->n_pairs, pr.bodies, world, woff,
+                                                                     d_hits);
+    } else {
+      const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(items.back(), 148LL * LTSG_TILE_MINB * 8));
+      k_allpairs_tile<<<grid, kTileA, kTileSmemBytes, st>>>(pr.pairs, sc->n_pairs, pr.bodies, world, woff, d_items, d_rows,
+                                               d_hits, out_dist);
+    }
     t.stop(st);
     LTSG_CHECK_LAUNCH();
     *ms = t.ms();
@@ -2683,5 +2777,16 @@ extern "C" int ltsg_exhaustive_rows(const ltsg_scene* scene, int64_t* rows, int6
     ltsg::set_error("ltsg_exhaustive_rows: null argument");
     return LTSG_EINVAL;
   }
-  return ltsg::run_allpairs(scene, rows, hits, ms, ws, (cudaStream_t)stream);
+  return ltsg::run_allpairs(scene, rows, hits, ms, nullptr, ws, (cudaStream_t)stream);
+}
+
+extern "C" int ltsg_exhaustive_distances(const ltsg_scene* scene, double* out_dist, int64_t* rows,
+                                         ltsg_workspace* ws, void* stream) {
+  if (!scene || !out_dist || !rows || !ws) {
+    ltsg::set_error("ltsg_exhaustive_distances: null argument");
+    return LTSG_EINVAL;
+  }
+  int64_t hits = 0;
+  double ms = 0.0;
+  return ltsg::run_allpairs(scene, rows, &hits, &ms, out_dist, ws, (cudaStream_t)stream);
 }
