@@ -318,7 +318,7 @@ def run_ours(args, rank, world, local_rank):
                                                        C.c_void_p(torch.cuda.current_stream().cuda_stream)),
                        "ltsg_exhaustive_rows")
         ach = rows_c.value * FLOPS_PER_TEST / (ms_c.value * 1e-3) / 1e12
-        allpairs = {"kernel": "k_allpairs", "pairs": len(sub), "rows": rows_c.value, "hits": hits_c.value,
+        allpairs = {"kernel": "k_allpairs_tile", "pairs": len(sub), "rows": rows_c.value, "hits": hits_c.value,
                     "ms": ms_c.value, "tests_per_s": rows_c.value / (ms_c.value * 1e-3),
                     "achieved_tflops": ach, "frac": ach / peak_tflops.value}
         del ds_sub
