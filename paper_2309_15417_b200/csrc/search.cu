@@ -91,6 +91,8 @@ struct Counters {
   unsigned long long records;
   unsigned long long overflow;   // zoom queue overflow flag
   unsigned long long screen_exact;  // screen rows evaluated with the exact 15-feature distance
+  unsigned long long rows_window;   // moving screen: rows inside the candidates' cull windows
+  unsigned long long rows_sphere;   // moving screen: rows surviving the per-row sphere cull
 };
 
 // ---------------------------------------------------------------- prep
@@ -516,7 +518,7 @@ k_screen(const Cand* __restrict__ front, int64_t n, const PairInfo* __restrict__
   ChildInfo* kid = s_u[warp].child;
   uint8_t* bits = s_bits[warp];
   int16_t* queue = s_queue[warp];
-  unsigned long long acc_rows = 0, acc_exact = 0;
+  unsigned long long acc_rows = 0, acc_exact = 0, acc_window = 0, acc_sphere = 0;
 
   for (int64_t wi = blockIdx.x * (int64_t)kScreenWarps + warp; wi < n_warps;
        wi += (int64_t)gridDim.x * kScreenWarps) {
@@ -624,6 +626,7 @@ k_screen(const Cand* __restrict__ front, int64_t n, const PairInfo* __restrict__
       nq += __popc(m);
     }
     __syncwarp();
+    const int nq_sphere = nq;
     // (b1) separating-axis cull of the sphere survivors, densely; survivors
     // are compacted in place (a chunk is read before any lane writes)
     {
@@ -738,6 +741,8 @@ k_screen(const Cand* __restrict__ front, int64_t n, const PairInfo* __restrict__
     unsigned long long cbase = 0;
     acc_rows += (unsigned long long)all_rows;  // warp-uniform; flushed once per warp
     acc_exact += (unsigned long long)nq;
+    acc_window += (unsigned long long)total;
+    acc_sphere += (unsigned long long)nq_sphere;
     if (lane == 0 && ctotal) cbase = atomicAdd(out.n_out, (unsigned long long)ctotal);
     cbase = __shfl_sync(0xffffffffu, cbase, 0);
     if (ctotal) {
@@ -770,6 +775,8 @@ k_screen(const Cand* __restrict__ front, int64_t n, const PairInfo* __restrict__
   if (lane == 0) {
     if (acc_rows) atomicAdd(&out.ctr->rows, acc_rows);
     if (acc_exact) atomicAdd(&out.ctr->screen_exact, acc_exact);
+    if (acc_window) atomicAdd(&out.ctr->rows_window, acc_window);
+    if (acc_sphere) atomicAdd(&out.ctr->rows_sphere, acc_sphere);
   }
 }
 
@@ -968,7 +975,11 @@ __device__ __forceinline__ bool sat_cull(const double* wa, const double* wb, dou
 }
 
 constexpr int kStaticWarps = 4;
-constexpr int kStaticStageBytes = kStaged * 32 * kStaticWarps * sizeof(double);
+#ifndef LTSG_STATIC_LITE
+#define LTSG_STATIC_LITE 0
+#endif
+constexpr int kStaticStageBytes = (LTSG_STATIC_LITE ? kStagedLite : kStaged) * 32 * kStaticWarps * sizeof(double);
+constexpr int kAllpairsStageBytes = kStaged * 32 * kStaticWarps * sizeof(double);
 #ifndef LTSG_STATIC_MINB
 #define LTSG_STATIC_MINB 5
 #endif
@@ -1079,8 +1090,13 @@ k_screen_static(const Cand* __restrict__ front, int64_t n, const PairInfo* __res
       const double* wa = world + (size_t)c.ia * kWorld;
       const double* wb = world + (size_t)c.ib * kWorld;
       const double h = add(__ldg(wa + 9), __ldg(wb + 9));
+#if LTSG_STATIC_LITE
+      stage_pair_lite(st, load_world(wa), load_world(wb));
+      const double d = __dsqrt_rn(staged_dist_sq_lite(st));
+#else
       stage_pair(st, load_world(wa), load_world(wb));
       const double d = __dsqrt_rn(staged_dist_sq(st));
+#endif
       if (c.la == 0 && c.lb == 0) {
         if (d <= add(h, kRestSlop)) {
           const PairInfo p = pairs[c.pair];
@@ -2004,7 +2020,7 @@ static int configure_kernels() {
     LTSG_CUDA(cudaFuncSetAttribute(k_screen, cudaFuncAttributeMaxDynamicSharedMemorySize, kScreenStageBytes));
     LTSG_CUDA(cudaFuncSetAttribute(k_screen_static, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                    kStaticStageBytes));
-    LTSG_CUDA(cudaFuncSetAttribute(k_allpairs, cudaFuncAttributeMaxDynamicSharedMemorySize, kStaticStageBytes));
+    LTSG_CUDA(cudaFuncSetAttribute(k_allpairs, cudaFuncAttributeMaxDynamicSharedMemorySize, kAllpairsStageBytes));
     LTSG_CUDA(cudaFuncSetAttribute(k_allpairs_tile, cudaFuncAttributeMaxDynamicSharedMemorySize, kTileSmemBytes));
     done = 1;
   }
@@ -2421,6 +2437,9 @@ static int run_search(const ltsg_scene* sc, ltsg_result* out, ltsg_workspace* ws
   ws->hint_cross = std::max(ws->hint_cross, (size_t)h.cross);
 
   tr.mark("traverse");
+  if (tr.on)
+    fprintf(stderr, "[ltsg trace] rows %llu window %llu sphere %llu exact %llu\n", h.rows, h.rows_window,
+            h.rows_sphere, h.screen_exact);
   // ---- certified zoom + bisection
   t_refine.start(st);
   const int64_t n_entries = (int64_t)h.entries;
@@ -2703,7 +2722,7 @@ static int run_allpairs(const ltsg_scene* sc, int64_t* rows, int64_t* hits, doub
     t.start(st);
     if (legacy && legacy[0] == '1' && !out_dist) {
       dim3 grid(148 * 8, (unsigned)std::min<int64_t>(sc->n_pairs, 65535));
-      k_allpairs<<<grid, 32 * kStaticWarps, kStaticStageBytes, st>>>(pr.pairs, sc->n_pairs, pr.bodies, world, woff,
+      k_allpairs<<<grid, 32 * kStaticWarps, kAllpairsStageBytes, st>>>(pr.pairs, sc->n_pairs, pr.bodies, world, woff,
                                                                      d_hits);
     } else {
       const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(items.back(), 148LL * LTSG_TILE_MINB * 8));

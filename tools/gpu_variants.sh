@@ -4,7 +4,7 @@ mkdir -p gpurun_out
 CFG=${1:-c1}
 for v in default variants/lib_*.so; do echo "== $v" >> gpurun_out/variants_summary.txt
   if [ "$v" = default ]; then unset LTSG_LIB; else export LTSG_LIB=$v; fi
-  timeout 600 python bench.py --config $CFG --steps 10 --warmup 3 --no-cpu --no-allpairs > gpurun_out/var.log 2>&1
+  timeout 600 python bench.py --config $CFG --steps ${STEPS:-10} --warmup 3 --no-cpu --no-allpairs ${EXTRA:-} > gpurun_out/var.log 2>&1
   python - "$v" <<'PY'
 import json,sys
 d=json.loads(open('gpurun_out/var.log').read().strip().splitlines()[-1])
