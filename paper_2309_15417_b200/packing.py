@@ -26,7 +26,7 @@ from __future__ import annotations
 import threading
 import weakref
 from itertools import chain
-from operator import is_not
+from operator import attrgetter, is_not
 from dataclasses import dataclass
 
 import numpy as np
@@ -251,7 +251,7 @@ class Packer:
         bodies, pair_body, pair_problem, pair_group, _d, _t = self._tables
         dts = np.fromiter((float(dt) for _p, dt, _tb in problems), dtype=np.float64, count=len(problems))
         tbs = np.fromiter((float(tb) for _p, _dt, tb in problems), dtype=np.float64, count=len(problems))
-        key = tuple(id(b.tree) for b in bodies)
+        key = tuple(map(id, map(_TREE, bodies)))
         if key != self._key:
             self._static = _assemble_static(bodies, self.pinned)
             self._key = key
@@ -315,7 +315,7 @@ class Packer:
             self._skey = skey
             self._key = None  # force the tree block check below
         bodies, pb, pp, pg, _d, _t = self._tables
-        key = tuple(id(b.tree) for b in bodies)
+        key = tuple(map(id, map(_TREE, bodies)))
         if key != self._key:
             self._static = _assemble_static(bodies, self.pinned)
             self._key = key
@@ -324,6 +324,11 @@ class Packer:
         state = self._states(bodies)
         dts = np.array(np.broadcast_to(np.asarray(dts, dtype=np.float64), (len(pairs),)), copy=True)
         return _scene(self._static, state, self._ids(bodies, skey), pb, pp, pg, dts, np.zeros(len(pairs)))
+
+
+_TREE = attrgetter("tree")
+_CURRENT = attrgetter("timeline.current")
+_POS, _VEL, _ROT, _OMEGA = (attrgetter(k) for k in ("position", "velocity", "rotation", "angular_velocity"))
 
 
 def _states(bodies, out, dyn=None):
@@ -336,11 +341,10 @@ def _states(bodies, out, dyn=None):
         dyn = np.flatnonzero(np.fromiter((hasattr(b, "timeline") for b in bodies), dtype=bool, count=n))
     if len(dyn):
         sel = slice(None) if len(dyn) == n else dyn
-        cur = [b.timeline.current for b in bodies] if len(dyn) == n else [bodies[i].timeline.current for i in dyn]
-        state[sel, 0:3] = np.array([c.position for c in cur], dtype=np.float64)
-        state[sel, 3:6] = np.array([c.velocity for c in cur], dtype=np.float64)
-        state[sel, 6:10] = np.array([c.rotation for c in cur], dtype=np.float64)
-        state[sel, 10:13] = np.array([c.angular_velocity for c in cur], dtype=np.float64)
+        cur = list(map(_CURRENT, bodies if len(dyn) == n else [bodies[i] for i in dyn]))
+        # one concatenation per field (C-level iteration over the states)
+        for lo, hi, get in ((0, 3, _POS), (3, 6, _VEL), (6, 10, _ROT), (10, 13, _OMEGA)):
+            state[sel, lo:hi] = np.concatenate(list(map(get, cur))).reshape(len(cur), hi - lo)
     if len(dyn) < n:
         stat = np.ones(n, dtype=bool)
         stat[dyn] = False
