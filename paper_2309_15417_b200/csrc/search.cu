@@ -803,7 +803,10 @@ __global__ void k_world_count(const BodyInfo* __restrict__ bodies, int n, int64_
   cnt[b] = B.level_off[top] + B.level_size[top] - B.level_off[0];
 }
 
-__global__ void __launch_bounds__(128) k_world_fill(const BodyInfo* __restrict__ bodies, int n,
+#ifndef LTSG_WORLD_MINB
+#define LTSG_WORLD_MINB 8
+#endif
+__global__ void __launch_bounds__(128, LTSG_WORLD_MINB) k_world_fill(const BodyInfo* __restrict__ bodies, int n,
                                                     const int64_t* __restrict__ woff,
                                                     const double* __restrict__ tris, double* __restrict__ world,
                                                     double* __restrict__ wsph) {
