@@ -3,6 +3,7 @@
 #include "common.cuh"
 #include "geom.cuh"
 #include "dist_staged.cuh"
+#include "dist_tile.cuh"
 
 #include <cstring>
 
@@ -61,8 +62,16 @@ __global__ void k_segment_segment(const double* p1, const double* q1, const doub
   }
 }
 
+// ccd._feature_distances per row with the distance of dist_tile.cuh: both
+// triangles' per-triangle constants (edges, |e|^2, reciprocals) staged per
+// lane in shared memory.  The loop is warp-uniform (lanes past the end
+// evaluate a duplicate row) because the distance votes across the warp.
+#ifndef LTSG_ROWS_STAGED
+#define LTSG_ROWS_STAGED 0
+#endif
 __global__ void __launch_bounds__(128, 4) k_feature_distances(const double* ta, const double* tb, int64_t n,
                                                            double* dist) {
+#if LTSG_ROWS_STAGED
   __shared__ double s_stage[kStaged * 128];
   const Staged<128> st{s_stage + threadIdx.x};
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
@@ -70,6 +79,22 @@ __global__ void __launch_bounds__(128, 4) k_feature_distances(const double* ta, 
     stage_pair(st, ldtri(ta, i), ldtri(tb, i));
     dist[i] = __dsqrt_rn(staged_dist_sq(st));
   }
+#else
+  __shared__ double s_stage[2 * kTileASlots * 128];
+  double* sa = s_stage + threadIdx.x;
+  double* sb = s_stage + kTileASlots * 128 + threadIdx.x;
+  const int lane = threadIdx.x & 31;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t w0 = blockIdx.x * (int64_t)blockDim.x + (threadIdx.x & ~31); w0 < n; w0 += stride) {
+    const int64_t i = w0 + lane;  // w0 is the same on every lane: the loop is warp-uniform
+    const int64_t r = i < n ? i : n - 1;
+    const TriReg A = tri_reg(ldtri(ta, r), 0.0), B = tri_reg(ldtri(tb, r), 0.0);
+    tri_store_soa<128>(sa, A);
+    tri_store_soa<128>(sb, B);
+    const double d = __dsqrt_rn(exact_dist_sq(SmemTri<128>{sa}, SmemTri<128>{sb}, A.regular && B.regular));
+    if (i < n) dist[i] = d;
+  }
+#endif
 }
 
 __global__ void k_closest_feature(const double* ta, const double* tb, int64_t n, double* dist,

@@ -93,3 +93,52 @@ def test_allpairs_ragged_tiles_and_mixed_sizes(env):
     pairs = [(rocks[0], rocks[1]), (ico[0], rocks[2]), (rocks[3], ico[1]), (boxes[0], boxes[1]),
              (boxes[2], ico[2]), (rocks[4], boxes[3])]
     _check(env, pairs)
+
+
+def _degenerate_rows(rng):
+    """Triangle pairs that leave the distance kernel's fast paths: repeated
+    and collinear corners, tiny and huge scales (|e|^2 outside the regular
+    range), parallel and collinear edges, coplanar, identical and touching
+    triangles, exact zeros."""
+    base = rng.normal(size=(64, 3, 3))
+    other = rng.normal(size=(64, 3, 3)) * 0.5
+    rows_a, rows_b = [], []
+    dup = base.copy()
+    dup[:, 1] = dup[:, 0]
+    col = base.copy()
+    col[:, 2] = col[:, 0] + rng.uniform(-2, 2, (64, 1)) * (col[:, 1] - col[:, 0])
+    for ta in (dup, col):
+        rows_a.append(ta)
+        rows_b.append(other + ta.mean(1, keepdims=True))
+    for s in (1e-160, 1e-80, 1e-45, 1e40, 1e60):  # |e|^2 around and beyond 2^-150 .. 2^150
+        rows_a.append(base * s)
+        rows_b.append((base[:, [1, 2, 0]] + other * 0.1) * s)
+    par_a = base.copy()
+    par_b = base + rng.normal(size=(64, 1, 3)) * 0.3  # translated copy: every edge parallel
+    rows_a += [par_a, base, base]
+    rows_b += [par_b, base.copy(), base[:, [2, 0, 1]]]  # identical triangles (d = 0), permuted
+    touch = base.copy()
+    touch_b = rng.normal(size=(64, 3, 3))
+    touch_b[:, 0] = touch[:, 1]  # shared vertex
+    flat_a = base.copy()
+    flat_a[:, :, 2] = 0.0
+    flat_b = rng.normal(size=(64, 3, 3)) * 0.7
+    flat_b[:, :, 2] = 0.0  # coplanar
+    rows_a += [touch, flat_a]
+    rows_b += [touch_b, flat_b]
+    small_int = rng.integers(-3, 4, size=(64, 3, 3)).astype(float)  # exact zeros and ties
+    rows_a.append(small_int)
+    rows_b.append(rng.integers(-3, 4, size=(64, 3, 3)).astype(float))
+    return np.concatenate(rows_a), np.concatenate(rows_b)
+
+
+def test_row_distances_degenerate_bit_exact(env):
+    """ltsg_feature_distances (the tile kernels' distance code) on rows that
+    take the irregular-triangle and division fallbacks, bit for bit."""
+    from paper_2309_15417_b200 import kernels
+
+    ta, tb = _degenerate_rows(np.random.default_rng(7))
+    got = kernels.feature_distances(ta, tb)
+    want = O.tri_pair_distance(ta, tb)
+    bad = np.nonzero(got.view(np.uint64) != want.view(np.uint64))[0]
+    assert len(bad) == 0, f"{len(bad)} rows differ, first {bad[:5]}: {got[bad[:5]]} vs {want[bad[:5]]}"
