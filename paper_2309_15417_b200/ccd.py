@@ -269,6 +269,21 @@ class DeviceResult:
 
 
 _capacity_hint = [1 << 12]
+_results = _threading.local()
+_NO_RESULT_CACHE = os.environ.get("LTSG_NO_RESULT_CACHE", "0") == "1"
+
+
+def _result_buffers(n_problems: int, capacity: int, device, raw: bool) -> "DeviceResult":
+    """Device output buffers, re-used by the next call of this thread with the
+    same shape: to_host copies every result out before run_scene returns, and
+    calls on one thread are stream-ordered."""
+    key = (n_problems, capacity, str(device), raw)
+    cached = getattr(_results, "buf", None)
+    if cached is not None and cached[0] == key and not _NO_RESULT_CACHE:
+        return cached[1]
+    out = DeviceResult(n_problems, capacity, device, raw)
+    _results.buf = (key, out)
+    return out
 
 
 def run_scene(ds: DeviceScene, *, widen: float = _WIDEN, exhaustive: bool = False,
@@ -280,7 +295,7 @@ def run_scene(ds: DeviceScene, *, widen: float = _WIDEN, exhaustive: bool = Fals
     scene = ds.struct(widen, exhaustive)
     cap = _capacity_hint[0]
     while True:
-        out = DeviceResult(ds.host.n_problems, cap, ds.device, raw)
+        out = _result_buffers(ds.host.n_problems, cap, ds.device, raw)
         res = out.struct()
         rc = _lib.lib().ltsg_search(C.byref(scene), C.byref(res), ws.handle, C.c_void_p(st.cuda_stream))
         if rc == _lib.LTSG_ECAPACITY and res.n_fused > out.capacity:
