@@ -1056,6 +1056,104 @@ __global__ void k_seed_static(const PairInfo* __restrict__ pairs, int64_t n_pair
   if (lane == 0 && culled) atomicAdd(&ctr->rows, culled);
 }
 
+// Exhaustive static seeds (fine x fine rows of every pair, ccd.py:385-391)
+// as sphere-test tiles: a work item is (pair, 128 triangles of a, 32 of b);
+// the b tile's compact spheres are staged in shared memory and read by every
+// lane at the same address, each lane holds its a sphere in registers, so a
+// row's certified sphere test (static_child_cull's certificate) is a dozen
+// FP64 operations on registers.  Survivors take the separating-axis cull and
+// are appended to the exact frontier.  Every row is counted as a test.
+constexpr int kSeedTileA = 128, kSeedTileB = 32;
+
+__global__ void k_seed_tile_count(const PairInfo* pairs, int64_t n, const BodyInfo* bodies, int64_t* count) {
+  const int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (k > n) return;
+  if (k == n) {
+    count[n] = 0;
+    return;
+  }
+  int la, lb;
+  int64_t na, nb;
+  seed_levels(pairs[k], bodies, 1, &la, &lb, &na, &nb);
+  count[k] = ((na + kSeedTileA - 1) / kSeedTileA) * ((nb + kSeedTileB - 1) / kSeedTileB);
+}
+
+__global__ void __launch_bounds__(kSeedTileA)
+k_seed_static_tile(const PairInfo* __restrict__ pairs, int64_t n_pairs, const BodyInfo* __restrict__ bodies,
+                   const int64_t* __restrict__ woff, const double* __restrict__ world,
+                   const double* __restrict__ wsph, const int64_t* __restrict__ item_off, Cand* out,
+                   unsigned long long cap, Counters* ctr, unsigned long long* n_out) {
+  __shared__ double4 sB[kSeedTileB];
+  const int lane = threadIdx.x & 31;
+  const int64_t n_items = item_off[n_pairs];
+  unsigned long long rows = 0;
+  for (int64_t item = blockIdx.x; item < n_items; item += gridDim.x) {
+    int64_t lo = 0, hi = n_pairs;  // last pair with item_off[k] <= item
+    while (hi - lo > 1) {
+      const int64_t mid = (lo + hi) >> 1;
+      if (__ldg(item_off + mid) <= item) lo = mid; else hi = mid;
+    }
+    const PairInfo p = pairs[lo];
+    int la, lb;
+    int64_t na, nb;
+    seed_levels(p, bodies, 1, &la, &lb, &na, &nb);
+    const int64_t tiles_b = (nb + kSeedTileB - 1) / kSeedTileB;
+    const int64_t local = item - item_off[lo];
+    const int64_t ta = local / tiles_b, tb = local - ta * tiles_b;
+    const int64_t a0 = woff[p.ba] + ta * kSeedTileA, b0 = woff[p.bb] + tb * kSeedTileB;
+    const int nat = (int)min((int64_t)kSeedTileA, na - ta * kSeedTileA);
+    const int nbt = (int)min((int64_t)kSeedTileB, nb - tb * kSeedTileB);
+    __syncthreads();
+    if (threadIdx.x < nbt) {
+      const double2* q = reinterpret_cast<const double2*>(wsph + (size_t)(b0 + threadIdx.x) * kSph);
+      const double2 x = __ldg(q), y = __ldg(q + 1);
+      sB[threadIdx.x] = make_double4(x.x, x.y, y.x, y.y);
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) rows += (unsigned long long)nat * (unsigned long long)nbt;
+    const bool valid = threadIdx.x < nat;
+    const int32_t wa = (int32_t)(a0 + (valid ? threadIdx.x : 0));
+    const double2* qa = reinterpret_cast<const double2*>(wsph + (size_t)wa * kSph);
+    const double2 a01 = __ldg(qa), a2r = __ldg(qa + 1);
+    const double base = 1.0 + fabs(a01.x) + fabs(a01.y) + fabs(a2r.x) + a2r.y;
+    // the sphere tests of 4 rows per step (independent chains); the rare
+    // survivors take the separating-axis cull in place
+#pragma unroll 4
+    for (int j = 0; j < nbt; ++j) {
+      const double4 b = sB[j];
+      bool keep = false;
+      if (valid) {
+        if (a2r.y < 0.0 || b.w < 0.0) {
+          keep = true;  // slivers are never culled
+        } else {  // static_child_cull's certificate, same arithmetic
+          const double dx = a01.x - b.x, dy = a01.y - b.y, dz = a2r.x - b.z;
+          const double reach = a2r.y + b.w + kRestSlop + kCullMargin * (base + b.w);
+          keep = !(fma(dx, dx, fma(dy, dy, dz * dz)) > reach * reach);
+        }
+      }
+      if (__any_sync(0xffffffffu, keep)) {
+        if (keep) {
+          const int32_t wb = (int32_t)(b0 + j);
+          const double* pa = world + (size_t)wa * kWorld;
+          const double* pb = world + (size_t)wb * kWorld;
+          keep = !sat_cull(pa, pb, add(add(__ldg(pa + 9), __ldg(pb + 9)), kRestSlop));
+        }
+        const unsigned m = __ballot_sync(0xffffffffu, keep);
+        if (m) {
+          unsigned long long slot = 0;
+          if (lane == 0) slot = atomicAdd(n_out, (unsigned long long)__popc(m));
+          slot = __shfl_sync(0xffffffffu, slot, 0);
+          if (keep) {
+            const unsigned long long dst = slot + __popc(m & ((1u << lane) - 1u));
+            if (dst < cap) out[dst] = Cand{(int32_t)lo, wa, (int32_t)(b0 + j), 0, 0, 0.0};
+          }
+        }
+      }
+    }
+  }
+  if (threadIdx.x == 0 && rows) atomicAdd(&ctr->rows, rows);
+}
+
 // A flagged coarse row of a static generation: its na x nb children
 // (ccd.py:418-427) in absolute world indices.
 struct Parent {
@@ -2294,6 +2392,29 @@ static int run_search(const ltsg_scene* sc, ltsg_result* out, ltsg_workspace* ws
     return LTSG_OK;
   };
 
+  // static seeds: roots x roots per pair, or fine x fine (exhaustive) as
+  // sphere-test tiles; both count every row and cull on the fly
+  int64_t* seed_items = nullptr;
+  if (all_static && sc->exhaustive && sc->n_pairs > 0) {
+    int64_t* item_cnt;
+    LTSG_TRY(ws_get(ws, "seed_item_cnt", (size_t)sc->n_pairs + 1, &item_cnt));
+    LTSG_TRY(ws_get(ws, "seed_item_off", (size_t)sc->n_pairs + 1, &seed_items));
+    k_seed_tile_count<<<grid_for(sc->n_pairs + 1, 128), 128, 0, st>>>(pr.pairs, sc->n_pairs, pr.bodies, item_cnt);
+    LTSG_LAUNCHED();
+    LTSG_TRY(scan_exclusive(ws, item_cnt, seed_items, sc->n_pairs + 1, st));
+  }
+  auto launch_static_seeds = [&](Cand* dst, size_t cap) -> int {
+    if (seed_items) {
+      k_seed_static_tile<<<148 * 8, kSeedTileA, 0, st>>>(pr.pairs, sc->n_pairs, pr.bodies, woff, world, wsph,
+                                                         seed_items, dst, cap, d_ctr, gen_cnt);
+    } else {
+      k_seed_static<<<(int)std::min<int64_t>(sc->n_pairs, 148 * 16), 128, 0, st>>>(
+          pr.pairs, sc->n_pairs, pr.bodies, woff, world, wsph, dst, cap, d_ctr, gen_cnt, sc->exhaustive);
+    }
+    LTSG_LAUNCHED();
+    return LTSG_OK;
+  };
+
   auto traverse = [&](bool async_mode, bool* overflow) -> int {
     *overflow = false;
     n_timed = 0;
@@ -2316,14 +2437,13 @@ static int run_search(const ltsg_scene* sc, ltsg_result* out, ltsg_workspace* ws
     // the static seed kernel tests (and culls) the root rows: it is screen work
     t_screen.start(st);
     if (all_static) {
-      k_seed_static<<<(int)std::min<int64_t>(sc->n_pairs, 148 * 16), 128, 0, st>>>(
-          pr.pairs, sc->n_pairs, pr.bodies, woff, world, wsph, front, seed_cap, d_ctr, gen_cnt, sc->exhaustive);
+      LTSG_TRY(launch_static_seeds(front, seed_cap));
     } else {
       k_seed_fill<<<(int)std::min<int64_t>(sc->n_pairs, 148 * 16), 128, 0, st>>>(
           pr.pairs, sc->n_pairs, pr.bodies, sc->exhaustive, seed_off, front);
+      LTSG_LAUNCHED();
       LTSG_CUDA(cudaMemcpyAsync(gen_cnt, &seed_total, sizeof(unsigned long long), cudaMemcpyHostToDevice, st));
     }
-    LTSG_LAUNCHED();
     if (async_mode) {
       Cand* buf[2];
       buf[0] = front;
@@ -2364,9 +2484,7 @@ static int run_search(const ltsg_scene* sc, ltsg_result* out, ltsg_workspace* ws
       LTSG_CUDA(cudaMemsetAsync(d_ctr, 0, sizeof(Counters), st));
       LTSG_CUDA(cudaMemsetAsync(gen_cnt, 0, sizeof(unsigned long long) * (kMaxGen + 1), st));
       LTSG_TRY(ws_get(ws, "front0", (size_t)n_first, &front));
-      k_seed_static<<<(int)std::min<int64_t>(sc->n_pairs, 148 * 16), 128, 0, st>>>(
-          pr.pairs, sc->n_pairs, pr.bodies, woff, world, wsph, front, n_first, d_ctr, gen_cnt, sc->exhaustive);
-      LTSG_LAUNCHED();
+      LTSG_TRY(launch_static_seeds(front, n_first));
       LTSG_CUDA(cudaMemcpyAsync(&n_first, gen_cnt, sizeof(n_first), cudaMemcpyDeviceToHost, st));
       LTSG_TRY(read_ctr(d_ctr, &h, st));
     }
