@@ -806,6 +806,9 @@ __global__ void k_world_count(const BodyInfo* __restrict__ bodies, int n, int64_
 #ifndef LTSG_WORLD_MINB
 #define LTSG_WORLD_MINB 8
 #endif
+#ifndef LTSG_WORLD_STAGE
+#define LTSG_WORLD_STAGE 1
+#endif
 __global__ void __launch_bounds__(128, LTSG_WORLD_MINB) k_world_fill(const BodyInfo* __restrict__ bodies, int n,
                                                     const int64_t* __restrict__ woff,
                                                     const double* __restrict__ tris, double* __restrict__ world,
@@ -816,6 +819,10 @@ __global__ void __launch_bounds__(128, LTSG_WORLD_MINB) k_world_fill(const BodyI
   // (lane 0) and a short forward walk per lane.
   const int lane = threadIdx.x & 31;
   const int64_t n_world = woff[n];
+#if LTSG_WORLD_STAGE
+  __shared__ double2 s_stage_w[4][32 * (kWorld / 2)];  // 128 threads = 4 warps
+  double2* stage = s_stage_w[threadIdx.x >> 5];
+#endif
   for (int64_t w0 = ((int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5)) * 32; w0 < n_world;
        w0 += (int64_t)gridDim.x * blockDim.x) {
     int b0 = 0;
@@ -829,69 +836,85 @@ __global__ void __launch_bounds__(128, LTSG_WORLD_MINB) k_world_fill(const BodyI
     }
     b0 = __shfl_sync(0xffffffffu, b0, 0);
     const int64_t w = w0 + lane;
-    if (w >= n_world) continue;
-    int b = b0;
-    while (__ldg(woff + b + 1) <= w) ++b;
-    const int64_t j = w - woff[b];
-    const BodyInfo& B = bodies[b];
-    const double2* src = reinterpret_cast<const double2*>(tris + (size_t)(B.level_off[0] + j) * kRecord);
-    double r[kRecord];
+    const bool valid = w < n_world;
+    if (valid) {
+      int b = b0;
+      while (__ldg(woff + b + 1) <= w) ++b;
+      const int64_t j = w - woff[b];
+      const BodyInfo& B = bodies[b];
+      const double2* src = reinterpret_cast<const double2*>(tris + (size_t)(B.level_off[0] + j) * kRecord);
+      double r[kRecord];
 #pragma unroll
-    for (int k = 0; k < kRecord / 2; ++k) {
-      const double2 v = __ldg(src + k);
-      r[2 * k] = v.x;
-      r[2 * k + 1] = v.y;
-    }
-    double pos[3];
-    position_at(B.m, 0.0, pos);
-    const Tri t = world_tri(B.m.base, pos, r);
-    double wr[kWorld];
+      for (int k = 0; k < kRecord / 2; ++k) {
+        const double2 v = __ldg(src + k);
+        r[2 * k] = v.x;
+        r[2 * k + 1] = v.y;
+      }
+      double pos[3];
+      position_at(B.m, 0.0, pos);
+      const Tri t = world_tri(B.m.base, pos, r);
+      double wr[kWorld];
 #pragma unroll
-    for (int k = 0; k < 3; ++k) {
-      wr[3 * k] = t.v[k].x;
-      wr[3 * k + 1] = t.v[k].y;
-      wr[3 * k + 2] = t.v[k].z;
-    }
-    wr[9] = r[9];
-    wr[10] = r[10];
-    {  // first child as an absolute world index (children are contiguous)
-      int lvl = 0;
-      while (lvl + 1 < B.n_levels && B.level_off[0] + j >= B.level_off[lvl + 1]) ++lvl;
-      int2 ch = *reinterpret_cast<const int2*>(r + 11);
-      if (lvl > 0) ch.x = (int32_t)(woff[b] + B.level_off[lvl - 1] - B.level_off[0] + ch.x);
-      *reinterpret_cast<int2*>(wr + 11) = ch;
-    }
-    // bounding sphere in world coordinates (approximate; the cull margin absorbs it)
-    constexpr double kThird = 1.0 / 3.0;
-    const V3 c{(t.v[0].x + t.v[1].x + t.v[2].x) * kThird, (t.v[0].y + t.v[1].y + t.v[2].y) * kThird,
-               (t.v[0].z + t.v[1].z + t.v[2].z) * kThird};
-    double r2 = 0.0;
+      for (int k = 0; k < 3; ++k) {
+        wr[3 * k] = t.v[k].x;
+        wr[3 * k + 1] = t.v[k].y;
+        wr[3 * k + 2] = t.v[k].z;
+      }
+      wr[9] = r[9];
+      wr[10] = r[10];
+      {  // first child as an absolute world index (children are contiguous)
+        int lvl = 0;
+        while (lvl + 1 < B.n_levels && B.level_off[0] + j >= B.level_off[lvl + 1]) ++lvl;
+        int2 ch = *reinterpret_cast<const int2*>(r + 11);
+        if (lvl > 0) ch.x = (int32_t)(woff[b] + B.level_off[lvl - 1] - B.level_off[0] + ch.x);
+        *reinterpret_cast<int2*>(wr + 11) = ch;
+      }
+      // bounding sphere in world coordinates (approximate; the cull margin absorbs it)
+      constexpr double kThird = 1.0 / 3.0;
+      const V3 c{(t.v[0].x + t.v[1].x + t.v[2].x) * kThird, (t.v[0].y + t.v[1].y + t.v[2].y) * kThird,
+                 (t.v[0].z + t.v[1].z + t.v[2].z) * kThird};
+      double r2 = 0.0;
 #pragma unroll
-    for (int k = 0; k < 3; ++k) {
-      const V3 d = t.v[k] - c;
-      r2 = fmax(r2, fma(d.x, d.x, fma(d.y, d.y, d.z * d.z)));
-    }
-    // unit face normal and plane offset for the separating-axis cull
-    const V3 e1{t.v[1].x - t.v[0].x, t.v[1].y - t.v[0].y, t.v[1].z - t.v[0].z};
-    const V3 e2{t.v[2].x - t.v[0].x, t.v[2].y - t.v[0].y, t.v[2].z - t.v[0].z};
-    const V3 nn{fma(e1.y, e2.z, -e1.z * e2.y), fma(e1.z, e2.x, -e1.x * e2.z), fma(e1.x, e2.y, -e1.y * e2.x)};
-    const double nl = sqrt(fma(nn.x, nn.x, fma(nn.y, nn.y, nn.z * nn.z)));
-    const double inv = nl > 0.0 ? 1.0 / nl : 0.0;
-    wr[16] = nn.x * inv;
-    wr[17] = nn.y * inv;
-    wr[18] = nn.z * inv;
-    wr[19] = fma(wr[16], t.v[0].x, fma(wr[17], t.v[0].y, wr[18] * t.v[0].z));
-    wr[12] = c.x;
-    wr[13] = c.y;
-    wr[14] = c.z;
-    // sliver flag from the body record; a zero-area triangle is never culled either
-    wr[15] = r[15] >= 0.0 && nl > 0.0 ? sqrt(r2) * (1.0 + 1e-12) : -1.0;
-    double2* dst = reinterpret_cast<double2*>(world + (size_t)w * kWorld);
+      for (int k = 0; k < 3; ++k) {
+        const V3 d = t.v[k] - c;
+        r2 = fmax(r2, fma(d.x, d.x, fma(d.y, d.y, d.z * d.z)));
+      }
+      // unit face normal and plane offset for the separating-axis cull
+      const V3 e1{t.v[1].x - t.v[0].x, t.v[1].y - t.v[0].y, t.v[1].z - t.v[0].z};
+      const V3 e2{t.v[2].x - t.v[0].x, t.v[2].y - t.v[0].y, t.v[2].z - t.v[0].z};
+      const V3 nn{fma(e1.y, e2.z, -e1.z * e2.y), fma(e1.z, e2.x, -e1.x * e2.z), fma(e1.x, e2.y, -e1.y * e2.x)};
+      const double nl = sqrt(fma(nn.x, nn.x, fma(nn.y, nn.y, nn.z * nn.z)));
+      const double inv = nl > 0.0 ? 1.0 / nl : 0.0;
+      wr[16] = nn.x * inv;
+      wr[17] = nn.y * inv;
+      wr[18] = nn.z * inv;
+      wr[19] = fma(wr[16], t.v[0].x, fma(wr[17], t.v[0].y, wr[18] * t.v[0].z));
+      wr[12] = c.x;
+      wr[13] = c.y;
+      wr[14] = c.z;
+      // sliver flag from the body record; a zero-area triangle is never culled either
+      wr[15] = r[15] >= 0.0 && nl > 0.0 ? sqrt(r2) * (1.0 + 1e-12) : -1.0;
+#if LTSG_WORLD_STAGE
 #pragma unroll
-    for (int k = 0; k < kWorld / 2; ++k) dst[k] = make_double2(wr[2 * k], wr[2 * k + 1]);
-    double2* sp = reinterpret_cast<double2*>(wsph + (size_t)w * kSph);
-    sp[0] = make_double2(c.x, c.y);
-    sp[1] = make_double2(c.z, wr[15] < 0.0 ? -1.0 : wr[15] + r[9]);
+      for (int k = 0; k < kWorld / 2; ++k) stage[lane * (kWorld / 2) + k] = make_double2(wr[2 * k], wr[2 * k + 1]);
+#else
+      double2* dst = reinterpret_cast<double2*>(world + (size_t)w * kWorld);
+#pragma unroll
+      for (int k = 0; k < kWorld / 2; ++k) dst[k] = make_double2(wr[2 * k], wr[2 * k + 1]);
+#endif
+      double2* sp = reinterpret_cast<double2*>(wsph + (size_t)w * kSph);
+      sp[0] = make_double2(c.x, c.y);
+      sp[1] = make_double2(c.z, wr[15] < 0.0 ? -1.0 : wr[15] + r[9]);
+    }
+#if LTSG_WORLD_STAGE
+    // the warp's records are consecutive in `world`: write them out from the
+    // stage with contiguous 16-byte stores
+    __syncwarp();
+    const int nv = (int)min((int64_t)32, n_world - w0);
+    double2* dst = reinterpret_cast<double2*>(world + (size_t)w0 * kWorld);
+    for (int idx = lane; idx < nv * (kWorld / 2); idx += 32) dst[idx] = stage[idx];
+    __syncwarp();
+#endif
   }
 }
 
