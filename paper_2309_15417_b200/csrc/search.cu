@@ -2706,10 +2706,14 @@ static int fuse_stage(ltsg_workspace* ws, cudaStream_t st, Soa ro, unsigned long
   LTSG_LAUNCHED();
   {
     size_t tmp = 0;
-    LTSG_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, tmp, key, keys_sorted, idx_in, idx, n_rec, 0, 64, st));
+    // keys are (problem << 32) | rank with problem < np: the bits above
+    // 32 + bit_width(np) are zero, so fewer radix passes sort them
+    int end_bit = 32;
+    while (end_bit < 64 && ((unsigned long long)np >> (end_bit - 32)) != 0) ++end_bit;
+    LTSG_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, tmp, key, keys_sorted, idx_in, idx, n_rec, 0, end_bit, st));
     void* t;
     LTSG_TRY(ws->get("cub_tmp", tmp, &t));
-    LTSG_CUDA(cub::DeviceRadixSort::SortPairs(t, tmp, key, keys_sorted, idx_in, idx, n_rec, 0, 64, st));
+    LTSG_CUDA(cub::DeviceRadixSort::SortPairs(t, tmp, key, keys_sorted, idx_in, idx, n_rec, 0, end_bit, st));
   }
   k_heads<<<grid_for(n_rec + 1, 256), 256, 0, st>>>(keys_sorted, n_rec, head);
   LTSG_LAUNCHED();
