@@ -2049,10 +2049,7 @@ constexpr int kTileB = 32;
 #define LTSG_TILE_MINB 6
 #endif
 
-#ifndef LTSG_TILE_ASMEM
-#define LTSG_TILE_ASMEM 1
-#endif
-constexpr int kTileSmemBytes = (kTileB * kTilePre + (LTSG_TILE_ASMEM ? kTileA * kTileASlots : 0)) * 8;
+constexpr int kTileSmemBytes = (kTileB * kTilePre + kTileA * kTileASlots) * 8;
 
 __global__ void __launch_bounds__(kTileA, LTSG_TILE_MINB)
 k_allpairs_tile(const PairInfo* __restrict__ pairs, int64_t n_pairs, const BodyInfo* __restrict__ bodies,
@@ -2084,20 +2081,12 @@ k_allpairs_tile(const PairInfo* __restrict__ pairs, int64_t n_pairs, const BodyI
     const int i = ta * kTileA + threadIdx.x;
     const bool valid = i < na;
     const double* wa = world + (size_t)(woff[p.ba] + (valid ? i : na - 1)) * kWorld;
-#if LTSG_TILE_ASMEM
     const double eps_a = __ldg(wa + 9);
     const TriReg ar = tri_reg(load_world(wa), eps_a);
     const bool a_regular = ar.regular;
     tri_store_soa<kTileA>(sA + threadIdx.x, ar);
     __syncthreads();
     const SmemTri<kTileA> A{sA + threadIdx.x};
-#else
-    __syncthreads();
-    const TriReg AR = tri_reg(load_world(wa), __ldg(wa + 9));
-    const double eps_a = AR.eps;
-    const bool a_regular = AR.regular;
-    const RegA A{AR};
-#endif
     double* od = out_dist ? out_dist + row_start[lo] + (int64_t)(valid ? i : 0) * nb + jb0 : nullptr;
 #pragma unroll 1
     for (int j = 0; j < nbt; ++j) {
