@@ -1310,19 +1310,41 @@ k_expand_filter(const Parent* __restrict__ par, const unsigned long long* n_par,
     no += __popc(mk);
     if (no >= 64) flush(64);
   };
-  for (int64_t t0 = ((int64_t)blockIdx.x * kExpWarps + warp) * 32; t0 < total;
-       t0 += (int64_t)gridDim.x * kExpThreads) {
-    const int64_t t = t0 + lane;
+  // The slot -> parent mapping uses 32-bit division (total < 2^32 for any
+  // workspace that fits), and the next iteration's parent record is loaded
+  // before this iteration's child spheres are tested.
+  const int64_t stride = (int64_t)gridDim.x * kExpThreads;
+  const bool small = total < ((int64_t)1 << 32);
+  auto parent_of = [&](int64_t t, int* j) -> int64_t {
+    int64_t pi;
+    if (small) {
+      const uint32_t tt = (uint32_t)t, f = (uint32_t)fan, p = tt / f;
+      pi = p;
+      *j = (int)(tt - p * f);
+    } else {
+      pi = t / fan;
+      *j = (int)(t - pi * fan);
+    }
+    return pi;
+  };
+  int64_t t = ((int64_t)blockIdx.x * kExpWarps + warp) * 32 + lane;
+  Parent Pn{};
+  int jn = 0;
+  if (t < total) Pn = par[parent_of(t, &jn)];
+  for (int64_t t0 = ((int64_t)blockIdx.x * kExpWarps + warp) * 32; t0 < total; t0 += stride) {
+    const Parent P = Pn;
+    const int j = jn;
+    const bool live = t < total;
+    t += stride;
+    if (t < total) Pn = par[parent_of(t, &jn)];  // prefetch
     bool keep = false;
     Cand c{};
-    if (t < total) {
-      const int64_t pi = t / fan;
-      const int j = (int)(t - pi * fan);
-      const Parent P = par[pi];
-      if (j < (int)P.na * (int)P.nb) {
+    if (live) {
+      const int nb = P.nb;
+      if (j < (int)P.na * nb) {
         ++rows;
-        const int k = j / P.nb;
-        c = Cand{P.pair, P.a0 + k, P.b0 + (j - k * P.nb), (int16_t)P.la, (int16_t)P.lb, 0.0};
+        const int k = nb == 4 ? (j >> 2) : (nb == 2 ? (j >> 1) : j / nb);
+        c = Cand{P.pair, P.a0 + k, P.b0 + (j - k * nb), (int16_t)P.la, (int16_t)P.lb, 0.0};
         keep = !static_child_cull(wsph, c.ia, c.ib);
       }
     }
