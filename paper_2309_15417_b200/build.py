@@ -49,8 +49,31 @@ def _stale() -> bool:
     return any(os.path.getmtime(d) > t for d in deps)
 
 
+def build_fastpack(force: bool = False) -> str:
+    """The host packing helper (csrc/fastpack.c, CPython C API) -> in-tree
+    _fastpack<EXT_SUFFIX>, built with the system C compiler."""
+    import sysconfig
+
+    src = os.path.join(CSRC, "fastpack.c")
+    dst = os.path.join(PKG, "_fastpack" + sysconfig.get_config_var("EXT_SUFFIX"))
+    if not force and os.path.exists(dst) and os.path.getmtime(dst) >= os.path.getmtime(src):
+        return dst
+    cc = shutil.which("gcc") or shutil.which("cc")
+    if cc is None:
+        raise RuntimeError("no C compiler for the packing helper")
+    tmp = dst + ".tmp"
+    import numpy
+
+    subprocess.run([cc, "-O2", "-shared", "-fPIC", "-I", sysconfig.get_paths()["include"], "-I", numpy.get_include(),
+                    src, "-o", tmp], check=True)
+    os.replace(tmp, dst)
+    return dst
+
+
 def build(force: bool = False, verbose: bool = False, extra=(), out: str | None = None) -> str:
     lib = out or LIB
+    if out is None:
+        build_fastpack(force)
     if out is None and not force and not _stale():
         return LIB
     objs = []

@@ -291,13 +291,16 @@ class Packer:
         """Fast path for pair-mode batches (one body pair per problem, as
         `pair_earliest_contact`): no per-problem Python tuples, one fusion
         group per problem, t_base 0."""
-        flat = list(chain.from_iterable(pairs))
         prev = getattr(self, "_flat", None)
-        same = (prev is not None and len(prev) == len(flat) and getattr(self, "_skey", None) == "pairs"
-                and not any(map(is_not, flat, prev)))
+        if prev is not None and getattr(self, "_skey", None) == "pairs" and _fastpack is not None:
+            same = _fastpack.pairs_are(pairs, prev)
+        else:
+            flat = list(chain.from_iterable(pairs))
+            same = (prev is not None and len(prev) == len(flat) and getattr(self, "_skey", None) == "pairs"
+                    and not any(map(is_not, flat, prev)))
         skey = "pairs"
         if not same:
-            self._flat = flat
+            self._flat = list(chain.from_iterable(pairs))
             slot_of = {}
             bodies = []
             pb = np.empty((len(pairs), 2), dtype=np.int32)
@@ -315,11 +318,12 @@ class Packer:
             self._skey = skey
             self._key = None  # force the tree block check below
         bodies, pb, pp, pg, _d, _t = self._tables
-        key = tuple(map(id, map(_TREE, bodies)))
-        if key != self._key:
-            self._static = _assemble_static(bodies, self.pinned)
-            self._key = key
-            self._trees = [b.tree for b in bodies]
+        if not (self._key is not None and _fastpack is not None and _fastpack.trees_are(bodies, self._trees)):
+            key = tuple(map(id, map(_TREE, bodies)))
+            if key != self._key:
+                self._static = _assemble_static(bodies, self.pinned)
+                self._key = key
+                self._trees = [b.tree for b in bodies]
         self._pair_arrays = (pb, pp, pg)
         state = self._states(bodies)
         dts = np.array(np.broadcast_to(np.asarray(dts, dtype=np.float64), (len(pairs),)), copy=True)
@@ -331,10 +335,19 @@ _CURRENT = attrgetter("timeline.current")
 _POS, _VEL, _ROT, _OMEGA = (attrgetter(k) for k in ("position", "velocity", "rotation", "angular_velocity"))
 
 
+try:  # the C gather of the states (csrc/fastpack.c), built in-tree by build.build_fastpack
+    from . import _fastpack
+except ImportError:  # pragma: no cover - host packing falls back to numpy
+    _fastpack = None
+
+
 def _states(bodies, out, dyn=None):
     """Body snapshot rows (body_state_row for every body), vectorised.
     `dyn`: indices of the dynamic bodies (computed when not given)."""
     n = len(bodies)
+    if _fastpack is not None and out.dtype == np.float64 and out.flags.c_contiguous and out.shape == (n, 16):
+        _fastpack.gather_states(bodies, out)
+        return out
     state = out
     state.fill(0.0)
     if dyn is None:
