@@ -1002,12 +1002,12 @@ __device__ __forceinline__ bool sat_cull(const double* wa, const double* wb, dou
 
 constexpr int kStaticWarps = 4;
 #ifndef LTSG_STATIC_LITE
-#define LTSG_STATIC_LITE 0
+#define LTSG_STATIC_LITE 1
 #endif
 constexpr int kStaticStageBytes = (LTSG_STATIC_LITE ? kStagedLite : kStaged) * 32 * kStaticWarps * sizeof(double);
 constexpr int kAllpairsStageBytes = kStaged * 32 * kStaticWarps * sizeof(double);
 #ifndef LTSG_STATIC_MINB
-#define LTSG_STATIC_MINB 5
+#define LTSG_STATIC_MINB 7
 #endif
 
 // Static batches (every problem has dt = 0) run a leaner traversal.  Every
