@@ -1009,6 +1009,9 @@ constexpr int kAllpairsStageBytes = kStaged * 32 * kStaticWarps * sizeof(double)
 #ifndef LTSG_STATIC_MINB
 #define LTSG_STATIC_MINB 7
 #endif
+#ifndef LTSG_STATIC_GRID
+#define LTSG_STATIC_GRID 20
+#endif
 
 // Static batches (every problem has dt = 0) run a leaner traversal.  Every
 // candidate has exactly one sample at tau = w0 = 0 (span 0, ccd.py:352), its
@@ -1260,6 +1263,9 @@ k_screen_static(const Cand* __restrict__ front, int64_t n, const PairInfo* __res
 // separating-axis cull on the block-compacted sphere survivors, settle
 // most of them, and the rest are appended (one atomic per block
 // iteration) as the next generation's exact frontier.
+#ifndef LTSG_EXP_GRID
+#define LTSG_EXP_GRID 4
+#endif
 constexpr int kExpThreads = 256;
 constexpr int kExpWarps = kExpThreads / 32;
 // Each warp works alone (no block barriers, so the load latency of one warp
@@ -2404,15 +2410,15 @@ static int run_search(const ltsg_scene* sc, ltsg_result* out, ltsg_workspace* ws
     if (all_static) {
       // exact pass of the frontier (parents into xbuf, count in xcnt), then
       // the culled expansion of the parents into the next frontier
-      const int64_t blocks = n_in ? 148LL * 20 : (n + 32 * kStaticWarps - 1) / (32 * kStaticWarps);
+      const int64_t blocks = n_in ? 148LL * LTSG_STATIC_GRID : (n + 32 * kStaticWarps - 1) / (32 * kStaticWarps);
       const size_t e = 3 * n_timed++;
       LTSG_CUDA(cudaEventRecord(ws->event(e), st));
-      k_screen_static<<<(int)std::max<int64_t>(1, std::min<int64_t>(blocks, 148LL * 20)), 32 * kStaticWarps,
+      k_screen_static<<<(int)std::max<int64_t>(1, std::min<int64_t>(blocks, 148LL * LTSG_STATIC_GRID)), 32 * kStaticWarps,
                         kStaticStageBytes, st>>>(in, n, pr.pairs, pr.bodies, world, woff, so,
                                                  reinterpret_cast<Parent*>(xbuf), xcnt);
       LTSG_LAUNCHED();
       LTSG_CUDA(cudaEventRecord(ws->event(e + 1), st));
-      k_expand_filter<<<148 * 8, kExpThreads, 0, st>>>(reinterpret_cast<const Parent*>(xbuf), xcnt, cap, (int)fan,
+      k_expand_filter<<<148 * LTSG_EXP_GRID, kExpThreads, 0, st>>>(reinterpret_cast<const Parent*>(xbuf), xcnt, cap, (int)fan,
                                                        world, wsph, next, cap, n_out, d_ctr);
       LTSG_LAUNCHED();
       LTSG_CUDA(cudaEventRecord(ws->event(e + 2), st));
