@@ -282,9 +282,12 @@ struct ScreenOut {
   Counters* ctr;
 };
 
-constexpr int kScreenWarps = 2;
+#ifndef LTSG_SCREEN_WARPS
+#define LTSG_SCREEN_WARPS 8
+#endif
+constexpr int kScreenWarps = LTSG_SCREEN_WARPS;
 #ifndef LTSG_SCREEN_MINB
-#define LTSG_SCREEN_MINB 8
+#define LTSG_SCREEN_MINB 2
 #endif
 constexpr int kRowsPerWarp = 32 * kMaxSamples;
 
