@@ -34,6 +34,7 @@ extern "C" {
 #define LTSG_EINVAL 1
 #define LTSG_ECUDA 2
 #define LTSG_ECAPACITY 3
+#define LTSG_ENOMEM 4 /* cudaMalloc failed inside the budget: a real out-of-memory, not retried */
 
 const char* ltsg_last_error(void);
 int ltsg_version(void);
@@ -200,8 +201,12 @@ typedef struct {
 typedef struct ltsg_workspace ltsg_workspace;
 
 /* Scratch owner for ltsg_search: grows on demand, reused across calls.  One
- * workspace per concurrent stream.  `budget_bytes` caps its device memory
- * (0 = 75% of free memory at creation). */
+ * workspace per concurrent stream.  All workspaces of the process draw from
+ * one pool of 75% of the device memory free at the first allocation, so
+ * concurrent engine threads cannot jointly exceed the device; `budget_bytes`
+ * additionally caps this workspace (0 = pool only).  Beyond either limit a
+ * call returns LTSG_ECAPACITY (the host splits the batch); a cudaMalloc
+ * failure inside them returns LTSG_ENOMEM. */
 ltsg_workspace* ltsg_workspace_create(int64_t budget_bytes);
 void ltsg_workspace_destroy(ltsg_workspace* ws);
 int64_t ltsg_workspace_bytes(const ltsg_workspace* ws);

@@ -14,7 +14,7 @@ import threading
 _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.environ.get("LTSG_LIB") or os.path.join(_HERE, "libltsgpu.so")
 
-LTSG_OK, LTSG_EINVAL, LTSG_ECUDA, LTSG_ECAPACITY = 0, 1, 2, 3
+LTSG_OK, LTSG_EINVAL, LTSG_ECUDA, LTSG_ECAPACITY, LTSG_ENOMEM = 0, 1, 2, 3, 4
 
 P = C.c_void_p
 I64 = C.c_int64
@@ -67,6 +67,11 @@ class LtsgError(RuntimeError):
 
 class CapacityError(LtsgError):
     pass
+
+
+class DeviceMemoryError(LtsgError):
+    """cudaMalloc failed inside the workspace budget (LTSG_ENOMEM): a real
+    out-of-memory, which splitting the batch would not cure."""
 
 
 def lib():
@@ -127,6 +132,8 @@ def check(rc: int, what: str) -> None:
         raise ValueError(f"{what}: {msg}")
     if rc == LTSG_ECAPACITY:
         raise CapacityError(f"{what}: {msg}")
+    if rc == LTSG_ENOMEM:
+        raise DeviceMemoryError(f"{what}: {msg}")
     raise LtsgError(f"{what} failed ({rc}): {msg}")
 
 

@@ -76,24 +76,31 @@ def build(force: bool = False, verbose: bool = False, extra=(), out: str | None 
         build_fastpack(force)
     if out is None and not force and not _stale():
         return LIB
-    objs = []
+    import tempfile
+
     nvcc = nvcc_path()
     tmp = lib + ".tmp"
-    for src in SOURCES:
-        obj = os.path.join(CSRC, src.replace(".cu", f".{os.getpid()}.o"))
-        cmd = [nvcc, *NVCC_FLAGS, *extra, "-I", os.path.join(REPO, "include"), "-c",
-               os.path.join(CSRC, src), "-o", obj]
-        if verbose:
-            cmd.insert(1, "-Xptxas=-v")
-            print(" ".join(cmd), flush=True)
-        subprocess.run(cmd, check=True)
-        objs.append(obj)
-    cmd = [nvcc, "-gencode", "arch=compute_100a,code=sm_100a", "-shared", "-Xcompiler", "-fPIC",
-           *objs, "-o", tmp]
-    subprocess.run(cmd, check=True)
-    os.replace(tmp, lib)
-    for obj in objs:
-        os.remove(obj)
+    # objects go to a private temporary directory that is removed whatever
+    # happens (a failed compile leaves nothing next to the sources)
+    with tempfile.TemporaryDirectory(prefix="ltsg_build_") as objdir:
+        objs = []
+        for src in SOURCES:
+            obj = os.path.join(objdir, src.replace(".cu", ".o"))
+            cmd = [nvcc, *NVCC_FLAGS, *extra, "-I", os.path.join(REPO, "include"), "-c",
+                   os.path.join(CSRC, src), "-o", obj]
+            if verbose:
+                cmd.insert(1, "-Xptxas=-v")
+                print(" ".join(cmd), flush=True)
+            subprocess.run(cmd, check=True)
+            objs.append(obj)
+        cmd = [nvcc, "-gencode", "arch=compute_100a,code=sm_100a", "-shared", "-Xcompiler", "-fPIC",
+               *objs, "-o", tmp]
+        try:
+            subprocess.run(cmd, check=True)
+            os.replace(tmp, lib)
+        finally:
+            if os.path.exists(tmp):
+                os.remove(tmp)
     return lib
 
 

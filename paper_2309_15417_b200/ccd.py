@@ -291,7 +291,13 @@ def run_scene(ds: DeviceScene, *, widen: float = _WIDEN, exhaustive: bool = Fals
     """ltsg_search on a device-resident scene; returns host arrays."""
     torch = _lib.require_cuda()
     ws = workspace or _lib.workspace()
-    st = stream if stream is not None else torch.cuda.current_stream()
+    if stream is not None and stream != torch.cuda.current_stream():
+        # the scene was uploaded on the current stream: order the search after
+        # it, then run the search and the D2H copies (to_host) on `stream`
+        stream.wait_stream(torch.cuda.current_stream())
+        with torch.cuda.stream(stream):
+            return run_scene(ds, widen=widen, exhaustive=exhaustive, raw=raw, workspace=ws)
+    st = torch.cuda.current_stream()
     scene = ds.struct(widen, exhaustive)
     cap = _capacity_hint[0]
     while True:

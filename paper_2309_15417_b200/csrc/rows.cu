@@ -5,6 +5,8 @@
 #include "dist_staged.cuh"
 #include "dist_tile.cuh"
 
+#include <atomic>
+#include <cstdint>
 #include <cstring>
 
 namespace ltsg {
@@ -243,15 +245,8 @@ int ltsg_fp64_peak(double* tflops, double* ms, void* stream) {
 ltsg_workspace* ltsg_workspace_create(int64_t budget_bytes) {
   ltsg_workspace* ws = new ltsg_workspace();
   cudaGetDevice(&ws->device);
-  if (budget_bytes <= 0) {
-    size_t free_b = 0, total_b = 0;
-    if (cudaMemGetInfo(&free_b, &total_b) == cudaSuccess)
-      ws->budget = (size_t)(0.75 * (double)free_b);
-    else
-      ws->budget = (size_t)8 << 30;
-  } else {
-    ws->budget = (size_t)budget_bytes;
-  }
+  // 0 = no per-workspace cap: only the process-wide pool (below) applies
+  ws->budget = budget_bytes > 0 ? (size_t)budget_bytes : SIZE_MAX;
   return ws;
 }
 
@@ -260,6 +255,37 @@ void ltsg_workspace_destroy(ltsg_workspace* ws) { delete ws; }
 int64_t ltsg_workspace_bytes(const ltsg_workspace* ws) { return ws ? (int64_t)ws->total : 0; }
 
 }  // extern "C"
+
+// Process-wide budget shared by every workspace (one per engine thread): 75%
+// of the device memory free when the first workspace allocates.  N threads
+// therefore cannot jointly claim more than the device has; a request beyond
+// it is a capacity condition (LTSG_ECAPACITY: the host splits the batch),
+// while a failing cudaMalloc inside the budget is a genuine out-of-memory
+// (LTSG_ENOMEM: not retried by splitting).
+static std::atomic<size_t> g_pool_used{0};
+static std::atomic<size_t> g_pool_budget{0};
+
+static size_t pool_budget() {
+  size_t b = g_pool_budget.load();
+  if (b == 0) {
+    size_t free_b = 0, total_b = 0;
+    b = cudaMemGetInfo(&free_b, &total_b) == cudaSuccess ? (size_t)(0.75 * (double)free_b) : ((size_t)8 << 30);
+    size_t zero = 0;
+    if (!g_pool_budget.compare_exchange_strong(zero, b)) b = zero;
+  }
+  return b;
+}
+
+static bool pool_reserve(size_t bytes) {
+  const size_t budget = pool_budget();
+  size_t cur = g_pool_used.load();
+  while (true) {
+    if (cur + bytes > budget) return false;
+    if (g_pool_used.compare_exchange_weak(cur, cur + bytes)) return true;
+  }
+}
+
+static void pool_release(size_t bytes) { g_pool_used.fetch_sub(bytes); }
 
 int ltsg_workspace::get(const char* name, size_t bytes, void** out, bool keep) {
   Buf& b = bufs[name];
@@ -275,16 +301,27 @@ int ltsg_workspace::get(const char* name, size_t bytes, void** out, bool keep) {
               bytes, total, budget);
     return LTSG_ECAPACITY;
   }
+  // the old buffer stays allocated while a kept one is copied: reserve both
+  if (!pool_reserve(want)) {
+    want = bytes;
+    if (!pool_reserve(want)) {
+      set_error("device memory pool exhausted: slot %s needs %zu bytes (pool %zu of %zu in use)", name, bytes,
+                g_pool_used.load(), pool_budget());
+      return LTSG_ECAPACITY;
+    }
+  }
   void* p = nullptr;
   cudaError_t err = cudaMalloc(&p, want);
   if (err != cudaSuccess) {
     cudaGetLastError();
+    pool_release(want);
     set_error("cudaMalloc(%zu) for %s failed: %s", want, name, cudaGetErrorString(err));
-    return LTSG_ECAPACITY;
+    return LTSG_ENOMEM;
   }
   if (b.ptr) {
     if (keep) cudaMemcpy(p, b.ptr, b.bytes, cudaMemcpyDeviceToDevice);
     cudaFree(b.ptr);
+    pool_release(b.bytes);
   }
   total = total - b.bytes + want;
   b.ptr = p;
@@ -295,7 +332,10 @@ int ltsg_workspace::get(const char* name, size_t bytes, void** out, bool keep) {
 
 ltsg_workspace::~ltsg_workspace() {
   for (auto& kv : bufs)
-    if (kv.second.ptr) cudaFree(kv.second.ptr);
+    if (kv.second.ptr) {
+      cudaFree(kv.second.ptr);
+      pool_release(kv.second.bytes);
+    }
   for (auto e : events)
     if (e) cudaEventDestroy(e);
 }

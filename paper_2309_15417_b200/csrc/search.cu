@@ -1008,7 +1008,6 @@ constexpr int kStaticWarps = 4;
 #define LTSG_STATIC_LITE 1
 #endif
 constexpr int kStaticStageBytes = (LTSG_STATIC_LITE ? kStagedLite : kStaged) * 32 * kStaticWarps * sizeof(double);
-constexpr int kAllpairsStageBytes = kStaged * 32 * kStaticWarps * sizeof(double);
 #ifndef LTSG_STATIC_MINB
 #define LTSG_STATIC_MINB 7
 #endif
@@ -1372,7 +1371,7 @@ k_expand_filter(const Parent* __restrict__ par, const unsigned long long* n_par,
 
 // ---------------------------------------------------------------- zoom
 
-constexpr int kZoomQueue = 512;
+constexpr int kZoomQueue = 512;  // pending intervals per entry on the first pass
 constexpr int kZoomWarps = 4;
 
 struct Interval {
@@ -1383,21 +1382,26 @@ struct Interval {
 // intervals of a round are processed in order, each sampled at 17 points by
 // lanes 0..16; once a bracket exists, intervals starting at or after its lo
 // are skipped (ccd.py:278-279), exactly as the reference's sequential loop.
+// The reference's pending list is unbounded; here each warp has two queues
+// of `qcap` intervals.  An entry that would exceed them is abandoned without
+// output and appended to `spill`; the host re-runs the spilled entries
+// (`sel`) with a queue 16x larger, until none spills.
 __global__ void __launch_bounds__(32 * kZoomWarps)
-k_zoom(const Entry* __restrict__ entries, int64_t n, const PairInfo* __restrict__ pairs,
-       const BodyInfo* __restrict__ bodies, const double* __restrict__ tris,
-       Interval* __restrict__ queue, Bracket* brackets, Counters* ctr) {
+k_zoom(const Entry* __restrict__ entries, int64_t n, const int64_t* __restrict__ sel,
+       const PairInfo* __restrict__ pairs, const BodyInfo* __restrict__ bodies, const double* __restrict__ tris,
+       Interval* __restrict__ queue, int qcap, int64_t* __restrict__ spill, Bracket* brackets, Counters* ctr) {
   __shared__ double s_grid[kZoomWarps][kZoomSamples + 1];
   __shared__ double s_stage[kStaged * 32 * kZoomWarps];
   const Staged<32 * kZoomWarps> st{s_stage + threadIdx.x};
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
   const int64_t gw = blockIdx.x * (int64_t)kZoomWarps + warp;
-  Interval* q0 = queue + gw * 2 * kZoomQueue;
-  Interval* q1 = q0 + kZoomQueue;
+  Interval* q0 = queue + gw * 2 * (int64_t)qcap;
+  Interval* q1 = q0 + qcap;
   double* grid = s_grid[warp];
   for (int64_t e = gw; e < n; e += (int64_t)gridDim.x * kZoomWarps) {
-    const Entry en = entries[e];
+    const int64_t ei = sel ? sel[e] : e;
+    const Entry en = entries[ei];
     const PairInfo p = pairs[en.pair];
     const BodyInfo& A = bodies[p.ba];
     const BodyInfo& B = bodies[p.bb];
@@ -1410,7 +1414,7 @@ k_zoom(const Entry* __restrict__ entries, int64_t n, const PairInfo* __restrict_
     double blo = 0.0, bhi = 0.0;
     unsigned long long ref_rows = 0, exec_rows = 0;
     bool overflow = false;
-    for (int round = 0; round < 64 && n_cur > 0; ++round) {
+    for (int round = 0; round < 64 && n_cur > 0 && !overflow; ++round) {
       ref_rows += (unsigned long long)n_cur * kZoomSamples;
       int n_nxt = 0;
       for (int iv = 0; iv < n_cur; ++iv) {
@@ -1443,13 +1447,14 @@ k_zoom(const Entry* __restrict__ entries, int64_t n, const PairInfo* __restrict_
                 const double sa = grid[k > 0 ? k - 1 : 0];
                 const double sb = grid[ke + 1 < cut - 1 ? ke + 1 : cut - 1];
                 if (sb > sa) {
-                  if (n_nxt < kZoomQueue) nxt[n_nxt] = Interval{sa, sb}; else overflow = true;
+                  if (n_nxt < qcap) nxt[n_nxt] = Interval{sa, sb}; else overflow = true;
                   ++n_nxt;
                 }
                 k = ke + 1;
               }
             }
             n_nxt = __shfl_sync(0xffffffffu, n_nxt, 0);
+            overflow = __shfl_sync(0xffffffffu, overflow, 0);
           }
         }
         __syncwarp();
@@ -1457,12 +1462,13 @@ k_zoom(const Entry* __restrict__ entries, int64_t n, const PairInfo* __restrict_
       Interval* t = cur;
       cur = nxt;
       nxt = t;
-      n_cur = n_nxt < kZoomQueue ? n_nxt : kZoomQueue;
+      n_cur = n_nxt < qcap ? n_nxt : qcap;
     }
-    if (lane == 0) {
+    if (lane == 0 && overflow) {
+      spill[atomicAdd(&ctr->overflow, 1ULL)] = ei;  // re-run with a larger queue
+    } else if (lane == 0) {
       atomicAdd(&ctr->zoom_rows, ref_rows);
       atomicAdd(&ctr->zoom_exec, exec_rows);
-      if (overflow) atomicExch(&ctr->overflow, 1ULL);
       if (have) {
         const unsigned long long slot = atomicAdd(&ctr->brackets, 1ULL);
         brackets[slot] = Bracket{en.pair, en.ia, en.ib, 0, blo, bhi, en.h};
@@ -1905,8 +1911,8 @@ k_fuse_large(Soa o, int64_t* __restrict__ idx, const int64_t* __restrict__ g_off
   }
   __syncthreads();
   for (int r = tid; r < n; r += kFuseLargeThreads) ix[r] = gi_[r];
-  for (int w = tid; w < n * words; w += kFuseLargeThreads) {
-    const int row = w / words, word = w % words;
+  for (int64_t w = tid; w < (int64_t)n * words; w += kFuseLargeThreads) {
+    const int row = (int)(w / words), word = (int)(w % words);
     const V3 pi{px[3 * row], px[3 * row + 1], px[3 * row + 2]};
     const double ti = th[row];
     uint32_t bits = 0;
@@ -2038,34 +2044,6 @@ __global__ void k_widen(const int32_t* a, int64_t* b, int64_t n) {
   if (i < n) b[i] = a[i];
 }
 
-// Exhaustive fine x fine rows of every pair at tau = 0 over an implicit
-// frontier: the exact 15-feature distance on every row, no cull -- the
-// roofline measurement of the distance kernel on real mesh rows.  Counts the
-// rows within h + 1e-9 (the resting test).
-__global__ void __launch_bounds__(32 * kStaticWarps, LTSG_STATIC_MINB)
-k_allpairs(const PairInfo* __restrict__ pairs, int64_t n_pairs, const BodyInfo* __restrict__ bodies,
-           const double* __restrict__ world, const int64_t* __restrict__ woff, unsigned long long* hits) {
-  extern __shared__ double s_stage[];
-  const Staged<32 * kStaticWarps> st{s_stage + threadIdx.x};
-  unsigned long long local = 0;
-  for (int64_t k = blockIdx.y; k < n_pairs; k += gridDim.y) {
-    const PairInfo p = pairs[k];
-    const int64_t na = bodies[p.ba].level_size[0], nb = bodies[p.bb].level_size[0];
-    const double* wa0 = world + (size_t)woff[p.ba] * kWorld;
-    const double* wb0 = world + (size_t)woff[p.bb] * kWorld;
-    for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < na * nb;
-         j += (int64_t)gridDim.x * blockDim.x) {
-      const double* wa = wa0 + (size_t)(j / nb) * kWorld;
-      const double* wb = wb0 + (size_t)(j % nb) * kWorld;
-      const double h = add(__ldg(wa + 9), __ldg(wb + 9));
-      stage_pair(st, load_world(wa), load_world(wb));
-      if (__dsqrt_rn(staged_dist_sq(st)) <= add(h, kRestSlop)) ++local;
-    }
-  }
-  for (int o = 16; o > 0; o >>= 1) local += __shfl_down_sync(0xffffffffu, local, o);
-  if ((threadIdx.x & 31) == 0 && local) atomicAdd(hits, local);
-}
-
 // Exhaustive fine x fine rows as register x broadcast tiles (the roofline
 // kernel; ccd._search with exhaustive=True evaluates the same rows,
 // ccd.py:385-391).  A work item is (pair, tile of kTileA fine triangles of
@@ -2164,7 +2142,6 @@ static int configure_kernels() {
     LTSG_CUDA(cudaFuncSetAttribute(k_screen, cudaFuncAttributeMaxDynamicSharedMemorySize, kScreenStageBytes));
     LTSG_CUDA(cudaFuncSetAttribute(k_screen_static, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                    kStaticStageBytes));
-    LTSG_CUDA(cudaFuncSetAttribute(k_allpairs, cudaFuncAttributeMaxDynamicSharedMemorySize, kAllpairsStageBytes));
     LTSG_CUDA(cudaFuncSetAttribute(k_allpairs_tile, cudaFuncAttributeMaxDynamicSharedMemorySize, kTileSmemBytes));
     done = 1;
   }
@@ -2611,16 +2588,33 @@ static int run_search(const ltsg_scene* sc, ltsg_result* out, ltsg_workspace* ws
   if (n_entries > 0) {
     Bracket* br;
     Interval* queue;
+    int64_t *spill_a, *spill_b;
     LTSG_TRY(ws_get(ws, "brackets", (size_t)n_entries, &br));
-    const int zblocks = (int)std::min<int64_t>((n_entries + kZoomWarps - 1) / kZoomWarps, 148 * 8);
-    LTSG_TRY(ws_get(ws, "zoomq", (size_t)zblocks * kZoomWarps * 2 * kZoomQueue, &queue));
-    k_zoom<<<zblocks, 32 * kZoomWarps, 0, st>>>(entries, n_entries, pr.pairs, pr.bodies, sc->tris, queue,
-                                                br, d_ctr);
-    LTSG_LAUNCHED();
-    LTSG_TRY(read_ctr(d_ctr, &h, st));
-    if (h.overflow) {
-      set_error("zoom interval queue overflow (more than %d pending intervals)", kZoomQueue);
-      return LTSG_ECAPACITY;
+    LTSG_TRY(ws_get(ws, "zoom_spill_a", (size_t)n_entries, &spill_a));
+    LTSG_TRY(ws_get(ws, "zoom_spill_b", (size_t)n_entries, &spill_b));
+    // first pass: every entry with kZoomQueue intervals per queue (LTSG_ZOOM_QUEUE overrides it, to
+    // exercise the spill path in tests); spilled entries re-run with 16x larger queues
+    int64_t qcap = kZoomQueue;
+    if (const char* q = getenv("LTSG_ZOOM_QUEUE")) qcap = std::max(1, atoi(q));
+    const int64_t* sel = nullptr;
+    int64_t n_zoom = n_entries;
+    while (true) {
+      const int zblocks = (int)std::min<int64_t>((n_zoom + kZoomWarps - 1) / kZoomWarps, 148 * 8);
+      LTSG_TRY(ws_get(ws, "zoomq", (size_t)zblocks * kZoomWarps * 2 * qcap, &queue));
+      LTSG_CUDA(cudaMemsetAsync(&d_ctr->overflow, 0, sizeof(unsigned long long), st));
+      k_zoom<<<zblocks, 32 * kZoomWarps, 0, st>>>(entries, n_zoom, sel, pr.pairs, pr.bodies, sc->tris, queue,
+                                                  (int)qcap, spill_a, br, d_ctr);
+      LTSG_LAUNCHED();
+      LTSG_TRY(read_ctr(d_ctr, &h, st));
+      if (h.overflow == 0) break;
+      n_zoom = (int64_t)h.overflow;
+      qcap *= 16;
+      if (qcap > ((int64_t)1 << 26)) {
+        set_error("zoom: %lld entries need more than %lld pending intervals", (long long)n_zoom, (long long)(qcap / 16));
+        return LTSG_ECAPACITY;
+      }
+      std::swap(spill_a, spill_b);  // the spilled list becomes the selection; the next pass spills into the other
+      sel = spill_b;
     }
     n_br = (int64_t)h.brackets;
     if (n_br > 0) {
@@ -2885,18 +2879,11 @@ static int run_allpairs(const ltsg_scene* sc, int64_t* rows, int64_t* hits, doub
     LTSG_TRY(ws_get(ws, "tile_rows", rowv.size(), &d_rows));
     LTSG_CUDA(cudaMemcpyAsync(d_items, items.data(), sizeof(int64_t) * items.size(), cudaMemcpyHostToDevice, st));
     LTSG_CUDA(cudaMemcpyAsync(d_rows, rowv.data(), sizeof(int64_t) * rowv.size(), cudaMemcpyHostToDevice, st));
-    const char* legacy = getenv("LTSG_ALLPAIRS_STAGED");
     Timer t;
     t.start(st);
-    if (legacy && legacy[0] == '1' && !out_dist) {
-      dim3 grid(148 * 8, (unsigned)std::min<int64_t>(sc->n_pairs, 65535));
-      k_allpairs<<<grid, 32 * kStaticWarps, kAllpairsStageBytes, st>>>(pr.pairs, sc->n_pairs, pr.bodies, world, woff,
-                                                                     d_hits);
-    } else {
-      const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(items.back(), 148LL * LTSG_TILE_MINB * 8));
-      k_allpairs_tile<<<grid, kTileA, kTileSmemBytes, st>>>(pr.pairs, sc->n_pairs, pr.bodies, world, woff, d_items, d_rows,
-                                               d_hits, out_dist);
-    }
+    const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(items.back(), 148LL * LTSG_TILE_MINB * 8));
+    k_allpairs_tile<<<grid, kTileA, kTileSmemBytes, st>>>(pr.pairs, sc->n_pairs, pr.bodies, world, woff, d_items,
+                                                          d_rows, d_hits, out_dist);
     t.stop(st);
     LTSG_CHECK_LAUNCH();
     *ms = t.ms();

@@ -143,12 +143,9 @@ def _tree_chunk(args):
     return build_surrogate_trees(corners, eps)
 
 
-def make_particles(ids, meshes, eps, states, workers=None):
-    """Batched make_particle for meshes sharing one triangle topology:
-    centres of mass, recentring and surrogate trees vectorised across
-    particles, trees built on `workers` processes for large batches."""
-    import os
-
+def _recentre(meshes, eps):
+    """Mass centres, recentred corners (P, n, 3, 3) and bounding radii of
+    meshes sharing one triangle topology, vectorised across meshes."""
     f = meshes[0][1]
     V = np.stack([np.asarray(v, dtype=np.float64) for v, _ in meshes])
     a, b, c = V[:, f[:, 0]], V[:, f[:, 1]], V[:, f[:, 2]]
@@ -157,6 +154,17 @@ def make_particles(ids, meshes, eps, states, workers=None):
     com = (dets[..., None] * (a + b + c)).sum(axis=1) / (24.0 * vol)[:, None]
     Vc = V - com[:, None, :]
     corners = np.stack([Vc[:, f[:, 0]], Vc[:, f[:, 1]], Vc[:, f[:, 2]]], axis=2)
+    radius = np.linalg.norm(Vc, axis=2).max(axis=1) + eps
+    return corners, radius
+
+
+def make_particles(ids, meshes, eps, states, workers=None):
+    """Batched make_particle for meshes sharing one triangle topology:
+    centres of mass, recentring and surrogate trees vectorised across
+    particles, trees built on `workers` processes for large batches."""
+    import os
+
+    corners, radius = _recentre(meshes, eps)
     P = len(meshes)
     workers = workers or min(os.cpu_count() or 1, 32)
     # fork-based workers only for big batches (bench setup, before CUDA starts)
@@ -169,7 +177,6 @@ def make_particles(ids, meshes, eps, states, workers=None):
         trees = [t for part in parts for t in part]
     else:
         trees = _tree_chunk((corners, eps))
-    radius = np.linalg.norm(Vc, axis=2).max(axis=1) + eps
     return [B.Particle(pid=int(i), tree=t, epsilon=float(eps), radius=float(r), timeline=B.timeline(st))
             for i, t, r, st in zip(ids, trees, radius, states)]
 
@@ -272,8 +279,11 @@ def config3(n_rocks: int = 20000, phi: float = 0.55, seed_offset: int = 3) -> Sc
                        {"eps": eps, "n_rocks": n_rocks, "phi_bounding": float(achieved)})
 
 
-def config4(n_pairs: int = 8192, subdiv: int = 3, dt: float = 0.1, seed_offset: int = 4) -> Scene:
-    """c4: moving icosphere pairs, v ~ N(0,1)^3, w ~ N(0,2)^3, gap U(0,0.5)."""
+def config4_raw(n_pairs: int = 8192, subdiv: int = 3, dt: float = 0.1, seed_offset: int = 4) -> dict:
+    """c4's seeded draws without building trees: per body its mesh (not yet
+    recentred), bounding radius and snapshot state (positions set), so a
+    fixture generator can rebuild chosen pairs of the bench workload with
+    the reference's own make_particle."""
     rng = np.random.default_rng(SEED + seed_offset)
     eps = 1e-3
     meshes = _noisy_icosphere_trees(rng, 2 * n_pairs, subdiv, 0.05, eps)
@@ -282,27 +292,30 @@ def config4(n_pairs: int = 8192, subdiv: int = 3, dt: float = 0.1, seed_offset: 
     spin = rng.normal(0.0, 2.0, size=(2 * n_pairs, 3))
     gaps = rng.uniform(0.0, 0.5, size=n_pairs)
     axes = unit_vectors(rng, n_pairs)
-    states = [B.state(np.zeros(3), velocity=vel[pid], rotation=quats[pid], angular_velocity=spin[pid])
-              for pid in range(2 * n_pairs)]
-    made = make_particles(range(2 * n_pairs), meshes, eps, states)
-    particles = {}
-    pairs = []
-    for k in range(n_pairs):
-        a, b = made[2 * k], made[2 * k + 1]
-        sep = a.radius + b.radius + gaps[k]
-        for p, sgn in ((a, -0.5), (b, 0.5)):
-            p.timeline.current.position = sgn * sep * axes[k]
-            p.timeline.old.position = p.timeline.current.position.copy()
-            particles[p.pid] = p
-        pairs.append((2 * k, 2 * k + 1))
-    return _pair_scene("c4", particles, pairs, dt,
-                       {"eps": eps, "tris": 20 * 4 ** subdiv, "n_pairs": n_pairs})
+    _, radius = _recentre(meshes, eps)
+    states = []
+    for pid in range(2 * n_pairs):
+        k = pid // 2
+        sep = radius[2 * k] + radius[2 * k + 1] + gaps[k]
+        pos = (0.5 if pid % 2 else -0.5) * sep * axes[k]
+        states.append(B.state(pos, velocity=vel[pid], rotation=quats[pid], angular_velocity=spin[pid]))
+    return {"eps": eps, "dt": dt, "meshes": meshes, "radius": radius, "states": states,
+            "pairs": [(2 * k, 2 * k + 1) for k in range(n_pairs)], "gaps": gaps, "axes": axes}
 
 
-def config5(n_particles: int = 2000, dt: float = 0.1, max_subdiv: int = 5,
-            seed_offset: int = 5) -> Scene:
-    """c5: polydisperse icospheres (20..20480 tris) and boxes, size ratio
-    100:1, non-overlapping packing, clusters of the swept-sphere graph."""
+def config4(n_pairs: int = 8192, subdiv: int = 3, dt: float = 0.1, seed_offset: int = 4) -> Scene:
+    """c4: moving icosphere pairs, v ~ N(0,1)^3, w ~ N(0,2)^3, gap U(0,0.5)."""
+    raw = config4_raw(n_pairs, subdiv, dt, seed_offset)
+    made = make_particles(range(2 * n_pairs), raw["meshes"], raw["eps"], raw["states"])
+    particles = {p.pid: p for p in made}
+    return _pair_scene("c4", particles, raw["pairs"], dt,
+                       {"eps": raw["eps"], "tris": 20 * 4 ** subdiv, "n_pairs": n_pairs})
+
+
+def config5_raw(n_particles: int = 2000, dt: float = 0.1, max_subdiv: int = 5, seed_offset: int = 5) -> dict:
+    """c5's seeded draws without building trees: per particle its mesh (not
+    yet recentred), kind, radius and snapshot state after the packing, the
+    swept-sphere pairs and their clusters."""
     from scipy.sparse import coo_matrix
     from scipy.sparse.csgraph import connected_components
     from scipy.spatial import cKDTree
@@ -314,26 +327,17 @@ def config5(n_particles: int = 2000, dt: float = 0.1, max_subdiv: int = 5,
     vel = rng.normal(0.0, 1.0, size=(n_particles, 3))
     spin = rng.normal(0.0, 1.0, size=(n_particles, 3))
     quats = random_quaternions(rng, n_particles)
-    cache = {}
-    particles = {}
+    meshes = []
     bound = np.empty(n_particles)
     for i in range(n_particles):
         kind = int(kinds[i])
-        if kind <= max_subdiv:
-            v, f = icosphere(kind)
-        else:
-            v, f = box((1.0, 0.8, 0.6))
-        key = (kind, float(radii[i]))
-        p = B.make_particle(i, v * radii[i], f, eps, B.state(
-            np.zeros(3), velocity=vel[i], rotation=quats[i], angular_velocity=spin[i]),
-            tree=cache.get(key))
-        cache[key] = p.tree
-        particles[i] = p
-        bound[i] = p.radius
+        v, f = icosphere(kind) if kind <= max_subdiv else box((1.0, 0.8, 0.6))
+        v = v * radii[i]
+        meshes.append((v, f))
+        bound[i] = float(np.linalg.norm(v - B.centre_of_mass(v, f), axis=1).max()) + eps  # make_particle's radius
     x, _ = _relax(rng, bound, 0.35, overlap=-0.002)
-    for i in range(n_particles):
-        particles[i].timeline.current.position = x[i].copy()
-        particles[i].timeline.old.position = x[i].copy()
+    states = [B.state(x[i].copy(), velocity=vel[i], rotation=quats[i], angular_velocity=spin[i])
+              for i in range(n_particles)]
     # swept bounding spheres over [0, dt]
     reach = bound + dt * np.linalg.norm(vel, axis=1)
     tree = cKDTree(x)
@@ -346,9 +350,28 @@ def config5(n_particles: int = 2000, dt: float = 0.1, max_subdiv: int = 5,
     pairs = [(int(a), int(b)) for a, b in ij]
     comp = label[ij[:, 0]] if len(ij) else np.zeros(0, dtype=np.int64)
     uniq, problem = np.unique(comp, return_inverse=True)
-    n_prob = len(uniq)
-    return Scene(name="c5", particles=particles, statics={}, pairs=pairs,
-                 problem=np.asarray(problem, dtype=np.int64), dt=np.full(n_prob, float(dt)),
+    return {"eps": eps, "dt": dt, "meshes": meshes, "kinds": kinds, "radii": radii, "radius": bound,
+            "states": states, "pairs": pairs, "problem": np.asarray(problem, dtype=np.int64),
+            "n_problems": len(uniq)}
+
+
+def config5(n_particles: int = 2000, dt: float = 0.1, max_subdiv: int = 5,
+            seed_offset: int = 5) -> Scene:
+    """c5: polydisperse icospheres (20..20480 tris) and boxes, size ratio
+    100:1, non-overlapping packing, clusters of the swept-sphere graph."""
+    raw = config5_raw(n_particles, dt, max_subdiv, seed_offset)
+    eps = raw["eps"]
+    cache = {}
+    particles = {}
+    for i in range(n_particles):
+        v, f = raw["meshes"][i]
+        key = (int(raw["kinds"][i]), float(raw["radii"][i]))
+        p = B.make_particle(i, v, f, eps, raw["states"][i], tree=cache.get(key))
+        cache[key] = p.tree
+        particles[i] = p
+    n_prob = raw["n_problems"]
+    return Scene(name="c5", particles=particles, statics={}, pairs=raw["pairs"],
+                 problem=raw["problem"], dt=np.full(n_prob, float(dt)),
                  t_base=np.zeros(n_prob), mode="cluster",
                  meta={"eps": eps, "n_particles": n_particles, "clusters": n_prob})
 

@@ -12,6 +12,9 @@ Outputs (all small, committed):
   scenes_ccd.npz       the reference's own test_ccd.py known-answer scenes
   scenes_crit2.npz     acceptance criterion 2's 200 seeded pairs (replayed)
   scenes_configs.npz   small c1..c5-shaped scenes (reference-built trees)
+  scenes_baseline.npz  c4 pairs and c5 clusters drawn from the bench workloads
+                       at their BASELINE shapes (1280-tri spinning pairs;
+                       20480-tri icospheres against 12-tri boxes)
 
 Each scene records the reference result, the raw (pre-fusion) contact list
 (captured by wrapping ccd.filter_contacts, which _search resolves as a
@@ -75,20 +78,20 @@ class Recorder:
         ccd.filter_contacts, ccd._feature_distances = self._f, self._d
 
 
-def pair_case(name, a, b, dt, exhaustive=False, widen=1e-3):
+def pair_case(name, a, b, dt, exhaustive=False, widen=1e-3, dedup=False):
     with Recorder() as r:
         res = ccd.pair_earliest_contact(a, b, dt, widen=widen, exhaustive=exhaustive)
-    return {"name": name, "mode": "pair", "bodies": [SC.encode_body(a), SC.encode_body(b)],
+    return {"name": name, "mode": "pair", "bodies": [SC.encode_body(a, dedup), SC.encode_body(b, dedup)],
             "pairs": np.array([[_bid(a), _bid(b)]], dtype=np.int64), "dt": float(dt),
             "widen": float(widen), "exhaustive": bool(exhaustive), "t_base": 0.0,
             "result": SC.encode_result(res, r.raw), "rows": int(r.rows)}
 
 
-def cluster_case(name, cluster, particles, statics, pairs, widen=1e-3):
+def cluster_case(name, cluster, particles, statics, pairs, widen=1e-3, dedup=False):
     with Recorder() as r:
         res = ccd.compute_effective_dt(cluster, particles, statics, pairs, widen=widen)
-    bodies = [SC.encode_body(p) for p in particles.values()] + \
-             [SC.encode_body(s) for s in statics.values()]
+    bodies = [SC.encode_body(p, dedup) for p in particles.values()] + \
+             [SC.encode_body(s, dedup) for s in statics.values()]
     return {"name": name, "mode": "cluster", "bodies": bodies,
             "pairs": np.array(list(pairs), dtype=np.int64).reshape(-1, 2),
             "dt": float(cluster.dt), "widen": float(widen), "exhaustive": False,
@@ -420,6 +423,128 @@ def gen_scenes_configs(rng):
     return {"cases": cases}
 
 
+# ------------------------------------------------------------------ bench-shaped scenes
+
+def _ref_body(raw, pid):
+    v, f = raw["meshes"][pid]
+    st = raw["states"][pid]
+    return ref_particle(pid, v, f, raw["eps"], position=st.position, velocity=st.velocity,
+                        rotation=st.rotation, angular_velocity=st.angular_velocity)
+
+
+def _c4_job(k):
+    raw = _BASE["c4"]
+    ia, ib = raw["pairs"][k]
+    t0 = time.time()
+    case = pair_case(f"c4_bench_pair_{k}", _ref_body(raw, ia), _ref_body(raw, ib), raw["dt"], dedup=True)
+    case["bench_index"] = int(k)
+    case["ref_seconds"] = time.time() - t0
+    return case
+
+
+def _c5_job(p):
+    raw = _BASE["c5"]
+    sel = np.flatnonzero(raw["problem"] == p)
+    pairs = [raw["pairs"][i] for i in sel]
+    members = sorted({x for pr in pairs for x in pr})
+    parts = {pid: _ref_body(raw, pid) for pid in members}
+    t0 = time.time()
+    case = cluster_case(f"c5_bench_cluster_{p}", Cluster(members=tuple(members), t_current=0.0, dt=raw["dt"]),
+                        parts, {}, pairs, dedup=True)
+    case["bench_index"] = int(p)
+    case["ref_seconds"] = time.time() - t0
+    return case
+
+
+_BASE = {}
+
+
+def c4_bench_picks(raw, n_hit=4, n_graze=3, n_other=3):
+    """Pairs of the c4 bench workload (BASELINE configs[3], 8192 pairs):
+    the ones whose closing speed along the centre line covers the gap by the
+    widest margin (hits), the ones it covers by about zero (grazes), and
+    seeded random others."""
+    dt = raw["dt"]
+    n = len(raw["pairs"])
+    margin = np.empty(n)
+    for k, (ia, ib) in enumerate(raw["pairs"]):
+        closing = float(np.dot(raw["states"][ia].velocity - raw["states"][ib].velocity, raw["axes"][k]))
+        margin[k] = closing * dt - raw["gaps"][k]
+    hits = list(np.argsort(-margin)[:n_hit])
+    graze = [int(k) for k in np.argsort(np.abs(margin)) if k not in hits][:n_graze]
+    rng = np.random.default_rng(7)
+    others = [int(k) for k in rng.permutation(n) if k not in hits and k not in graze][:n_other]
+    return [int(k) for k in hits] + graze + others
+
+
+def c5_bench_picks(raw, big_kind=5, box_kind=6, max_members=6, limit=5):
+    """Clusters of the c5 bench workload (BASELINE configs[4]) holding a
+    20480-triangle icosphere and a 12-triangle box, smallest first."""
+    out = []
+    for p in range(raw["n_problems"]):
+        sel = np.flatnonzero(raw["problem"] == p)
+        members = sorted({x for i in sel for x in raw["pairs"][i]})
+        kinds = raw["kinds"][members]
+        if (kinds == big_kind).any() and (kinds == box_kind).any() and len(members) <= max_members:
+            out.append((len(members), p))
+    return [p for _, p in sorted(out)[:limit]]
+
+
+def c5_impact_picks(raw, big_kind=5, box_kind=6, limit=3):
+    """Sphere-box pairs of the c5 bench workload (inside its large clusters)
+    whose closing speed covers the bounding-sphere gap within dt by the
+    widest margin: each becomes a one-pair cluster (the 20480-triangle tree
+    descending against the box's [12, 3, 1] levels, with an impact)."""
+    dt = raw["dt"]
+    cand = []
+    for i, (a, b) in enumerate(raw["pairs"]):
+        ka, kb = raw["kinds"][a], raw["kinds"][b]
+        if {int(ka), int(kb)} != {big_kind, box_kind}:
+            continue
+        sa, sb = raw["states"][a], raw["states"][b]
+        d = sb.position - sa.position
+        dist = float(np.linalg.norm(d))
+        gap = dist - raw["radius"][a] - raw["radius"][b]
+        closing = float(np.dot(sa.velocity - sb.velocity, d / dist))
+        cand.append((closing * dt - gap, i))
+    return [i for _, i in sorted(cand, reverse=True)[:limit]]
+
+
+def _c5_pair_job(i):
+    raw = _BASE["c5"]
+    a, b = raw["pairs"][i]
+    parts = {a: _ref_body(raw, a), b: _ref_body(raw, b)}
+    t0 = time.time()
+    case = cluster_case(f"c5_bench_pair_{i}", Cluster(members=(a, b), t_current=0.0, dt=raw["dt"]),
+                        parts, {}, [(a, b)], dedup=True)
+    case["bench_pair"] = int(i)
+    case["ref_seconds"] = time.time() - t0
+    return case
+
+
+def gen_scenes_baseline(workers=8):
+    """c4 pairs and c5 clusters taken from the bench workloads themselves
+    (scenes.config4_raw / config5_raw at their BASELINE sizes), rebuilt with
+    the reference's make_particle and run through the reference."""
+    import multiprocessing as mp
+
+    _BASE["c4"] = S.config4_raw()
+    _BASE["c5"] = S.config5_raw()
+    c4 = c4_bench_picks(_BASE["c4"])
+    c5 = c5_bench_picks(_BASE["c5"])
+    c5p = c5_impact_picks(_BASE["c5"])
+    print("c4 pairs", c4, "c5 clusters", c5, "c5 impact pairs", c5p, flush=True)
+    with mp.get_context("fork").Pool(workers) as pool:
+        r5 = pool.map_async(_c5_job, c5, chunksize=1)
+        r5p = pool.map_async(_c5_pair_job, c5p, chunksize=1)
+        r4 = pool.map_async(_c4_job, c4, chunksize=1)
+        cases = r4.get() + r5.get() + r5p.get()
+    for c in cases:
+        print(c["name"], "collision", c["result"]["collision"], "raw", len(c["result"]["raw"]["t"]),
+              "rows", c["rows"], f"{c['ref_seconds']:.1f}s", flush=True)
+    return {"cases": cases}
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--only", default="")
@@ -434,6 +559,7 @@ def main():
         "scenes_ccd": gen_scenes_ccd,
         "scenes_configs": lambda: gen_scenes_configs(np.random.default_rng(105)),
         "scenes_crit2": lambda: gen_scenes_crit2(limit=40 if args.quick else 200),
+        "scenes_baseline": gen_scenes_baseline,
     }
     del rng
     for name, job in jobs.items():

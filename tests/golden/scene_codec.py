@@ -8,11 +8,25 @@ import numpy as np
 from paper_2309_15417_b200 import bodies as B
 
 
-def encode_tree(tree):
+def encode_tree(tree, dedup=False):
+    """Levels as arrays.  With `dedup`, the fine level's corners are stored
+    as unique vertices plus int32 corner indices (the fine corners are the
+    mesh's recentred vertices gathered per face, so this is lossless) and a
+    constant epsilon as one value: large meshes stay small on disk."""
     levels = []
-    for lvl in tree.levels:
-        rec = {"corners": np.asarray(lvl.corners, dtype=np.float64),
-               "epsilon": np.asarray(lvl.epsilon, dtype=np.float64)}
+    for li, lvl in enumerate(tree.levels):
+        corners = np.asarray(lvl.corners, dtype=np.float64)
+        eps = np.asarray(lvl.epsilon, dtype=np.float64)
+        if dedup and li == 0:
+            v, inv = np.unique(corners.reshape(-1, 3), axis=0, return_inverse=True)
+            rec = {"fine_v": v, "fine_f": inv.reshape(-1, 3).astype(np.int32)}
+            assert np.array_equal(v[rec["fine_f"]].view(np.uint64), corners.view(np.uint64))
+            if len(eps) and np.all(eps.view(np.uint64) == eps[:1].view(np.uint64)):
+                rec["epsilon_const"] = float(eps[0])
+            else:
+                rec["epsilon"] = eps
+        else:
+            rec = {"corners": corners, "epsilon": eps}
         if lvl.children is not None:
             ch = [np.asarray(c, dtype=np.int64) for c in lvl.children]
             rec["child_ptr"] = np.cumsum([0] + [len(c) for c in ch]).astype(np.int64)
@@ -28,20 +42,24 @@ def decode_tree(levels):
         if "child_ptr" in rec:
             ptr, idx = rec["child_ptr"], rec["child_idx"]
             children = [idx[ptr[i]:ptr[i + 1]] for i in range(len(ptr) - 1)]
-        out.append(B.SurrogateLevel(corners=np.asarray(rec["corners"]),
-                                    epsilon=np.asarray(rec["epsilon"]), children=children))
+        if "fine_v" in rec:
+            corners = np.ascontiguousarray(rec["fine_v"][rec["fine_f"]])
+            eps = rec["epsilon"] if "epsilon" in rec else np.full(len(corners), rec["epsilon_const"])
+        else:
+            corners, eps = rec["corners"], rec["epsilon"]
+        out.append(B.SurrogateLevel(corners=np.asarray(corners), epsilon=np.asarray(eps), children=children))
     return B.SurrogateTree(levels=out)
 
 
-def encode_body(body):
+def encode_body(body, dedup=False):
     if hasattr(body, "timeline"):
         s = body.timeline.current
-        return {"kind": "particle", "id": int(body.pid), "tree": encode_tree(body.tree),
+        return {"kind": "particle", "id": int(body.pid), "tree": encode_tree(body.tree, dedup),
                 "epsilon": float(body.epsilon),
                 "position": np.asarray(s.position, float), "velocity": np.asarray(s.velocity, float),
                 "rotation": np.asarray(s.rotation, float),
                 "angular_velocity": np.asarray(s.angular_velocity, float), "t": float(s.t)}
-    return {"kind": "static", "id": int(body.sid), "tree": encode_tree(body.tree),
+    return {"kind": "static", "id": int(body.sid), "tree": encode_tree(body.tree, dedup),
             "epsilon": float(body.epsilon)}
 
 

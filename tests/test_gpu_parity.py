@@ -148,7 +148,7 @@ def run_gpu(G, case, exhaustive=None):
     return batch
 
 
-def check_case(G, case, want=None, want_rows=None, exhaustive=None):
+def check_case(G, case, want=None, want_rows=None, exhaustive=None, check_spinning_rows=False):
     want = case["result"] if want is None else want
     batch = run_gpu(G, case, exhaustive)
     res = batch.result(0)
@@ -185,6 +185,12 @@ def check_case(G, case, want=None, want_rows=None, exhaustive=None):
         for k in ("tri_a", "tri_b"):
             got_f[k] = want_f[k]
         compare_contacts(got_f, want_f, label=label + " fused", **tol)
+        if want_rows is not None and check_spinning_rows:
+            # the sample grids depend on no transcendental (counts from the
+            # Lipschitz speed, children windows from flagged samples), so the
+            # row count matches unless a flag sits within ulps of its threshold
+            st = batch.stats
+            assert st["rows_screen"] + st["rows_zoom"] + st["rows_bisect"] == want_rows, label
 
 
 def _ids(name):
@@ -202,6 +208,18 @@ def test_reference_test_scenes(G, idx):
 def test_config_shaped_scenes(G, idx):
     case = golden("scenes_configs")["cases"][idx]
     check_case(G, case, want_rows=case["rows"])
+
+
+@pytest.mark.parametrize("idx", range(len(golden("scenes_baseline")["cases"])),
+                         ids=_ids("scenes_baseline"))
+def test_bench_shaped_scenes(G, idx):
+    """c4 pairs and c5 clusters drawn from the bench workloads at their
+    BASELINE shapes (1280-triangle spinning icospheres, v ~ N(0,1),
+    w ~ N(0,2), gap U(0,0.5), dt 0.1; 20480-triangle icospheres against
+    12-triangle boxes), run by the reference itself: raw and fused
+    contacts, dt, first_contact and the reference's row count."""
+    case = golden("scenes_baseline")["cases"][idx]
+    check_case(G, case, want_rows=case["rows"], check_spinning_rows=True)
 
 
 def test_acceptance_criterion2_pairs(G):
@@ -306,3 +324,51 @@ def test_cluster_config_vs_oracle(G):
         assert got[p].collision == ref.collision
         assert abs(got[p].dt - ref.dt) <= TAU_TOL
         compare_contacts(got[p].contacts, SC.encode_contacts(ref.contacts), rtol=RTOL, atol=TAU_TOL)
+
+
+# ---------------------------------------------------------------- large fusion groups
+
+def _synthetic_contacts(rng, groups):
+    """Raw contacts in body-pair groups of the given sizes: positions in a few
+    tight clumps (chains of near points join through the union-find), ties in
+    t, several thresholds."""
+    out = []
+    for (ba, bb), n in groups:
+        centres = rng.normal(size=(max(n // 40, 1), 3))
+        for i in range(n):
+            c = centres[rng.integers(len(centres))]
+            pos = c + rng.normal(scale=rng.choice([2e-3, 2e-2]), size=3)
+            nrm = rng.normal(size=3)
+            nrm /= np.linalg.norm(nrm)
+            t = float(rng.choice([0.0, 0.05, rng.uniform(0, 0.1)]))
+            out.append(O.Contact(ba, bb, pos, nrm, float(rng.uniform(0, 0.01)), t, int(rng.integers(0, 5000)),
+                                 int(rng.integers(0, 5000)), float(rng.choice([0.002, 0.01, 0.02]))))
+    rng.shuffle(out)
+    return out
+
+
+@pytest.mark.parametrize("sizes", [(257,), (256, 300), (600, 3, 900)], ids=["257", "256+300", "600+3+900"])
+def test_fusion_large_groups_bit_exact(G, sizes):
+    """Groups above k_fuse_block's 256-record cap go through k_fuse_large;
+    checked bit for bit against the oracle's filter_contacts (itself pinned
+    to the reference's fusion goldens)."""
+    rng = np.random.default_rng(sum(sizes))
+    groups = [((k, k + 11), n) for k, n in enumerate(sizes)]
+    raw = _synthetic_contacts(rng, groups)
+    want = SC.encode_contacts(O.fuse(raw))
+    contacts = [G.ContactPoint(c.body_a, c.body_b, c.position, c.normal, c.depth, c.t, c.tri_a, c.tri_b,
+                               c.threshold) for c in raw]
+    compare_contacts(G.filter_contacts(contacts), want, label=f"large fusion {sizes}")
+
+
+def test_zoom_spill_matches_unbounded_reference(G, monkeypatch):
+    """The reference's pending-interval list is unbounded (ccd.py:261-303).
+    With the first-pass zoom queue forced down to 1 interval per entry, every
+    entry that fans out spills and re-runs with larger queues; results and
+    the reference's zoom row counts are unchanged."""
+    monkeypatch.setenv("LTSG_ZOOM_QUEUE", "1")
+    cases = [c for c in golden("scenes_crit2")["cases"] if c["result"]["collision"]][:40]
+    cases += [c for c in golden("scenes_baseline")["cases"] if c["result"]["collision"]][:3]
+    assert cases
+    for case in cases:
+        check_case(G, case, want_rows=case["rows"])

@@ -99,3 +99,45 @@ def test_acceptance_criterion2_pairs_bit_exact():
             ex = run_case(O, case, exhaustive=True)
             compare_result(ex, case["exhaustive_result"], raw=ex.raw, label=case["name"] + " ex")
             assert sum(ex.stats.values()) == case["exhaustive_rows"]
+
+
+# bench-shaped scenes (c4 at 1280 triangles, c5 20480-triangle icospheres vs
+# boxes): the cheapest ones keep the CPU suite within minutes; every case is
+# checked against the GPU in tests/test_gpu_parity.py
+_BASELINE_CPU = [c["name"] for c in golden("scenes_baseline")["cases"] if c["ref_seconds"] < 10.0][:4]
+
+
+@pytest.mark.parametrize("name", _BASELINE_CPU)
+def test_bench_shaped_scenes_bit_exact(name):
+    case = next(c for c in golden("scenes_baseline")["cases"] if c["name"] == name)
+    res = run_case(O, case)
+    compare_result(res, case["result"], raw=res.raw, label=case["name"])
+    assert sum(res.stats.values()) == case["rows"]
+
+
+def test_bench_shaped_scenes_come_from_the_bench_workloads():
+    """The fixture bodies are the bench scenes' bodies: same snapshot states
+    (bit for bit) as scenes.config4_raw / config5_raw at their BASELINE sizes."""
+    from paper_2309_15417_b200 import scenes
+
+    cases = golden("scenes_baseline")["cases"]
+    raws = {"c4": scenes.config4_raw(), "c5": scenes.config5_raw()}
+    assert sum(c["name"].startswith("c4_") for c in cases) >= 8
+    assert sum(c["name"].startswith("c5_") for c in cases) >= 2
+    assert sum(c["result"]["collision"] for c in cases if c["name"].startswith("c4_")) >= 3
+    for case in cases:
+        raw = raws[case["name"][:2]]
+        for b in case["bodies"]:
+            st = raw["states"][b["id"]]
+            for f in ("position", "velocity", "rotation", "angular_velocity"):
+                np.testing.assert_array_equal(b[f], getattr(st, f), err_msg=f"{case['name']} body {b['id']} {f}")
+        if case["name"].startswith("c5_bench_cluster"):
+            sel = np.flatnonzero(raw["problem"] == case["bench_index"])
+            assert [tuple(raw["pairs"][i]) for i in sel] == [tuple(p) for p in case["pairs"]]
+        if case["name"].startswith("c4_"):
+            assert tuple(raw["pairs"][case["bench_index"]]) == tuple(case["pairs"][0])
+        sizes = [len(lv["fine_f"]) for b in case["bodies"] for lv in b["tree"][:1] if "fine_f" in lv]
+        if case["name"].startswith("c4_"):
+            assert sizes == [1280, 1280]
+        else:
+            assert 20480 in sizes
