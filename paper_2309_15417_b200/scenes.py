@@ -24,6 +24,23 @@ from . import bodies as B
 
 SEED = 230915417
 
+# Process-pool start method of the scene builders.  "fork" is cheapest; a
+# caller that has already initialised CUDA (bench.py building its second
+# workload) switches to "forkserver" so no worker inherits a CUDA context.
+MP_CONTEXT = "fork"
+
+
+def _pool(workers):
+    import multiprocessing as mp
+
+    return mp.get_context(MP_CONTEXT).Pool(workers)
+
+
+def _workers(workers=None):
+    import os
+
+    return workers or min(os.cpu_count() or 1, 32)
+
 
 # ---------------------------------------------------------------- meshes
 
@@ -162,23 +179,57 @@ def make_particles(ids, meshes, eps, states, workers=None):
     """Batched make_particle for meshes sharing one triangle topology:
     centres of mass, recentring and surrogate trees vectorised across
     particles, trees built on `workers` processes for large batches."""
-    import os
-
     corners, radius = _recentre(meshes, eps)
     P = len(meshes)
-    workers = workers or min(os.cpu_count() or 1, 32)
-    # fork-based workers only for big batches (bench setup, before CUDA starts)
+    workers = _workers(workers)
+    # worker processes only for big batches (bench setup)
     if P >= 1024 and workers > 1:
-        import multiprocessing as mp
-
         chunks = np.array_split(np.arange(P), min(workers * 4, P))
-        with mp.get_context("fork").Pool(workers) as pool:
+        with _pool(workers) as pool:
             parts = pool.map(_tree_chunk, [(corners[ch], eps) for ch in chunks])
         trees = [t for part in parts for t in part]
     else:
         trees = _tree_chunk((corners, eps))
     return [B.Particle(pid=int(i), tree=t, epsilon=float(eps), radius=float(r), timeline=B.timeline(st))
             for i, t, r, st in zip(ids, trees, radius, states)]
+
+
+def _each_chunk(specs):
+    out = []
+    for pid, v, f, eps, st, key in specs:
+        out.append(B.make_particle(pid, v, f, eps, st))
+    return out
+
+
+def make_particles_each(specs, workers=None, share=None):
+    """B.make_particle for every (pid, vertices, faces, eps, state, key) of
+    `specs` (meshes of any topology), on worker processes for big batches.
+    Specs with an equal non-None `key` share the tree of the first one
+    (identical meshes).  Same particles as the serial loop."""
+    workers = _workers(workers)
+    first = {}
+    todo = []
+    for sp in specs:
+        key = sp[5]
+        if key is None or key not in first:
+            if key is not None:
+                first[key] = sp[0]
+            todo.append(sp)
+    if len(todo) >= 256 and workers > 1:
+        chunks = [todo[i::workers * 4] for i in range(workers * 4)]
+        with _pool(workers) as pool:
+            parts = pool.map(_each_chunk, chunks)
+        built = {p.pid: p for part in parts for p in part}
+    else:
+        built = {p.pid: p for p in _each_chunk(todo)}
+    out = {}
+    for pid, v, f, eps, st, key in specs:
+        if pid in built:
+            out[pid] = built[pid]
+        else:
+            src = built[first[key]]
+            out[pid] = B.make_particle(pid, v, f, eps, st, tree=src.tree)
+    return out
 
 
 def config1(n_pairs: int = 1024, subdiv: int = 3, seed_offset: int = 1) -> Scene:
@@ -256,13 +307,13 @@ def config3(n_rocks: int = 20000, phi: float = 0.55, seed_offset: int = 3) -> Sc
     rng = np.random.default_rng(SEED + seed_offset)
     eps = 0.005
     radii = np.exp(rng.uniform(np.log(0.5), np.log(5.0), size=n_rocks))
-    particles = {}
-    bound = np.empty(n_rocks)
+    specs = []
     for i in range(n_rocks):
         v, f = rock(rng)
         q = random_quaternions(rng, 1)[0]
-        particles[i] = B.make_particle(i, v * radii[i], f, eps, B.state(np.zeros(3), rotation=q))
-        bound[i] = particles[i].radius
+        specs.append((i, v * radii[i], f, eps, B.state(np.zeros(3), rotation=q), None))
+    particles = make_particles_each(specs)
+    bound = np.array([particles[i].radius for i in range(n_rocks)])
     x, side = _relax(rng, bound, phi)
     for i in range(n_rocks):
         particles[i].timeline.current.position = x[i].copy()
@@ -361,14 +412,9 @@ def config5(n_particles: int = 2000, dt: float = 0.1, max_subdiv: int = 5,
     100:1, non-overlapping packing, clusters of the swept-sphere graph."""
     raw = config5_raw(n_particles, dt, max_subdiv, seed_offset)
     eps = raw["eps"]
-    cache = {}
-    particles = {}
-    for i in range(n_particles):
-        v, f = raw["meshes"][i]
-        key = (int(raw["kinds"][i]), float(raw["radii"][i]))
-        p = B.make_particle(i, v, f, eps, raw["states"][i], tree=cache.get(key))
-        cache[key] = p.tree
-        particles[i] = p
+    particles = make_particles_each(
+        [(i, raw["meshes"][i][0], raw["meshes"][i][1], eps, raw["states"][i],
+          (int(raw["kinds"][i]), float(raw["radii"][i]))) for i in range(n_particles)])
     n_prob = raw["n_problems"]
     return Scene(name="c5", particles=particles, statics={}, pairs=raw["pairs"],
                  problem=raw["problem"], dt=np.full(n_prob, float(dt)),
