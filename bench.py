@@ -1,24 +1,39 @@
 """Benchmark of the B200 narrow phase.
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
-                    [--config c1] [--pairs P]
+                    [--config c1] [--pairs P] [--exhaustive] [--only]
 
 One step = one batched narrow-phase pass (ltsg_search) over the whole
-workload of the configuration: for c1, 1024 static pairs of 1280-triangle
-noisy icospheres (BASELINE.json configs[0]).  Inputs are seeded synthetic
-scenes (no dataset exists for this path).  Rank 0 prints ONE JSON line.
+workload of a configuration.  The headline workload is c1: 1024 static pairs
+of 1280-triangle noisy icospheres (BASELINE.json configs[0]).  With the
+default arguments on one GPU the same run also measures every other
+BASELINE configuration (c1 exhaustive, c2, c3, c4, c5) and reports them
+under `configs`; `--only` (or any non-default --config / --pairs /
+--exhaustive) measures just the named workload.  Inputs are seeded
+synthetic scenes (no dataset exists for this path).  Rank 0 prints ONE
+JSON line.
 
-  value    reference-equivalent triangle-pair tests per second (the rows the
-           reference's _feature_distances evaluates for the same search:
-           screen + zoom + bisection), inputs resident in HBM, device time
-  e2e      the same metric through the public batched API
-           (`ccd.earliest_contacts`) from host bodies: packing, H2D copies,
-           the search and the D2H copy of every result inside the timed region
-  roofline the exact-distance kernel (k_screen_static for static batches,
-           k_screen for moving ones): 984 FP64 flops per exact row over its
-           CUDA-event time, against the FP64 DFMA peak measured in this run
-  cpu_baseline  the CPU oracle (numpy restatement of the reference) on a
-           bounded sample of the same workload, on this host's cores
+Per workload:
+  value        reference-equivalent triangle-pair tests per second: the rows
+               the reference's _feature_distances evaluates for the same
+               searches (screen + zoom + bisection), inputs resident in HBM,
+               device time.  Rows settled by a certified cull count (their
+               decision is identical); `rows_executed_per_s` and
+               `exact_rows_per_s` give the rows the GPU actually evaluated.
+  e2e          the same metric through the public batched API
+               (`ccd.earliest_contacts` / `ccd.effective_dts`) from host
+               bodies: packing, H2D copies, the search and the D2H copy of
+               every result inside the timed region
+  roofline     the exact-distance kernel (k_screen_static for static
+               batches, k_screen for moving ones): 984 FP64 flops per exact
+               row over its CUDA-event time, against the FP64 DFMA peak
+               measured in this run
+  cpu_baseline the CPU oracle (numpy restatement of the reference, pinned
+               bit-exact to it) on a bounded sample of the same workload, on
+               this host's cores, one single-threaded process per core
+  parity       the GPU results of the sampled problems against the oracle's
+               (bit-exact for static / non-spinning searches, the SURVEY
+               §8(c) tolerances for spinning ones)
 
 `--impl reference` times the CPU oracle alone (the reference is pure
 Python/numpy and cannot travel to the GPU box; the oracle is bit-identical
@@ -27,14 +42,19 @@ to it on the golden fixtures) and prints the same line with "impl".
 
 from __future__ import annotations
 
-import argparse
-import json
 import os
-import statistics
-import subprocess
-import sys
-import threading
-import time
+
+# one BLAS thread per process: the CPU legs run one process per core
+for _v in ("OMP_NUM_THREADS", "OPENBLAS_NUM_THREADS", "MKL_NUM_THREADS"):
+    os.environ.setdefault(_v, "1")
+
+import argparse  # noqa: E402
+import json  # noqa: E402
+import statistics  # noqa: E402
+import subprocess  # noqa: E402
+import sys  # noqa: E402
+import threading  # noqa: E402
+import time  # noqa: E402
 
 REPO = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, REPO)
@@ -46,8 +66,20 @@ CONFIG_DOC = {
     "c2": "4096 domino boxes (12 tris), neighbour pairs within bounding-sphere overlap, eps 1e-3, dt 0",
     "c3": "20k convex rocks (~124 tris) packed at phi~0.55, bounding-sphere pairs, eps 0.005, dt 0",
     "c4": "8192 moving pairs of 1280-tri icospheres, v~N(0,1), w~N(0,2), gap U(0,0.5), eps 1e-3, dt 0.1",
-    "c5": "2000 polydisperse mixed meshes, clusters of the swept-sphere graph, eps 1e-3, dt 0.1",
+    "c5": "2000 polydisperse mixed meshes (12..20480 tris), clusters of the swept-sphere graph, eps 1e-3, dt 0.1",
 }
+# the workloads of a full run: (label, config, exhaustive)
+WORKLOADS = (("c1", "c1", False), ("c1_exhaustive", "c1", True), ("c2", "c2", False), ("c3", "c3", False),
+             ("c4", "c4", False), ("c5", "c5", False))
+# CPU-leg sample per worker process (about 10-30 s of numpy on the box's cores)
+CPU_PER_WORKER = {"c1": 8, "c1_exhaustive": 1, "c2": 64, "c3": 32, "c4": 1, "c5": 2}
+# c5 clusters the oracle samples: at most this many pairs each (its largest
+# cluster, ~1200 pairs sharing one bound, is hours of numpy)
+C5_SAMPLE_MAX_PAIRS = 8
+# ... and meshes of at most this many triangles (the 5120/20480-triangle
+# spheres' clusters take minutes each in numpy; their parity is pinned by
+# tests/golden/scenes_baseline.npz instead)
+C5_SAMPLE_MAX_TRIS = 1280
 
 
 def _env_rank():
@@ -74,8 +106,10 @@ def scene_problems(scene):
         return [([(scene.body(a), scene.body(b))], float(scene.dt[k]), 0.0)
                 for k, (a, b) in enumerate(scene.pairs)]
     probs = []
+    order = np.argsort(scene.problem, kind="stable")
+    bounds = np.searchsorted(scene.problem[order], np.arange(scene.n_problems + 1))
     for p in range(scene.n_problems):
-        sel = np.flatnonzero(scene.problem == p)
+        sel = order[bounds[p]:bounds[p + 1]]
         probs.append(([(scene.body(scene.pairs[i][0]), scene.body(scene.pairs[i][1])) for i in sel],
                       float(scene.dt[p]), float(scene.t_base[p])))
     return probs
@@ -86,7 +120,7 @@ def committed_traffic(config: str, kernel: str) -> dict:
     (profiles/rNN_traffic_<config>.json, written by tools/traffic.py)."""
     import glob
 
-    for path in sorted(glob.glob(os.path.join(REPO, "profiles", f"r*_traffic_{config}.json")), reverse=True):
+    for path in sorted(glob.glob(os.path.join(REPO, "profiles", f"r*_traffic_{config}*.json")), reverse=True):
         try:
             d = json.load(open(path))
         except (OSError, ValueError):
@@ -158,12 +192,17 @@ class ClockSampler:
 
 # ------------------------------------------------------------------ CPU arms
 
-def _oracle_job(args):
-    os.environ.setdefault("OMP_NUM_THREADS", "1")
-    os.environ.setdefault("OPENBLAS_NUM_THREADS", "1")
+def _bid(b):
+    return int(b.pid) if hasattr(b, "timeline") else int(b.sid)
+
+
+_CPU_PROBLEMS = []
+_CPU_EXHAUSTIVE = False
+
+
+def _oracle_job(idx):
     from oracle import narrow_oracle as O
 
-    idx = args
     pairs, dt, tb = _CPU_PROBLEMS[idx]
     t0 = time.perf_counter()
     if len(pairs) == 1 and tb == 0.0:
@@ -178,35 +217,47 @@ def _oracle_job(args):
             plist.append((_bid(a), _bid(b)))
         res = O.compute_effective_dt(SimpleNamespace(dt=dt, t_current=tb), parts, stats, plist)
     rows = res.stats.get("rows", 0) + res.stats.get("zoom_rows", 0) + res.stats.get("bisect_rows", 0)
-    return rows, len(res.raw), time.perf_counter() - t0
+    res.raw = []  # parity compares the fused contacts; keep the pickle small
+    return rows, time.perf_counter() - t0, res
 
 
-def _bid(b):
-    return int(b.pid) if hasattr(b, "timeline") else int(b.sid)
+class OraclePool:
+    """`workers` single-threaded oracle processes forked over `problems`
+    (started before the timed region; forked before this process touches
+    CUDA)."""
+
+    def __init__(self, problems, workers: int, exhaustive: bool = False):
+        import multiprocessing as mp
+
+        global _CPU_PROBLEMS, _CPU_EXHAUSTIVE
+        _CPU_PROBLEMS = problems
+        _CPU_EXHAUSTIVE = exhaustive
+        self.workers = workers
+        self.pool = mp.get_context("fork").Pool(workers) if workers > 1 else None
+        if self.pool is not None:  # the workers are up before anything is timed
+            self.pool.map(_noop, range(workers), chunksize=1)
+
+    def run(self, idx):
+        """(rows, wall seconds, per-problem seconds, results) over problems[idx]."""
+        t0 = time.perf_counter()
+        if self.pool is None:
+            out = [_oracle_job(i) for i in idx]
+        else:
+            idx = list(idx)
+            out = self.pool.map(_oracle_job, idx, chunksize=max(1, len(idx) // (8 * self.workers)))
+        wall = time.perf_counter() - t0
+        return sum(o[0] for o in out), wall, [o[1] for o in out], [o[2] for o in out]
+
+    def close(self):
+        global _CPU_PROBLEMS
+        if self.pool is not None:
+            self.pool.close()
+            self.pool.join()
+        _CPU_PROBLEMS = []
 
 
-_CPU_PROBLEMS = []
-_CPU_EXHAUSTIVE = False
-
-
-def cpu_sample(problems, n_items: int, workers: int, exhaustive: bool = False):
-    """Run the oracle over the first n_items problems on `workers` processes."""
-    import multiprocessing as mp
-
-    global _CPU_PROBLEMS, _CPU_EXHAUSTIVE
-    _CPU_PROBLEMS = problems
-    _CPU_EXHAUSTIVE = exhaustive
-    idx = list(range(min(n_items, len(problems))))
-    t0 = time.perf_counter()
-    if workers <= 1:
-        out = [_oracle_job(i) for i in idx]
-    else:
-        with mp.get_context("fork").Pool(workers) as pool:
-            out = pool.map(_oracle_job, idx, chunksize=1)
-    wall = time.perf_counter() - t0
-    rows = sum(o[0] for o in out)
-    contacts = sum(o[1] for o in out)
-    return rows, contacts, wall, len(idx)
+def _noop(_):
+    return 0
 
 
 def cpu_cores():
@@ -216,6 +267,50 @@ def cpu_cores():
         return os.cpu_count() or 1
 
 
+def cpu_model():
+    try:
+        for ln in open("/proc/cpuinfo"):
+            if ln.startswith("model name"):
+                return ln.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    import platform
+
+    return platform.processor() or "unknown"
+
+
+def sample_indices(label, scene, problems, workers):
+    """The bounded CPU sample of a workload: the first problems in index
+    order (c5: the first clusters with at most C5_SAMPLE_MAX_PAIRS pairs)."""
+    n = CPU_PER_WORKER.get(label, 2) * workers
+    if label == "c5":
+        ok = [p for p, pr in enumerate(problems) if len(pr[0]) <= C5_SAMPLE_MAX_PAIRS
+              and max(b.tree.levels[0].size if hasattr(b.tree.levels[0], "size") else len(b.tree.levels[0].corners)
+                      for pair in pr[0] for b in pair) <= C5_SAMPLE_MAX_TRIS]
+        return ok[:n]
+    return list(range(min(n, len(problems))))
+
+
+def cpu_leg(label, scene, problems, exhaustive, workers):
+    idx = sample_indices(label, scene, problems, workers)
+    pool = OraclePool(problems, workers, exhaustive)
+    try:
+        rows, wall, per, results = pool.run(idx)
+    finally:
+        pool.close()
+    what = (f"clusters with <= {C5_SAMPLE_MAX_PAIRS} pairs and <= {C5_SAMPLE_MAX_TRIS}-triangle meshes"
+            if label == "c5" else "problems")
+    cpu = {"value": rows / wall if wall > 0 else 0.0, "unit": "tests/s", "cores": workers, "kind": "port",
+           "sample": f"the first {len(idx)} {what} of {len(problems)} ({scene.name}"
+                     f"{' exhaustive' if exhaustive else ''}) through the numpy oracle, {workers} single-threaded "
+                     f"processes, {wall:.1f} s wall",
+           "tests": rows, "wall_s": wall, "problems": len(idx),
+           "single_thread_s_per_problem": (sum(per) / len(per)) if per else None,
+           "single_thread_tests_per_s": rows / sum(per) if per and sum(per) > 0 else None,
+           "cpu_model": cpu_model()}
+    return cpu, idx, results
+
+
 def run_reference(args, rank, world):
     """--impl reference: the CPU oracle on this host's cores."""
     if rank != 0:
@@ -223,17 +318,26 @@ def run_reference(args, rank, world):
     scene = build_scene(args.config, 0, args.pairs)
     problems = scene_problems(scene)
     workers = max(1, min(cpu_cores(), args.cpu_workers or cpu_cores()))
-    per_step = max(workers, 1)
-    for _ in range(args.warmup if args.warmup < 1 else 1):
-        cpu_sample(problems, min(per_step, 2), min(workers, 2))
-    rows = contacts = 0
+    label = args.config + ("_exhaustive" if args.exhaustive else "")
+    per_step = CPU_PER_WORKER.get(label, 1) * workers
+    if label == "c5":
+        pool_idx = sample_indices("c5", scene, problems, workers * 64)
+    else:
+        pool_idx = list(range(len(problems)))
+    pool = OraclePool(problems, workers, args.exhaustive)
+    rows = 0
     wall = 0.0
-    for s in range(args.steps):
-        r, c, w, _ = cpu_sample(problems[s * per_step % max(len(problems), 1):] or problems,
-                                per_step, workers)
-        rows += r
-        contacts += c
-        wall += w
+    per_all = []
+    try:
+        pool.run(pool_idx[:min(len(pool_idx), workers)])  # warm-up: imports, first-touch
+        for s in range(args.steps):
+            idx = [pool_idx[(s * per_step + i) % len(pool_idx)] for i in range(per_step)]
+            r, w, per, _ = pool.run(idx)
+            rows += r
+            wall += w
+            per_all += per
+    finally:
+        pool.close()
     value = rows / wall if wall > 0 else 0.0
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": "tests/s",
@@ -241,123 +345,92 @@ def run_reference(args, rank, world):
         "ms_per_step": 1e3 * wall / max(args.steps, 1), "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic (seeded, BASELINE.json shapes)",
-        "config": {"workload": args.config, "description": CONFIG_DOC[args.config],
+        "config": {"workload": label, "description": CONFIG_DOC[args.config],
                    "sample_problems_per_step": per_step},
         "cpu_baseline": {"value": value, "unit": "tests/s", "cores": workers, "kind": "port",
-                         "sample": f"{per_step} {args.config} problems per step x {args.steps} steps"},
+                         "sample": f"{per_step} {label} problems per step x {args.steps} steps, one "
+                                   f"single-threaded process per core",
+                         "cpu_model": cpu_model(),
+                         "single_thread_s_per_problem": sum(per_all) / len(per_all) if per_all else None},
         "e2e": {"value": value, "unit": "tests/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
-        "contacts_per_s": contacts / wall if wall > 0 else 0.0,
     }
     print(json.dumps(line), flush=True)
     return 0
 
 
+# ------------------------------------------------------------------ parity
+
+def parity(batch, idx, oracle_results, spinning):
+    """GPU results of the sampled problems against the oracle's."""
+    import numpy as np
+
+    checked = exact = coll_ok = count_ok = 0
+    max_dt = max_first = max_pos = max_nrm = max_depth = 0.0
+    for i, ref in zip(idx, oracle_results):
+        got = batch.result(i)
+        checked += 1
+        coll_ok += got.collision == ref.collision
+        same_n = len(got.contacts) == len(ref.contacts)
+        count_ok += same_n
+        max_dt = max(max_dt, abs(got.dt - ref.dt))
+        if got.first_contact is not None and ref.first_contact is not None:
+            max_first = max(max_first, abs(got.first_contact - ref.first_contact))
+        bit = got.dt == ref.dt and got.first_contact == ref.first_contact and same_n
+        if same_n:
+            for x, y in zip(got.contacts, ref.contacts):
+                dp = float(np.max(np.abs(np.asarray(x.position) - y.position) / (1.0 + np.abs(y.position))))
+                dn = float(np.max(np.abs(np.asarray(x.normal) - y.normal)))
+                max_pos, max_nrm = max(max_pos, dp), max(max_nrm, dn)
+                max_depth = max(max_depth, abs(x.depth - y.depth))
+                bit = bit and np.array_equal(x.position, y.position) and np.array_equal(x.normal, y.normal) \
+                    and x.depth == y.depth and x.t == y.t and x.tri_a == y.tri_a and x.tri_b == y.tri_b
+        exact += bool(bit)
+    tol = 1e-9
+    within = (coll_ok == checked and count_ok == checked and max_dt <= tol and max_first <= tol
+              and max_pos <= tol and max_nrm <= tol and max_depth <= tol)
+    return {"checked": checked, "bit_exact": exact, "collision_match": coll_ok, "contact_count_match": count_ok,
+            "max_dt_err": max_dt, "max_first_contact_err": max_first, "max_position_rel_err": max_pos,
+            "max_normal_err": max_nrm, "max_depth_err": max_depth,
+            "contract": "bit-exact" if not spinning else "sin/cos searches: |dt|, |t| <= 1e-9, values <= 1e-9",
+            "ok": bool(within and (spinning or exact == checked))}
+
+
 # ------------------------------------------------------------------ GPU arm
 
-def run_ours(args, rank, world, local_rank):
-    import ctypes as C
-
+def gpu_workload(label, config, exhaustive, scene, problems, hs, steps, warmup, flush, dist, cold_steps=0):
+    """Device-resident timing, then the e2e loop through the public API."""
     import numpy as np
     import torch
 
-    from paper_2309_15417_b200 import _lib, ccd, packing
+    from paper_2309_15417_b200 import ccd
 
-    # host setup first: the scene builders fork worker processes, which must
-    # happen before this process starts CUDA
-    t_build = time.perf_counter()
-    scene = build_scene(args.config, rank, args.pairs)
-    problems = scene_problems(scene)
-    hs = packing.pack(problems)
-    t_build = time.perf_counter() - t_build
-
-    # CPU baseline leg (rank 0 only): the oracle on this host's cores over a
-    # bounded sample of the same workload, run before this process starts CUDA
-    cpu = None
-    if rank == 0 and not args.no_cpu:
-        workers = max(1, min(cpu_cores(), 64))
-        per_worker = 1 if args.exhaustive else 2  # an exhaustive c1 pair is ~40 s of numpy
-        r, c, w, n = cpu_sample(problems, min(len(problems), per_worker * workers), workers, args.exhaustive)
-        cpu = {"value": r / w if w > 0 else 0.0, "unit": "tests/s", "cores": workers, "kind": "port",
-               "sample": f"{n} {args.config} problems (of {len(problems)}) through the numpy oracle, "
-                         f"{workers} processes, {w:.1f} s wall"}
-
-    torch.cuda.set_device(local_rank)
-    dist = None
-    if world > 1:
-        import torch.distributed as dist
-
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
-    # The scene holds ~10^6 long-lived numpy objects (the reference's tree
-    # format keeps one children array per surrogate triangle); exclude them
-    # from cyclic GC scans, as a long-running engine would.
-    import gc
-
-    gc.collect()
-    gc.freeze()
     ds = ccd.DeviceScene(hs)
     torch.cuda.synchronize()
-
-    peak_tflops = C.c_double(0.0)
-    peak_ms = C.c_double(0.0)
-    _lib.check(_lib.lib().ltsg_fp64_peak(C.byref(peak_tflops), C.byref(peak_ms),
-                                         C.c_void_p(torch.cuda.current_stream().cuda_stream)),
-               "ltsg_fp64_peak")
-
-    flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")  # > 126 MB L2
-
-    # roofline of the 15-feature distance itself: every fine x fine row of a
-    # sample of pairs evaluated exactly at tau = 0 (ltsg_exhaustive_rows)
-    allpairs = None
-    if scene.mode == "pair" and not args.no_allpairs:
-        sub = problems[: min(len(problems), 16)]
-        ds_sub = ccd.DeviceScene(packing.pack(sub))
-        sc_sub = ds_sub.struct(1e-3, False)
-        rows_c, hits_c, ms_c = C.c_int64(), C.c_int64(), C.c_double()
-        for _ in range(2):
-            _lib.check(_lib.lib().ltsg_exhaustive_rows(C.byref(sc_sub), C.byref(rows_c), C.byref(hits_c),
-                                                       C.byref(ms_c), _lib.workspace().handle,
-                                                       C.c_void_p(torch.cuda.current_stream().cuda_stream)),
-                       "ltsg_exhaustive_rows")
-        ach = rows_c.value * FLOPS_PER_TEST / (ms_c.value * 1e-3) / 1e12
-        allpairs = {"kernel": "k_allpairs_tile", "pairs": len(sub), "rows": rows_c.value, "hits": hits_c.value,
-                    "ms": ms_c.value, "tests_per_s": rows_c.value / (ms_c.value * 1e-3),
-                    "achieved_tflops": ach, "frac": ach / peak_tflops.value}
-        del ds_sub
 
     def barrier():
         torch.cuda.synchronize()
         if dist is not None:
             dist.barrier()
 
-    # ---- device-resident steps
-    for _ in range(args.warmup):
-        res = ccd.run_scene(ds, exhaustive=args.exhaustive)
-    stats = []
-    step_ms = []
+    for _ in range(warmup):
+        res = ccd.run_scene(ds, exhaustive=exhaustive)
+    stats, step_ms = [], []
     barrier()
-    # clocks and throttle reasons sampled across both timed loops (device, e2e)
-    clocks = ClockSampler(local_rank).__enter__()
-    for _ in range(args.steps):
+    for _ in range(steps):
         flush.fill_(1)
         ev0 = torch.cuda.Event(enable_timing=True)
         ev1 = torch.cuda.Event(enable_timing=True)
         ev0.record()
-        res = ccd.run_scene(ds, exhaustive=args.exhaustive)
+        res = ccd.run_scene(ds, exhaustive=exhaustive)
         ev1.record()
         ev1.synchronize()
         step_ms.append(ev0.elapsed_time(ev1))
         stats.append(res.stats)
     barrier()
-    total_ms = sum(step_ms)
-    tests = sum(s["rows_screen"] + s["rows_zoom"] + s["rows_bisect"] for s in stats)
-    contacts = sum(s["n_raw"] for s in stats)
-    # per-kernel device time of the screen from the library's own events
-    screen_ms = sum(s.get("ms_screen", 0.0) for s in stats)
-    screen_rows = sum(s["rows_screen"] for s in stats)
-    exact_rows = sum(s.get("rows_screen_exact", s["rows_screen"]) for s in stats)
-    exact_ms = sum(s.get("ms_exact", 0.0) for s in stats)
-    expand_ms = sum(s.get("ms_expand", 0.0) for s in stats)
-    launches = sum(s.get("launches", 0) for s in stats)
+    del ds
+
+    def tot(k):
+        return sum(s.get(k, 0) for s in stats)
 
     # ---- end to end through the public API from host bodies.  Every step
     # packs the bodies' current states, copies the step's inputs H2D from
@@ -365,8 +438,6 @@ def run_ours(args, rank, world, local_rank):
     # trees are immutable geometry: the public API keeps them
     # resident on the device after the first call (ccd.DeviceScene
     # cache_trees), so a step uploads the kinematic states and pair tables.
-    # The same loop with the tree cache off (every step uploads the compact
-    # geometry too) is reported as e2e_cold.
     pairs_obj = [pr[0][0] for pr in problems] if scene.mode == "pair" else None
 
     def e2e_loop(n_warm, n_timed):
@@ -378,7 +449,7 @@ def run_ours(args, rank, world, local_rank):
             tm = ph if i >= n_warm else None
             t0 = time.perf_counter()
             if scene.mode == "pair":
-                out = ccd.earliest_contacts(pairs_obj, scene.dt, timings=tm, exhaustive=args.exhaustive)
+                out = ccd.earliest_contacts(pairs_obj, scene.dt, timings=tm, exhaustive=exhaustive)
             else:
                 out = ccd._run_problems(problems, widen=1e-3, timings=tm)
             t1 = time.perf_counter()
@@ -387,103 +458,224 @@ def run_ours(args, rank, world, local_rank):
         return ms, ph, out
 
     ccd.set_tree_cache(True)
-    e2e_ms, phases, out = e2e_loop(args.warmup, args.steps)
-    cold_steps = min(args.steps, 5)
-    ccd.set_tree_cache(False)
-    cold_ms, cold_phases, _ = e2e_loop(2, cold_steps)
-    ccd.set_tree_cache(True)
-    clocks.__exit__(None, None, None)
+    e2e_ms, phases, out = e2e_loop(min(warmup, 2), steps)
+    cold = None
+    if cold_steps:
+        ccd.set_tree_cache(False)
+        cold_ms, cold_ph, _ = e2e_loop(2, cold_steps)
+        ccd.set_tree_cache(True)
+        cold = (cold_ms, cold_ph)
     h2d = float(np.mean(phases.pop("h2d_bytes"))) if phases.get("h2d_bytes") else float(hs.nbytes)
-    h2d_cold = float(np.mean(cold_phases.pop("h2d_bytes"))) if cold_phases.get("h2d_bytes") else float(hs.nbytes)
     d2h = sum(v.nbytes for v in out.contacts.values()) + out.dt.nbytes + out.collision.nbytes \
         + out.first_contact.nbytes + out.fused_offset.nbytes
+    static = tot("ms_exact") > 0
+    kern_ms = tot("ms_exact") if static else tot("ms_screen")
+    return {"label": label, "config": config, "exhaustive": exhaustive, "step_ms": step_ms, "stats": stats,
+            "tot": tot, "e2e_ms": e2e_ms, "phases": phases, "h2d": h2d, "d2h": d2h, "cold": cold,
+            "kernel": "k_screen_static" if static else "k_screen", "kern_ms": kern_ms, "last": res,
+            "problems": len(problems), "pairs": len(hs.pair_problem), "tris": int(hs.n_tris)}
 
-    # ---- reduce over ranks (max time, sum work)
-    vals = torch.tensor([total_ms, sum(e2e_ms), float(tests), float(contacts)], dtype=torch.float64,
-                        device="cuda")
-    if dist is not None:
-        t_max = vals[:2].clone()
-        dist.all_reduce(t_max, op=dist.ReduceOp.MAX)
-        w_sum = vals[2:].clone()
-        dist.all_reduce(w_sum, op=dist.ReduceOp.SUM)
-        total_ms, e2e_total = float(t_max[0]), float(t_max[1])
-        tests_all, contacts_all = float(w_sum[0]), float(w_sum[1])
-    else:
-        e2e_total = sum(e2e_ms)
-        tests_all, contacts_all = float(tests), float(contacts)
 
+def summarize(m, steps, peak, cpu, par, world, total_ms=None, e2e_total=None, tests_all=None, contacts_all=None):
+    tot = m["tot"]
+    total_ms = sum(m["step_ms"]) if total_ms is None else total_ms
+    e2e_total = sum(m["e2e_ms"]) if e2e_total is None else e2e_total
+    tests = tot("rows_screen") + tot("rows_zoom") + tot("rows_bisect")
+    tests_all = tests if tests_all is None else tests_all
+    contacts_all = tot("n_raw") if contacts_all is None else contacts_all
+    exact_rows = tot("rows_screen_exact")
+    achieved = exact_rows * FLOPS_PER_TEST / (m["kern_ms"] * 1e-3) / 1e12 if m["kern_ms"] > 0 else 0.0
+    traffic = committed_traffic(m["label"], m["kernel"])
+    return {
+        "value": tests_all / (total_ms * 1e-3), "unit": "tests/s", "ms_per_step": total_ms / steps, "steps": steps,
+        "tests_per_step": tests_all / steps,
+        "rows_executed_per_s": tot("rows_executed") / (sum(m["step_ms"]) * 1e-3),
+        "exact_rows_per_s": exact_rows / (sum(m["step_ms"]) * 1e-3),
+        "contacts_per_s": contacts_all / (total_ms * 1e-3),
+        "raw_contacts_per_step": contacts_all / steps,
+        "problems": m["problems"], "pairs": m["pairs"], "triangle_records": m["tris"],
+        "e2e": {"value": tests_all / (e2e_total * 1e-3), "unit": "tests/s",
+                "h2d_bytes_per_step": int(m["h2d"]), "d2h_bytes_per_step": int(m["d2h"]),
+                "ms_per_step": e2e_total / steps,
+                "phases_ms_per_step": {k: sum(v) / len(v) for k, v in m["phases"].items()}},
+        "roofline": {"bound": "fp64", "kernel": m["kernel"], "achieved": achieved, "peak": peak,
+                     "unit": "TFLOP/s", "frac": achieved / peak if peak else None,
+                     "traffic": traffic.get("dram_bytes_per_step"),
+                     "traffic_unit": "DRAM bytes per step (sum over the kernel's launches of one search)",
+                     "traffic_source": traffic.get("source"),
+                     "kernel_ms_per_step": m["kern_ms"] / steps,
+                     "exact_rows_per_step": exact_rows / steps},
+        "breakdown_ms_per_step": {
+            "screen": tot("ms_screen") / steps, "exact": tot("ms_exact") / steps,
+            "expand": tot("ms_expand") / steps, "refine": tot("ms_refine") / steps,
+            "contacts_fusion": tot("ms_contacts") / steps,
+            "generations": m["stats"][-1].get("generations"), "candidates": m["stats"][-1].get("candidates")},
+        "gpu_launches": tot("launches"),
+        "cpu_baseline": cpu,
+        "parity": par,
+    }
+
+
+def run_ours(args, rank, world, local_rank):
+    import ctypes as C
+
+    import torch
+
+    from paper_2309_15417_b200 import _lib, ccd, packing, scenes
+
+    full = (world == 1 and not args.only and args.config == "c1" and not args.exhaustive and args.pairs is None)
+    plan = list(WORKLOADS) if full else \
+        [(args.config + ("_exhaustive" if args.exhaustive else ""), args.config, args.exhaustive)]
+
+    # ---- host phase, before this process starts CUDA (the scene builders and
+    # the CPU legs fork worker processes): scenes, packing, CPU baselines
+    t_build = time.perf_counter()
+    built = {}
+    prep = []
+    workers = max(1, min(cpu_cores(), 64))
+    for label, config, exhaustive in plan:
+        t0 = time.perf_counter()
+        if config not in built:
+            sc = build_scene(config, rank, args.pairs)
+            probs = scene_problems(sc)
+            built[config] = (sc, probs, packing.pack(probs))
+        scene, problems, hs = built[config]
+        setup_s = time.perf_counter() - t0
+        cpu = idx = ores = None
+        if rank == 0 and not args.no_cpu:
+            cpu, idx, ores = cpu_leg(label, scene, problems, exhaustive, workers)
+        spinning = any(float(np_norm(b.timeline.current.angular_velocity)) > 0.0
+                       for pr in problems for pair in pr[0] for b in pair if hasattr(b, "timeline")) \
+            and float(max(scene.dt)) > 0.0
+        prep.append((label, config, exhaustive, scene, problems, hs, cpu, idx, ores, spinning, setup_s))
+    t_build = time.perf_counter() - t_build
+    scenes.MP_CONTEXT = "forkserver"  # nothing forks from a CUDA process below
+
+    torch.cuda.set_device(local_rank)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+    # The scenes hold ~10^6 long-lived numpy objects (the reference's tree
+    # format keeps one children array per surrogate triangle); exclude them
+    # from cyclic GC scans, as a long-running engine would.
+    import gc
+
+    gc.collect()
+    gc.freeze()
+
+    peak_tflops = C.c_double(0.0)
+    peak_ms = C.c_double(0.0)
+    _lib.check(_lib.lib().ltsg_fp64_peak(C.byref(peak_tflops), C.byref(peak_ms),
+                                         C.c_void_p(torch.cuda.current_stream().cuda_stream)),
+               "ltsg_fp64_peak")
+    peak = peak_tflops.value
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")  # > 126 MB L2
+
+    # roofline of the 15-feature distance itself: every fine x fine row of a
+    # sample of c1 pairs evaluated exactly at tau = 0 (ltsg_exhaustive_rows)
+    allpairs = None
+    head = prep[0]
+    if head[3].mode == "pair" and not args.no_allpairs:
+        sub = head[4][: min(len(head[4]), 16)]
+        ds_sub = ccd.DeviceScene(packing.pack(sub))
+        sc_sub = ds_sub.struct(1e-3, False)
+        rows_c, hits_c, ms_c = C.c_int64(), C.c_int64(), C.c_double()
+        for _ in range(2):
+            _lib.check(_lib.lib().ltsg_exhaustive_rows(C.byref(sc_sub), C.byref(rows_c), C.byref(hits_c),
+                                                       C.byref(ms_c), _lib.workspace().handle,
+                                                       C.c_void_p(torch.cuda.current_stream().cuda_stream)),
+                       "ltsg_exhaustive_rows")
+        ach = rows_c.value * FLOPS_PER_TEST / (ms_c.value * 1e-3) / 1e12
+        allpairs = {"kernel": "k_allpairs_tile", "pairs": len(sub), "rows": rows_c.value, "hits": hits_c.value,
+                    "ms": ms_c.value, "tests_per_s": rows_c.value / (ms_c.value * 1e-3),
+                    "achieved_tflops": ach, "frac": ach / peak}
+        del ds_sub
+
+    clocks = ClockSampler(local_rank).__enter__()
+    results = {}
+    for i, (label, config, exhaustive, scene, problems, hs, cpu, idx, ores, spinning, setup_s) in enumerate(prep):
+        steps = args.steps if i == 0 else min(args.steps, args.secondary_steps)
+        m = gpu_workload(label, config, exhaustive, scene, problems, hs, steps, args.warmup, flush, dist,
+                         cold_steps=min(args.steps, 5) if i == 0 else 0)
+        par = parity(m["last"], idx, ores, spinning) if ores is not None else None
+        if i == 0 and dist is not None:
+            tot = m["tot"]
+            vals = torch.tensor([sum(m["step_ms"]), sum(m["e2e_ms"]),
+                                 float(tot("rows_screen") + tot("rows_zoom") + tot("rows_bisect")),
+                                 float(tot("n_raw"))], dtype=torch.float64, device="cuda")
+            t_max = vals[:2].clone()
+            dist.all_reduce(t_max, op=dist.ReduceOp.MAX)
+            w_sum = vals[2:].clone()
+            dist.all_reduce(w_sum, op=dist.ReduceOp.SUM)
+            s = summarize(m, steps, peak, cpu, par, world, float(t_max[0]), float(t_max[1]), float(w_sum[0]),
+                          float(w_sum[1]))
+        else:
+            s = summarize(m, steps, peak, cpu, par, world)
+        s["setup_s"] = setup_s
+        s["description"] = CONFIG_DOC[config] + (", exhaustive (every fine x fine row screened)" if exhaustive else "")
+        results[label] = (m, s)
+        del m["last"]
+    clocks.__exit__(None, None, None)
 
     if rank == 0:
-        value = tests_all / (total_ms * 1e-3)
-        # flops of the rows that actually ran the exact 15-feature distance
-        # static batches time the exact kernel alone; moving batches run the
-        # culls and the exact distance in one kernel (k_screen)
-        kern_ms = exact_ms if exact_ms > 0 else screen_ms
-        traffic = committed_traffic(args.config, "k_screen_static" if exact_ms > 0 else "k_screen")
-        achieved = exact_rows * FLOPS_PER_TEST / (kern_ms * 1e-3) / 1e12 if kern_ms > 0 else 0.0
+        label0 = prep[0][0]
+        m0, s0 = results[label0]
+        steps0 = args.steps
+        cold = m0["cold"]
         line = {
-            "metric": METRIC, "value": value, "unit": "tests/s", "n_gpus": world,
-            "steps": args.steps, "warmup": args.warmup, "ms_per_step": total_ms / args.steps,
+            "metric": METRIC, "value": s0["value"], "unit": "tests/s", "n_gpus": world,
+            "steps": steps0, "warmup": args.warmup, "ms_per_step": s0["ms_per_step"],
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic (seeded, BASELINE.json shapes)",
-            "config": {"workload": args.config + (" exhaustive" if args.exhaustive else ""),
-                       "description": CONFIG_DOC[args.config],
-                       "problems_per_gpu": len(problems), "pairs_per_gpu": len(hs.pair_problem),
-                       "triangle_records_per_gpu": int(hs.n_tris),
+            "config": {"workload": label0.replace("_", " "), "description": s0["description"],
+                       "problems_per_gpu": s0["problems"], "pairs_per_gpu": s0["pairs"],
+                       "triangle_records_per_gpu": s0["triangle_records"],
                        "l2": "flushed (256 MiB write) before every timed step",
                        "parallelism": f"weak: {world} independent shards"},
-            "contacts_per_s": contacts_all / (total_ms * 1e-3),
-            "tests_per_step": tests_all / args.steps,
-            "raw_contacts_per_step": contacts_all / args.steps,
-            "e2e": {"value": tests_all / (e2e_total * 1e-3), "unit": "tests/s",
-                    "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
-                    "ms_per_step": e2e_total / args.steps,
-                    "path": "ccd.earliest_contacts(host bodies) -> pack -> H2D of the step's states and "
-                            "pair tables (surrogate trees device-resident after the first call) -> "
-                            "ltsg_search -> D2H",
-                    "phases_ms_per_step": {k: sum(v) / len(v) for k, v in phases.items()}},
-            "e2e_cold": {"value": tests_all / args.steps * cold_steps / (sum(cold_ms) * 1e-3)
-                         if dist is None else None,
-                         "unit": "tests/s", "steps": cold_steps,
-                         "h2d_bytes_per_step": int(h2d_cold), "ms_per_step": sum(cold_ms) / cold_steps,
-                         "path": "as e2e with the device tree cache off: every step also uploads the "
-                                 "compact surrogate trees and rebuilds the records on the device",
-                         "phases_ms_per_step": {k: sum(v) / len(v) for k, v in cold_phases.items()}},
-            "roofline": {"bound": "fp64", "kernel": "k_screen_static" if exact_ms > 0 else "k_screen",
-                         "achieved": achieved,
-                         "peak": peak_tflops.value, "unit": "TFLOP/s",
-                         "frac": achieved / peak_tflops.value if peak_tflops.value else None,
-                         "traffic": traffic.get("dram_bytes_per_step"),
-                         "traffic_unit": "DRAM bytes per step (sum over the kernel's launches of one search)",
-                         "traffic_source": traffic.get("source"),
-                         "peak_source": "in-run DFMA microbenchmark (ltsg_fp64_peak); "
-                                        "MEASURED_PEAKS.json has no FP64 entry",
-                         "flops_per_test": FLOPS_PER_TEST,
-                         "kernel_ms_per_step": kern_ms / args.steps,
-                         "screen_ms_per_step": screen_ms / args.steps,
-                         "expand_ms_per_step": expand_ms / args.steps,
-                         "screen_rows_per_step": screen_rows / args.steps,
-                         "screen_rows_exact_per_step": exact_rows / args.steps,
-                         "note": "rows settled by the certified culls (sphere, separating axes) are "
-                                 "counted as tests in `value` (their decision is identical) but not in "
-                                 "`achieved`; screen_ms also covers the seeds and the child expansion "
-                                 "with its culls (expand_ms)"},
+            "contacts_per_s": s0["contacts_per_s"],
+            "tests_per_step": s0["tests_per_step"],
+            "rows_executed_per_s": s0["rows_executed_per_s"],
+            "exact_rows_per_s": s0["exact_rows_per_s"],
+            "raw_contacts_per_step": s0["raw_contacts_per_step"],
+            "e2e": dict(s0["e2e"], path="public batched API from host bodies: pack -> H2D of the step's states "
+                                        "and pair tables (surrogate trees device-resident after the first "
+                                        "call) -> ltsg_search -> D2H of every result"),
+            "e2e_cold": None if cold is None else {
+                "value": s0["tests_per_step"] * len(cold[0]) / (sum(cold[0]) * 1e-3) if dist is None else None,
+                "unit": "tests/s", "steps": len(cold[0]), "ms_per_step": sum(cold[0]) / len(cold[0]),
+                "h2d_bytes_per_step": int(sum(cold[1].get("h2d_bytes", [0])) / max(len(cold[1].get("h2d_bytes", [1])), 1)),
+                "path": "as e2e with the device tree cache off: every step also uploads the compact surrogate "
+                        "trees and rebuilds the records on the device"},
+            "roofline": dict(s0["roofline"], peak_source="in-run DFMA microbenchmark (ltsg_fp64_peak); "
+                                                         "MEASURED_PEAKS.json has no FP64 entry",
+                             flops_per_test=FLOPS_PER_TEST,
+                             note="achieved counts only rows that ran the exact 15-feature distance; "
+                                  "rows settled by the certified culls count in `value`"),
             "roofline_distance_kernel": allpairs,
-            "gpu_launches": launches,
-            "breakdown_ms_per_step": {
-                "screen": screen_ms / args.steps,
-                "refine": sum(s.get("ms_refine", 0.0) for s in stats) / args.steps,
-                "contacts_fusion": sum(s.get("ms_contacts", 0.0) for s in stats) / args.steps,
-                "generations": stats[-1].get("generations"),
-                "candidates": stats[-1].get("candidates")},
+            "gpu_launches": s0["gpu_launches"],
+            "breakdown_ms_per_step": s0["breakdown_ms_per_step"],
             "clocks": clocks.summary(),
-            "cpu_baseline": cpu,
+            "cpu_baseline": s0["cpu_baseline"],
+            "parity": s0["parity"],
             "setup_s": t_build,
+            "value_note": "value/e2e count reference-equivalent tests (the rows the reference evaluates for the "
+                          "same searches, certified-culled rows included); rows_executed_per_s and "
+                          "exact_rows_per_s count what the GPU evaluated",
         }
+        if len(results) > 1:
+            line["configs"] = {lab: s for lab, (m, s) in results.items() if lab != label0}
         print(json.dumps(line), flush=True)
     if dist is not None:
         dist.destroy_process_group()
     return 0
+
+
+def np_norm(v):
+    import numpy as np
+
+    return np.linalg.norm(np.asarray(v, dtype=np.float64))
 
 
 def main(argv=None) -> int:
@@ -494,7 +686,9 @@ def main(argv=None) -> int:
     ap.add_argument("--impl", choices=("ours", "reference"), default="ours")
     ap.add_argument("--config", choices=tuple(CONFIG_DOC), default="c1")
     ap.add_argument("--pairs", type=int, default=None, help="override the workload size")
-    ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
+    ap.add_argument("--only", action="store_true", help="measure only --config (no secondary workloads)")
+    ap.add_argument("--secondary-steps", type=int, default=5, help="timed steps of the secondary workloads")
+    ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline / parity legs")
     ap.add_argument("--cpu-workers", type=int, default=0)
     ap.add_argument("--exhaustive", action="store_true",
                     help="screen every fine x fine pair (ccd.py:387-388) instead of the multiscale walk")
