@@ -2551,6 +2551,10 @@ static int run_search(const ltsg_scene* sc, ltsg_result* out, ltsg_workspace* ws
       unsigned long long nn = 0;
       LTSG_CUDA(cudaMemcpyAsync(&nn, gen_cnt + 1, sizeof(nn), cudaMemcpyDeviceToHost, st));
       LTSG_CUDA(cudaStreamSynchronize(st));
+      if (tr.on)
+        fprintf(stderr, "[ltsg trace] gen %d front %lld rows %llu window %llu sphere %llu exact %llu next %llu ms %.3f\n",
+                (int)out->generations, (long long)n_front, h.rows - before.rows, h.rows_window - before.rows_window,
+                h.rows_sphere - before.rows_sphere, h.screen_exact - before.screen_exact, nn, t_screen.ms());
       out->candidates += n_front;
       out->generations += 1;
       n_front = (int64_t)nn;
