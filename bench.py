@@ -468,11 +468,13 @@ def gpu_workload(label, config, exhaustive, scene, problems, hs, steps, warmup, 
     h2d = float(np.mean(phases.pop("h2d_bytes"))) if phases.get("h2d_bytes") else float(hs.nbytes)
     d2h = sum(v.nbytes for v in out.contacts.values()) + out.dt.nbytes + out.collision.nbytes \
         + out.first_contact.nbytes + out.fused_offset.nbytes
-    static = tot("ms_exact") > 0
-    kern_ms = tot("ms_exact") if static else tot("ms_screen")
+    static = float(max(scene.dt)) == 0.0
+    moving_split = tot("ms_exact") > 0  # moving batches: the exact distances run in k_mexact
+    kern_ms = tot("ms_exact") if (static or moving_split) else tot("ms_screen")
     return {"label": label, "config": config, "exhaustive": exhaustive, "step_ms": step_ms, "stats": stats,
             "tot": tot, "e2e_ms": e2e_ms, "phases": phases, "h2d": h2d, "d2h": d2h, "cold": cold,
-            "kernel": "k_screen_static" if static else "k_screen", "kern_ms": kern_ms, "last": res,
+            "kernel": "k_screen_static" if static else ("k_mexact" if moving_split else "k_screen"),
+            "kern_ms": kern_ms, "last": res,
             "problems": len(problems), "pairs": len(hs.pair_problem), "tris": int(hs.n_tris)}
 
 

@@ -57,7 +57,15 @@ static int copy_field(PyObject *obj, double *dst, Py_ssize_t n) {
   return 0;
 }
 
-/* gather_states(bodies: list, out: writable float64 buffer of len(bodies)*16) */
+/* gather_states(bodies: list, out: writable float64 buffer of len(bodies)*16)
+ *
+ * The objects of a large scene are scattered over the heap, so each
+ * attribute hop is a cache miss.  Walking body by body chains ~7 dependent
+ * misses per body; walking level by level (all timelines, then all current
+ * states, then every field) makes the misses of different bodies
+ * independent, and the core overlaps them.  Bodies are processed in blocks
+ * of kBlock to keep the pointer arrays in L1. */
+#define kBlock 256
 static PyObject *gather_states(PyObject *self, PyObject *args) {
   PyObject *bodies, *out;
   if (!PyArg_ParseTuple(args, "OO", &bodies, &out)) return NULL;
@@ -75,30 +83,52 @@ static PyObject *gather_states(PyObject *self, PyObject *args) {
     PyErr_SetString(PyExc_ValueError, "out must hold len(bodies) x 16 float64");
     return NULL;
   }
-  double *row = (double *)ob.buf;
-  memset(row, 0, (size_t)n * 16 * 8);
-  for (Py_ssize_t i = 0; i < n; ++i, row += 16) {
-    PyObject *body = PySequence_Fast_GET_ITEM(seq, i);
-    PyObject *tl = PyObject_GetAttr(body, s_timeline);
-    if (!tl) {
-      if (!PyErr_ExceptionMatches(PyExc_AttributeError)) goto fail;
-      PyErr_Clear();
-      row[13] = 1.0; /* static body: identity pose, no motion */
-      continue;
+  double *rows = (double *)ob.buf;
+  memset(rows, 0, (size_t)n * 16 * 8);
+  PyObject *cur[kBlock];
+  PyObject *fld[4][kBlock];
+  PyObject **items = PySequence_Fast_ITEMS(seq);
+  for (Py_ssize_t b0 = 0; b0 < n; b0 += kBlock) {
+    const Py_ssize_t m = n - b0 < kBlock ? n - b0 : kBlock;
+    /* level 1: timeline (statics have none) -> level 2: current state */
+    for (Py_ssize_t i = 0; i < m; ++i) {
+      PyObject *tl = PyObject_GetAttr(items[b0 + i], s_timeline);
+      cur[i] = NULL;
+      if (!tl) {
+        if (!PyErr_ExceptionMatches(PyExc_AttributeError)) {
+          for (Py_ssize_t k = 0; k < i; ++k) Py_XDECREF(cur[k]);
+          goto fail;
+        }
+        PyErr_Clear();
+        rows[(b0 + i) * 16 + 13] = 1.0; /* static body: identity pose, no motion */
+        continue;
+      }
+      cur[i] = tl; /* holds the timeline until level 2 */
     }
-    PyObject *cur = PyObject_GetAttr(tl, s_current);
-    Py_DECREF(tl);
-    if (!cur) goto fail;
-    for (int f = 0; f < 4; ++f) {
-      PyObject *v = PyObject_GetAttr(cur, s_fields[f]);
-      if (!v || copy_field(v, row + k_off[f], k_len[f]) != 0) {
-        Py_XDECREF(v);
-        Py_DECREF(cur);
+    for (Py_ssize_t i = 0; i < m; ++i) {
+      if (!cur[i]) continue;
+      PyObject *c = PyObject_GetAttr(cur[i], s_current);
+      Py_DECREF(cur[i]);
+      cur[i] = c;
+      if (!c) {
+        for (Py_ssize_t k = i + 1; k < m; ++k) Py_XDECREF(cur[k]);
         goto fail;
       }
-      Py_DECREF(v);
     }
-    Py_DECREF(cur);
+    /* level 3: the four field objects; level 4: their data */
+    for (int f = 0; f < 4; ++f)
+      for (Py_ssize_t i = 0; i < m; ++i) fld[f][i] = cur[i] ? PyObject_GetAttr(cur[i], s_fields[f]) : NULL;
+    int err = 0;
+    for (Py_ssize_t i = 0; i < m; ++i) {
+      if (!cur[i]) continue;
+      for (int f = 0; f < 4; ++f)
+        if (!err && (!fld[f][i] || copy_field(fld[f][i], rows + (b0 + i) * 16 + k_off[f], k_len[f]) != 0)) err = 1;
+    }
+    for (Py_ssize_t i = 0; i < m; ++i) {
+      for (int f = 0; f < 4; ++f) Py_XDECREF(fld[f][i]);
+      Py_XDECREF(cur[i]);
+    }
+    if (err) goto fail;
   }
   PyBuffer_Release(&ob);
   Py_DECREF(seq);

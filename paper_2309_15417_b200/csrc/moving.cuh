@@ -1,0 +1,396 @@
+// Moving-path screen (dt > 0 batches: c4, c5), one generation as three
+// kernels.  Included by search.cu after the candidate/record helpers.
+//
+//   k_mscreen  one warp per 32 frontier candidates: per candidate the
+//              reference's sample count, grid and thresholds (ccd.py:321-370,
+//              :410-411) and the certified window cull; per in-window row
+//              (flattened over the warp's lanes) the moved-sphere cull and
+//              the separating-axis cull.  The surviving rows are appended,
+//              per warp and in candidate order, to a global row list.  No
+//              exact distance here, so the kernel stays small and resident.
+//   k_mexact   one thread per surviving row: the exact 15-feature distance
+//              at the row's tau (pose table or Rodrigues, ccd.py:116-132)
+//              and its three decision bits.
+//   k_mdecide  one thread per row; the first row of each candidate's
+//              segment gathers the candidate's bits and makes the
+//              reference's decisions (ccd.py:404-446): resting record,
+//              children of a flagged coarse candidate, flagged fine runs.
+//              Rows settled by a cull carry no bits, exactly as a row whose
+//              distance clears every threshold.
+//
+// Every tau is the reference's linspace sample; the per-candidate step is
+// computed once (the same division linspace_at performs) and a row's tau is
+// i*step + w0, bit for bit what linspace_at returns.
+
+struct ExactRow {
+  uint32_t cand;  // frontier index of the candidate
+  int16_t i;      // sample index in linspace(w0, dt, count)
+  uint8_t count;  // the candidate's sample count (1..33)
+  uint8_t bits;   // k_mexact: 1 = flag (d <= thr), 2 = d <= h, 4 = resting test (d <= h + 1e-9)
+  double tau;
+  double thr;     // h + 0.5 * speed * step (ccd.py:410-411)
+};
+static_assert(sizeof(ExactRow) == 24, "ExactRow layout");
+
+struct RowList {
+  ExactRow* rows;
+  unsigned long long cap;
+  unsigned long long* n;  // device counter of this generation's rows
+};
+
+struct MCandInfo {
+  double w0, dt, h, thr, step, cull_lo, cull_hi;
+  int64_t off_a, off_b;  // record indices of the two triangles
+  int32_t ba, bb, count, first, culled;
+  int32_t tab;  // bit 0 / bit 1: the pose table covers side a / b
+};
+
+// linspace(w0, dt, count)[i] with the candidate's precomputed step
+__device__ __forceinline__ double cand_tau(const MCandInfo& c, int i) {
+  if (c.count <= 1) return c.w0;
+  if (i == c.count - 1) return c.dt;
+  if (c.step != 0.0) return add(mul((double)i, c.step), c.w0);
+  return linspace_at(c.w0, c.dt, c.count, i);
+}
+
+#ifndef LTSG_MSCREEN_MINB
+#define LTSG_MSCREEN_MINB 3
+#endif
+constexpr int kMWarps = 8;
+constexpr int kMRows = 32 * kMaxSamples;  // rows of one warp's 32 candidates, at most
+
+__device__ __forceinline__ int owner_of(const MCandInfo* info, int r) {
+  int o = 0;  // last lane with first <= r among lanes that own rows
+#pragma unroll
+  for (int step = 16; step > 0; step >>= 1)
+    if (info[o + step].first <= r) o += step;
+  while (info[o].culled || info[o].count == 0) --o;
+  return o;
+}
+
+__global__ void __launch_bounds__(32 * kMWarps, LTSG_MSCREEN_MINB)
+k_mscreen(const Cand* __restrict__ front, int64_t n, const PairInfo* __restrict__ pairs,
+          const BodyInfo* __restrict__ bodies, const double* __restrict__ tris, ScreenOut out, PoseTable pt,
+          RowList rl) {
+  if (out.n_in) n = (int64_t)min(*out.n_in, out.next_cap);
+  __shared__ MCandInfo s_info[kMWarps][32];
+  __shared__ uint16_t s_queue[kMWarps][kMRows];  // row (11 bits) | owner lane << 11
+  const int warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
+  const int64_t n_warps = (n + 31) / 32;
+  MCandInfo* info = s_info[warp];
+  uint16_t* queue = s_queue[warp];
+  unsigned long long acc_rows = 0, acc_exact = 0, acc_window = 0, acc_sphere = 0;
+
+  for (int64_t wi = blockIdx.x * (int64_t)kMWarps + warp; wi < n_warps; wi += (int64_t)gridDim.x * kMWarps) {
+    const int64_t ci = wi * 32 + lane;
+    MCandInfo me{};
+    if (ci < n) {
+      const Cand c = front[ci];
+      const PairInfo p = pairs[c.pair];
+      const BodyInfo& A = bodies[p.ba];
+      const BodyInfo& B = bodies[p.bb];
+      me.ba = p.ba;
+      me.bb = p.bb;
+      me.off_a = A.level_off[c.la] + c.ia;
+      me.off_b = B.level_off[c.lb] + c.ib;
+      const double* ra_ = tris + me.off_a * kRecord;
+      const double* rb_ = tris + me.off_b * kRecord;
+      me.h = add(__ldg(ra_ + 9), __ldg(rb_ + 9));  // ccd.py:339
+      double sp = p.speed0;                        // ccd.py:340-345
+      if (A.m.omega > 0.0) sp = add(sp, mul(A.m.omega, __ldg(ra_ + 10)));
+      if (B.m.omega > 0.0) sp = add(sp, mul(B.m.omega, __ldg(rb_ + 10)));
+      me.w0 = c.w0;
+      me.tab = (pt.tab != nullptr && c.w0 == 0.0)
+          ? ((pt.tdt[p.ba] == p.dt ? 1 : 0) | (pt.tdt[p.bb] == p.dt ? 2 : 0)) : 0;
+      me.dt = p.dt;
+      const double span = fmax(sub(p.dt, c.w0), 0.0);
+      me.count = sample_count(span, sp, me.h);
+      // linspace's step, once (numpy: (stop - start) / (n - 1))
+      me.step = me.count > 1 ? dv(sub(p.dt, c.w0), (double)(me.count - 1)) : 0.0;
+      const double step = me.count > 1 ? sub(cand_tau(me, 1), c.w0) : 0.0;  // grid[1] - grid[0]
+      me.thr = add(me.h, mul(mul(0.5, sp), step));  // ccd.py:410-411
+      // certified window (see k_screen): the bounding-sphere gap is
+      // `speed`-Lipschitz, evaluated at both window ends
+      me.cull_lo = -1.0;
+      me.cull_hi = 2.0 * p.dt + 1.0;
+      if (__ldg(ra_ + 15) >= 0.0 && __ldg(rb_ + 15) >= 0.0) {
+        const double T = fmax(me.thr, add(me.h, kRestSlop));
+        double sc0 = 0.0, sc1 = 0.0;
+        const double gap0 = sphere_gap_at(bodies, p.ba, p.bb, ra_, rb_, c.w0, me.tab, me.count, 0, pt, &sc0);
+        const double g0 = gap0 - (T + kCullMargin * sc0);
+        double g1 = g0;
+        if (p.dt > c.w0) {
+          const double gap1 = sphere_gap_at(bodies, p.ba, p.bb, ra_, rb_, p.dt, me.tab, me.count, me.count - 1, pt,
+                                            &sc1);
+          g1 = gap1 - (T + kCullMargin * sc1);
+        }
+        if (sp > 0.0) {
+          me.cull_lo = c.w0 + g0 / sp;
+          me.cull_hi = p.dt - g1 / sp;
+        } else if (g0 > 0.0) {
+          me.cull_lo = 2.0 * p.dt + 1.0;
+        }
+        me.culled = me.cull_lo > p.dt || me.cull_hi < c.w0 || me.cull_lo > me.cull_hi;
+      }
+    }
+    const int nrows = me.culled ? 0 : me.count;
+    const int incl = warp_incl_scan(nrows, lane);
+    const int total = __shfl_sync(0xffffffffu, incl, 31);
+    int all_rows = me.count;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) all_rows += __shfl_xor_sync(0xffffffffu, all_rows, o);
+    me.first = incl - nrows;
+    info[lane] = me;
+    __syncwarp();
+
+    // (a) window + moved-sphere cull per row; survivors queued with their owner
+    int nq = 0;
+    for (int r0 = 0; r0 < total; r0 += 32) {
+      const int r = r0 + lane;
+      bool keep = false;
+      int o = 0;
+      if (r < total) {
+        o = owner_of(info, r);
+        const MCandInfo& c = info[o];
+        const int i = r - c.first;
+        const double tau = cand_tau(c, i);
+        keep = !(tau < c.cull_lo || tau > c.cull_hi);
+        const double* ra_ = tris + c.off_a * kRecord;
+        const double* rb_ = tris + c.off_b * kRecord;
+        if (keep && __ldg(ra_ + 15) >= 0.0 && __ldg(rb_ + 15) >= 0.0) {
+          double scale;
+          const double gap = sphere_gap_at(bodies, c.ba, c.bb, ra_, rb_, tau, c.tab, c.count, i, pt, &scale);
+          keep = !(gap > fmax(c.thr, add(c.h, kRestSlop)) + kCullMargin * scale);
+        }
+      }
+      const unsigned m = __ballot_sync(0xffffffffu, keep);
+      if (keep) queue[nq + __popc(m & ((1u << lane) - 1u))] = (uint16_t)(r | (o << 11));
+      nq += __popc(m);
+    }
+    __syncwarp();
+    const int nq_sphere = nq;
+    // (b) separating-axis cull of the sphere survivors, compacted in place
+    {
+      int nq2 = 0;
+      for (int q0 = 0; q0 < nq; q0 += 32) {
+        const int q = q0 + lane;
+        bool keep = false;
+        uint16_t e = 0;
+        if (q < nq) {
+          e = queue[q];
+          const int r = e & 2047, o = e >> 11;
+          const MCandInfo& c = info[o];
+          const int i = r - c.first;
+          keep = !sat_cull_posed(bodies, c.ba, c.bb, tris + c.off_a * kRecord, tris + c.off_b * kRecord,
+                                 cand_tau(c, i), c.tab, c.count, i, pt, fmax(c.thr, add(c.h, kRestSlop)));
+        }
+        const unsigned m = __ballot_sync(0xffffffffu, keep);
+        __syncwarp();
+        if (keep) queue[nq2 + __popc(m & ((1u << lane) - 1u))] = e;
+        nq2 += __popc(m);
+      }
+      nq = nq2;
+    }
+    __syncwarp();
+    // (c) the survivors go to the global row list, in candidate order
+    unsigned long long base = 0;
+    if (lane == 0 && nq) base = atomicAdd(rl.n, (unsigned long long)nq);
+    base = __shfl_sync(0xffffffffu, base, 0);
+    for (int q = lane; q < nq; q += 32) {
+      const uint16_t e = queue[q];
+      const int r = e & 2047, o = e >> 11;
+      const MCandInfo& c = info[o];
+      const int i = r - c.first;
+      const unsigned long long dst = base + q;
+      if (dst < rl.cap) {
+        ExactRow x;
+        x.cand = (uint32_t)(wi * 32 + o);
+        x.i = (int16_t)i;
+        x.count = (uint8_t)c.count;
+        x.bits = 0;
+        x.tau = cand_tau(c, i);
+        x.thr = c.thr;
+        rl.rows[dst] = x;
+      }
+    }
+    acc_rows += (unsigned long long)all_rows;
+    acc_exact += (unsigned long long)nq;
+    acc_window += (unsigned long long)total;
+    acc_sphere += (unsigned long long)nq_sphere;
+    __syncwarp();
+  }
+  if (lane == 0) {
+    if (acc_rows) atomicAdd(&out.ctr->rows, acc_rows);
+    if (acc_exact) atomicAdd(&out.ctr->screen_exact, acc_exact);
+    if (acc_window) atomicAdd(&out.ctr->rows_window, acc_window);
+    if (acc_sphere) atomicAdd(&out.ctr->rows_sphere, acc_sphere);
+  }
+}
+
+#ifndef LTSG_MEXACT_MINB
+#define LTSG_MEXACT_MINB 7
+#endif
+constexpr int kMExactThreads = 128;
+constexpr int kMExactStageBytes = kStagedLite * kMExactThreads * sizeof(double);
+
+// Exact 15-feature distance of every surviving row (lite stage, 24 doubles
+// per thread in shared memory), three decision bits per row.
+__global__ void __launch_bounds__(kMExactThreads, LTSG_MEXACT_MINB)
+k_mexact(const Cand* __restrict__ front, const PairInfo* __restrict__ pairs, const BodyInfo* __restrict__ bodies,
+         const double* __restrict__ tris, PoseTable pt, RowList rl) {
+  extern __shared__ double s_stage[];
+  const Staged<kMExactThreads> st{s_stage + threadIdx.x};
+  const int64_t n = (int64_t)min(*rl.n, rl.cap);
+  for (int64_t x = blockIdx.x * (int64_t)kMExactThreads + threadIdx.x; x < n;
+       x += (int64_t)gridDim.x * kMExactThreads) {
+    const ExactRow r = rl.rows[x];
+    const Cand c = front[r.cand];
+    const PairInfo p = pairs[c.pair];
+    const double* ra = tris + (bodies[p.ba].level_off[c.la] + c.ia) * kRecord;
+    const double* rb = tris + (bodies[p.bb].level_off[c.lb] + c.ib) * kRecord;
+    const double h = add(__ldg(ra + 9), __ldg(rb + 9));
+    const int tab = (pt.tab != nullptr && c.w0 == 0.0)
+        ? ((pt.tdt[p.ba] == p.dt ? 1 : 0) | (pt.tdt[p.bb] == p.dt ? 2 : 0)) : 0;
+    const double d = row_distance_posed(st, bodies, p.ba, p.bb, ra, rb, r.tau, tab, r.count, r.i, pt);
+    uint8_t b = 0;
+    if (d <= r.thr) b |= 1;                // screen flag
+    if (d <= h) b |= 2;                    // at or below touching distance
+    if (d <= add(h, kRestSlop)) b |= 4;    // resting test (ccd.py:407)
+    rl.rows[x].bits = b;
+  }
+}
+
+struct MChild {
+  double w0;
+  int32_t first, count, pair, ia0, ib0, nb, la, lb;
+};
+
+constexpr int kMDecideWarps = 8;
+
+// Decisions per candidate (ccd.py:404-446) from its rows' bits.  The rows of
+// one candidate are contiguous in the list; the first one of each segment
+// acts.  Children of flagged coarse candidates are emitted warp-cooperatively
+// (one atomic per warp, coalesced stores).
+__global__ void __launch_bounds__(32 * kMDecideWarps)
+k_mdecide(const Cand* __restrict__ front, const PairInfo* __restrict__ pairs, const BodyInfo* __restrict__ bodies,
+          const double* __restrict__ tris, RowList rl, ScreenOut out) {
+  __shared__ MChild s_kid[kMDecideWarps][32];
+  const int warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
+  MChild* kid = s_kid[warp];
+  const int64_t n = (int64_t)min(*rl.n, rl.cap);
+  const int64_t n_warps = (n + 31) / 32;
+  for (int64_t wi = blockIdx.x * (int64_t)kMDecideWarps + warp; wi < n_warps;
+       wi += (int64_t)gridDim.x * kMDecideWarps) {
+    const int64_t x = wi * 32 + lane;
+    MChild ch{};
+    if (x < n) {
+      const ExactRow r = rl.rows[x];
+      const bool head = x == 0 || rl.rows[x - 1].cand != r.cand;
+      uint64_t flag = 0, touch = 0;
+      bool rest0 = false;
+      if (head) {
+        for (int64_t j = x; j < n; ++j) {
+          const ExactRow s = rl.rows[j];
+          if (s.cand != r.cand) break;
+          if (s.bits & 1) flag |= 1ull << s.i;
+          if (s.bits & 2) touch |= 1ull << s.i;
+          if (s.i == 0 && (s.bits & 4)) rest0 = true;
+        }
+      }
+      if (flag || rest0) {
+        const Cand own = front[r.cand];
+        const PairInfo p = pairs[own.pair];
+        const BodyInfo& A = bodies[p.ba];
+        const BodyInfo& B = bodies[p.bb];
+        const int64_t off_a = A.level_off[own.la] + own.ia;
+        const int64_t off_b = B.level_off[own.lb] + own.ib;
+        const double* ra = tris + off_a * kRecord;
+        const double* rb = tris + off_b * kRecord;
+        const double h = add(__ldg(ra + 9), __ldg(rb + 9));
+        const int count = r.count;
+        const bool fine = own.la == 0 && own.lb == 0;
+        if (fine && own.w0 == 0.0 && rest0) {
+          const unsigned long long slot = atomicAdd(&out.ctr->resting, 1ULL);
+          if (slot < out.rest_cap) out.resting[slot] = RestRec{own.pair, own.ia, own.ib, 0, h};
+        } else if (flag && !fine) {  // ccd.py:414-428
+          const int k0 = __ffsll((long long)flag) - 1;
+          ch.w0 = linspace_at(own.w0, p.dt, count, k0 > 0 ? k0 - 1 : 0);
+          ch.pair = own.pair;
+          int na = 1, nb = 1;
+          ch.ia0 = own.ia;
+          ch.ib0 = own.ib;
+          if (own.la > 0) {
+            const int2 cr = *reinterpret_cast<const int2*>(ra + 11);
+            ch.ia0 = cr.x;
+            na = cr.y;
+          }
+          if (own.lb > 0) {
+            const int2 cr = *reinterpret_cast<const int2*>(rb + 11);
+            ch.ib0 = cr.x;
+            nb = cr.y;
+          }
+          ch.nb = nb;
+          ch.count = na * nb;
+          ch.la = own.la > 0 ? own.la - 1 : 0;
+          ch.lb = own.lb > 0 ? own.lb - 1 : 0;
+        } else if (flag) {  // fine: flagged runs (ccd.py:429-446)
+          double sp = p.speed0;
+          if (A.m.omega > 0.0) sp = add(sp, mul(A.m.omega, __ldg(ra + 10)));
+          if (B.m.omega > 0.0) sp = add(sp, mul(B.m.omega, __ldg(rb + 10)));
+          int k = __ffsll((long long)flag) - 1;
+          while (k < count) {
+            if (!((flag >> k) & 1)) { ++k; continue; }
+            int ke = k;
+            while (ke + 1 < count && ((flag >> (ke + 1)) & 1)) ++ke;
+            const int lo_i = k > 0 ? k - 1 : 0;
+            const int hi_i = ke + 1 < count - 1 ? ke + 1 : count - 1;
+            if ((touch >> lo_i) & 1) {
+              const unsigned long long slot = atomicAdd(&out.ctr->cross, 1ULL);
+              if (slot < out.cross_cap)
+                out.cross[slot] = Cross{own.pair, own.ia, own.ib, 0, linspace_at(own.w0, p.dt, count, lo_i), h};
+            } else if (hi_i > lo_i) {
+              const unsigned long long slot = atomicAdd(&out.ctr->entries, 1ULL);
+              if (slot < out.entry_cap)
+                out.entries[slot] = Entry{own.pair, own.ia, own.ib, 0, linspace_at(own.w0, p.dt, count, lo_i),
+                                          linspace_at(own.w0, p.dt, count, hi_i), h, sp};
+            }
+            k = ke + 1;
+          }
+        }
+      }
+    }
+    // cooperative, coalesced child emission
+    const int cincl = warp_incl_scan(ch.count, lane);
+    const int ctotal = __shfl_sync(0xffffffffu, cincl, 31);
+    if (ctotal) {
+      unsigned long long cbase = 0;
+      if (lane == 0) cbase = atomicAdd(out.n_out, (unsigned long long)ctotal);
+      cbase = __shfl_sync(0xffffffffu, cbase, 0);
+      ch.first = cincl - ch.count;
+      kid[lane] = ch;
+      __syncwarp();
+      for (int s = lane; s < ctotal; s += 32) {
+        int o = 0;
+#pragma unroll
+        for (int step = 16; step > 0; step >>= 1)
+          if (kid[o + step].first <= s) o += step;
+        const MChild& c = kid[o];
+        const int j = s - c.first;
+        const unsigned long long dst = cbase + s;
+        if (dst < out.next_cap) {
+          Cand nc;
+          nc.pair = c.pair;
+          nc.ia = c.ia0 + j / c.nb;
+          nc.ib = c.ib0 + j % c.nb;
+          nc.la = (int16_t)c.la;
+          nc.lb = (int16_t)c.lb;
+          nc.w0 = c.w0;
+          out.next[dst] = nc;
+        }
+      }
+      __syncwarp();
+    }
+  }
+}

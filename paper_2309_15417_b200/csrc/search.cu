@@ -784,6 +784,8 @@ k_screen(const Cand* __restrict__ front, int64_t n, const PairInfo* __restrict__
 }
 
 
+#include "moving.cuh"
+
 // ---------------------------------------------------------------- static screen
 
 // World records at tau = 0 (the pose at the window start), 20 doubles each:
@@ -2143,6 +2145,7 @@ static int configure_kernels() {
     LTSG_CUDA(cudaFuncSetAttribute(k_screen_static, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                    kStaticStageBytes));
     LTSG_CUDA(cudaFuncSetAttribute(k_allpairs_tile, cudaFuncAttributeMaxDynamicSharedMemorySize, kTileSmemBytes));
+    LTSG_CUDA(cudaFuncSetAttribute(k_mexact, cudaFuncAttributeMaxDynamicSharedMemorySize, kMExactStageBytes));
     done = 1;
   }
   return LTSG_OK;
@@ -2370,7 +2373,11 @@ static int run_search(const ltsg_scene* sc, ltsg_result* out, ltsg_workspace* ws
   Counters h{};
   Cand* front = nullptr;
 
-  size_t n_timed = 0;  // static generations timed with event triples (exact, expand)
+  // moving batches: rows surviving the culls, per generation (k_mscreen -> k_mexact -> k_mdecide)
+  const bool legacy_moving = getenv("LTSG_MOVING_LEGACY") != nullptr;
+  ExactRow* mrows = nullptr;
+  size_t mrows_cap = 0;
+  size_t n_timed = 0;  // generations timed with event triples (exact, expand / decide)
   auto static_times = [&]() -> int {  // call once the stream has passed every recorded event
     out->ms_exact = out->ms_expand = 0.0;
     for (size_t g = 0; g < n_timed; ++g) {
@@ -2403,10 +2410,29 @@ static int run_search(const ltsg_scene* sc, ltsg_result* out, ltsg_workspace* ws
       LTSG_LAUNCHED();
       LTSG_CUDA(cudaEventRecord(ws->event(e + 2), st));
       return LTSG_OK;
-    } else {
+    } else if (legacy_moving) {
       const int grid = n_in ? 148 * 32 : screen_grid(n);
       k_screen<<<grid, 32 * kScreenWarps, kScreenStageBytes, st>>>(in, n, pr.pairs, pr.bodies, sc->tris, so,
                                                                    poses);
+    } else {
+      // cull kernel -> surviving rows (counted in xcnt) -> exact distances -> decisions
+      if (cap > 0xffffffffULL) {  // rows name their candidate with a 32-bit frontier index
+        set_error("moving frontier capacity %llu exceeds 2^32", cap);
+        return LTSG_ECAPACITY;
+      }
+      const RowList rl{mrows, mrows_cap, xcnt};
+      const int64_t mblocks = n_in ? 148LL * LTSG_MSCREEN_MINB * 8 : (n + 32 * kMWarps - 1) / (32 * kMWarps);
+      k_mscreen<<<(int)std::max<int64_t>(1, std::min<int64_t>(mblocks, 148LL * LTSG_MSCREEN_MINB * 8)),
+                  32 * kMWarps, 0, st>>>(in, n, pr.pairs, pr.bodies, sc->tris, so, poses, rl);
+      LTSG_LAUNCHED();
+      const size_t e = 3 * n_timed++;
+      LTSG_CUDA(cudaEventRecord(ws->event(e), st));
+      k_mexact<<<148 * LTSG_MEXACT_MINB * 4, kMExactThreads, kMExactStageBytes, st>>>(in, pr.pairs, pr.bodies,
+                                                                                    sc->tris, poses, rl);
+      LTSG_LAUNCHED();
+      LTSG_CUDA(cudaEventRecord(ws->event(e + 1), st));
+      k_mdecide<<<148 * 8, 32 * kMDecideWarps, 0, st>>>(in, pr.pairs, pr.bodies, sc->tris, rl, so);
+      LTSG_CUDA(cudaEventRecord(ws->event(e + 2), st));
     }
     LTSG_LAUNCHED();
     return LTSG_OK;
@@ -2470,6 +2496,10 @@ static int run_search(const ltsg_scene* sc, ltsg_result* out, ltsg_workspace* ws
       LTSG_TRY(ws_get(ws, "front1", cap_async, &buf[1]));
       Cand* xbuf = nullptr;
       if (all_static) LTSG_TRY(ws_get(ws, "frontx", cap_async, &xbuf));
+      if (!all_static && !legacy_moving) {
+        mrows_cap = std::max(cap_async, (size_t)(1.25 * (double)ws->hint_mrows) + 1024);
+        LTSG_TRY(ws_get(ws, "mrows", mrows_cap, &mrows));
+      }
       // one generation more than the deepest traversal seen: a non-empty
       // frontier after the last one means the budget was short (re-run sync)
       const int n_gen = std::min(kMaxGen, std::max(1, ws->hint_gens) + 1);
@@ -2490,6 +2520,15 @@ static int run_search(const ltsg_scene* sc, ltsg_result* out, ltsg_workspace* ws
         }
       }
       if (hg[n_gen] > 0) *overflow = true;  // deeper than the generation budget
+      if (!all_static && !legacy_moving) {
+        unsigned long long hx[kMaxGen + 1];
+        LTSG_CUDA(cudaMemcpyAsync(hx, x_cnt, sizeof(hx), cudaMemcpyDeviceToHost, st));
+        LTSG_CUDA(cudaStreamSynchronize(st));
+        for (int g = 0; g <= kMaxGen; ++g) {
+          if (hx[g] > mrows_cap) *overflow = true;
+          ws->hint_mrows = std::max(ws->hint_mrows, (size_t)hx[g]);
+        }
+      }
       if (h.resting > rest_cap || h.entries > entry_cap || h.cross > cross_cap) *overflow = true;
       return LTSG_OK;
     }
@@ -2517,6 +2556,10 @@ static int run_search(const ltsg_scene* sc, ltsg_result* out, ltsg_workspace* ws
       LTSG_TRY(ws_get(ws, fname[fsel ^ 1], (size_t)(n_front * fan), &next));
       Cand* xbuf = nullptr;
       if (all_static) LTSG_TRY(ws_get(ws, "frontx", (size_t)n_front, &xbuf));
+      if (!all_static && !legacy_moving) {
+        mrows_cap = std::max(mrows_cap, std::max((size_t)n_front, ws->hint_mrows) + 1024);
+        LTSG_TRY(ws_get(ws, "mrows", mrows_cap, &mrows));
+      }
       Counters before = h;
       const size_t timed_before = n_timed;
       for (;;) {
@@ -2545,6 +2588,17 @@ static int run_search(const ltsg_scene* sc, ltsg_result* out, ltsg_workspace* ws
           cross_cap = (size_t)h.cross * 2;
           LTSG_TRY(ws_get(ws, "cross", cross_cap, &cross, true));
           grow = true;
+        }
+        if (!all_static && !legacy_moving) {
+          unsigned long long nx = 0;
+          LTSG_CUDA(cudaMemcpyAsync(&nx, x_cnt, sizeof(nx), cudaMemcpyDeviceToHost, st));
+          LTSG_CUDA(cudaStreamSynchronize(st));
+          ws->hint_mrows = std::max(ws->hint_mrows, (size_t)nx);
+          if (nx > mrows_cap) {
+            mrows_cap = (size_t)(1.25 * (double)nx) + 1024;
+            LTSG_TRY(ws_get(ws, "mrows", mrows_cap, &mrows));
+            grow = true;
+          }
         }
         if (!grow) break;
       }
@@ -2576,7 +2630,7 @@ static int run_search(const ltsg_scene* sc, ltsg_result* out, ltsg_workspace* ws
     cross_cap = std::max(cross_cap, (size_t)h.cross * 2);
     LTSG_TRY(traverse(false, &overflow));
   }
-  if (all_static) LTSG_TRY(static_times());
+  if (all_static || !legacy_moving) LTSG_TRY(static_times());
   ws->hint_rest = std::max(ws->hint_rest, (size_t)h.resting);
   ws->hint_entries = std::max(ws->hint_entries, (size_t)h.entries);
   ws->hint_cross = std::max(ws->hint_cross, (size_t)h.cross);
