@@ -194,8 +194,10 @@ typedef struct {
   double ms_contacts;     /* records, contacts, fusion */
   int64_t rows_screen_exact; /* screen rows that ran the exact 15-feature distance
                                 (the rest were settled by the certified culls) */
-  double ms_exact;        /* static batches: device time of the exact-distance kernel alone */
-  double ms_expand;       /* static batches: device time of the child expansion + culls */
+  double ms_exact;        /* device time of the exact-distance kernels (k_screen_static / k_mexact) */
+  double ms_expand;       /* device time of the child expansion + culls (static) / decisions (moving) */
+  int64_t rows_bound;     /* rows that survived the culls and were decided by the certified FP32
+                             upper bound instead of the exact distance (rows_screen_exact excludes them) */
 } ltsg_result;
 
 typedef struct ltsg_workspace ltsg_workspace;

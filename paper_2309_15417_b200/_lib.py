@@ -53,7 +53,7 @@ class Result(C.Structure):
         ("rows_bisect", I64), ("rows_executed", I64), ("candidates", I64),
         ("generations", I32), ("launches", I32),
         ("ms_screen", F64), ("ms_refine", F64), ("ms_contacts", F64),
-        ("rows_screen_exact", I64), ("ms_exact", F64), ("ms_expand", F64),
+        ("rows_screen_exact", I64), ("ms_exact", F64), ("ms_expand", F64), ("rows_bound", I64),
     ]
 
 

@@ -22,7 +22,7 @@ REPO = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
 LIB = os.path.join(PKG, "libltsgpu.so")
 SOURCES = ["rows.cu", "search.cu", "unpack.cu"]
-HEADERS = ["common.cuh", "geom.cuh", "dist_staged.cuh", "dist_tile.cuh"]
+HEADERS = ["common.cuh", "geom.cuh", "dist_staged.cuh", "dist_tile.cuh", "moving.cuh", "bound32.cuh"]
 
 NVCC_FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",

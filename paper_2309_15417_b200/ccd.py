@@ -260,7 +260,7 @@ class DeviceResult:
         stream.synchronize()
         stats = {k: int(getattr(st, k)) for k in (
             "rows_screen", "rows_zoom", "rows_bisect", "rows_executed", "candidates",
-            "generations", "n_raw", "n_fused", "launches", "rows_screen_exact")}
+            "generations", "n_raw", "n_fused", "launches", "rows_screen_exact", "rows_bound")}
         stats.update({k: float(getattr(st, k)) for k in ("ms_screen", "ms_refine", "ms_contacts", "ms_exact",
                                                            "ms_expand")})
         return BatchResult(dt=dt.numpy(), collision=coll.numpy() != 0, first_contact=first.numpy(),

@@ -232,33 +232,117 @@ k_mscreen(const Cand* __restrict__ front, int64_t n, const PairInfo* __restrict_
 #define LTSG_MEXACT_MINB 7
 #endif
 constexpr int kMExactThreads = 128;
+constexpr int kMExactWarps = kMExactThreads / 32;
 constexpr int kMExactStageBytes = kStagedLite * kMExactThreads * sizeof(double);
 
-// Exact 15-feature distance of every surviving row (lite stage, 24 doubles
-// per thread in shared memory), three decision bits per row.
+// World triangles of a row's two records at the row's tau (pose table or
+// Rodrigues, the reference's rounding).
+__device__ __forceinline__ void row_world(const BodyInfo* bodies, int ba, int bb, const double* ra, const double* rb,
+                                          double tau, int tab, int n, int i, const PoseTable& pt, Tri* ta, Tri* tb) {
+  {
+    double R[9], pos[3], L[9];
+    pose_at(bodies[ba], ba, tau, tab & 1, n, i, pt, R, pos);
+    load_local(ra, L);
+    *ta = world_tri(R, pos, L);
+  }
+  {
+    double R[9], pos[3], L[9];
+    pose_at(bodies[bb], bb, tau, (tab >> 1) & 1, n, i, pt, R, pos);
+    load_local(rb, L);
+    *tb = world_tri(R, pos, L);
+  }
+}
+
+struct MRowCtx {
+  const double *ra, *rb;
+  double h;
+  int ba, bb, tab;
+};
+
+__device__ __forceinline__ MRowCtx mrow_ctx(const ExactRow& r, const Cand* front, const PairInfo* pairs,
+                                            const BodyInfo* bodies, const double* tris, const PoseTable& pt) {
+  const Cand c = front[r.cand];
+  const PairInfo p = pairs[c.pair];
+  MRowCtx x;
+  x.ba = p.ba;
+  x.bb = p.bb;
+  x.ra = tris + (bodies[p.ba].level_off[c.la] + c.ia) * kRecord;
+  x.rb = tris + (bodies[p.bb].level_off[c.lb] + c.ib) * kRecord;
+  x.h = add(__ldg(x.ra + 9), __ldg(x.rb + 9));
+  x.tab = (pt.tab != nullptr && c.w0 == 0.0) ? ((pt.tdt[p.ba] == p.dt ? 1 : 0) | (pt.tdt[p.bb] == p.dt ? 2 : 0)) : 0;
+  return x;
+}
+
+// The rows' three decision bits (1 = flag d <= thr, 2 = d <= h, 4 = resting
+// test d <= h + 1e-9).  Pass 1: the certified FP32 upper bound
+// (bound32.cuh) decides rows certainly at or below their thresholds -- all
+// three bits when the bound clears h; the flag alone for a sample i > 0
+// (k_mdecide reads the touch and resting bits of sample 0 only, and of no
+// flagged sample but the first).  Pass 2: the rows left undecided are
+// queued per warp and evaluated with the bit-exact 15-feature distance, 32
+// at a time, so the exact batches stay dense.
 __global__ void __launch_bounds__(kMExactThreads, LTSG_MEXACT_MINB)
 k_mexact(const Cand* __restrict__ front, const PairInfo* __restrict__ pairs, const BodyInfo* __restrict__ bodies,
-         const double* __restrict__ tris, PoseTable pt, RowList rl) {
+         const double* __restrict__ tris, PoseTable pt, RowList rl, unsigned long long* n_bound) {
   extern __shared__ double s_stage[];
+  __shared__ int64_t s_q[kMExactWarps][64];
   const Staged<kMExactThreads> st{s_stage + threadIdx.x};
+  const int lane = threadIdx.x & 31;
+  const int warp = threadIdx.x >> 5;
+  int64_t* q = s_q[warp];
   const int64_t n = (int64_t)min(*rl.n, rl.cap);
-  for (int64_t x = blockIdx.x * (int64_t)kMExactThreads + threadIdx.x; x < n;
-       x += (int64_t)gridDim.x * kMExactThreads) {
+  const int64_t n_warps = (n + 31) / 32;
+  int nq = 0;
+  unsigned long long decided = 0;
+  auto exact = [&](int64_t x) {
     const ExactRow r = rl.rows[x];
-    const Cand c = front[r.cand];
-    const PairInfo p = pairs[c.pair];
-    const double* ra = tris + (bodies[p.ba].level_off[c.la] + c.ia) * kRecord;
-    const double* rb = tris + (bodies[p.bb].level_off[c.lb] + c.ib) * kRecord;
-    const double h = add(__ldg(ra + 9), __ldg(rb + 9));
-    const int tab = (pt.tab != nullptr && c.w0 == 0.0)
-        ? ((pt.tdt[p.ba] == p.dt ? 1 : 0) | (pt.tdt[p.bb] == p.dt ? 2 : 0)) : 0;
-    const double d = row_distance_posed(st, bodies, p.ba, p.bb, ra, rb, r.tau, tab, r.count, r.i, pt);
+    const MRowCtx c = mrow_ctx(r, front, pairs, bodies, tris, pt);
+    const double d = row_distance_posed(st, bodies, c.ba, c.bb, c.ra, c.rb, r.tau, c.tab, r.count, r.i, pt);
     uint8_t b = 0;
-    if (d <= r.thr) b |= 1;                // screen flag
-    if (d <= h) b |= 2;                    // at or below touching distance
-    if (d <= add(h, kRestSlop)) b |= 4;    // resting test (ccd.py:407)
+    if (d <= r.thr) b |= 1;
+    if (d <= c.h) b |= 2;
+    if (d <= add(c.h, kRestSlop)) b |= 4;
     rl.rows[x].bits = b;
+  };
+  for (int64_t wi = blockIdx.x * (int64_t)kMExactWarps + warp; wi < n_warps; wi += (int64_t)gridDim.x * kMExactWarps) {
+    const int64_t x = wi * 32 + lane;
+    bool pend = false;
+    if (x < n) {
+      const ExactRow r = rl.rows[x];
+      const MRowCtx c = mrow_ctx(r, front, pairs, bodies, tris, pt);
+      pend = true;
+      if (LTSG_BOUND && __ldg(c.ra + 15) >= 0.0 && __ldg(c.rb + 15) >= 0.0) {
+        Tri ta, tb;
+        row_world(bodies, c.ba, c.bb, c.ra, c.rb, r.tau, c.tab, r.count, r.i, pt, &ta, &tb);
+        double ub, margin;
+        if (feature_ub(ta, tb, &ub, &margin)) {
+          const double u = ub + margin;
+          if (u <= c.h) {
+            rl.rows[x].bits = 7;
+            pend = false;
+          } else if (r.i > 0 && u <= r.thr) {
+            rl.rows[x].bits = 1;
+            pend = false;
+          }
+        }
+      }
+      decided += !pend;
+    }
+    const unsigned m = __ballot_sync(0xffffffffu, pend);
+    if (pend) q[nq + __popc(m & ((1u << lane) - 1u))] = x;
+    nq += __popc(m);
+    __syncwarp();
+    if (nq >= 32) {
+      exact(q[lane]);
+      __syncwarp();
+      if (lane < nq - 32) q[lane] = q[32 + lane];
+      nq -= 32;
+      __syncwarp();
+    }
   }
+  if (lane < nq) exact(q[lane]);
+  for (int o = 16; o > 0; o >>= 1) decided += __shfl_xor_sync(0xffffffffu, decided, o);
+  if (lane == 0 && decided) atomicAdd(n_bound, decided);
 }
 
 struct MChild {

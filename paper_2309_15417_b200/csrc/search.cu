@@ -27,6 +27,10 @@
 #include <ctime>
 #include <vector>
 
+#ifndef LTSG_BOUND
+#define LTSG_BOUND 1  // certified FP32 upper-bound pre-decision in the exact kernels
+#endif
+
 namespace ltsg {
 
 constexpr int kMaxLevels = 8;
@@ -37,6 +41,9 @@ constexpr int kSph = 4;      // doubles per compact cull sphere (after the world
 // coordinate scale) of a threshold are always evaluated exactly.
 constexpr double kCullMargin = 1e-7;
 // slivers (Lmax^2 > 1e4 |e0 x e2|, packing.CULL_COND) carry radius -1 and are never culled
+}  // namespace ltsg
+#include "bound32.cuh"
+namespace ltsg {
 
 struct BodyInfo {
   Motion m;
@@ -93,6 +100,7 @@ struct Counters {
   unsigned long long screen_exact;  // screen rows evaluated with the exact 15-feature distance
   unsigned long long rows_window;   // moving screen: rows inside the candidates' cull windows
   unsigned long long rows_sphere;   // moving screen: rows surviving the per-row sphere cull
+  unsigned long long bound_rows;    // screen_exact rows decided by the certified FP32 upper bound
 };
 
 // ---------------------------------------------------------------- prep
@@ -1206,36 +1214,30 @@ k_screen_static(const Cand* __restrict__ front, int64_t n, const PairInfo* __res
                 unsigned long long* n_par) {
   if (out.n_in) n = (int64_t)min(*out.n_in, out.next_cap);
   extern __shared__ double s_stage[];  // kStaged x (32 * kStaticWarps)
+  __shared__ int64_t s_q[kStaticWarps][64];
   const Staged<32 * kStaticWarps> st{s_stage + threadIdx.x};
   const int lane = threadIdx.x & 31;
   const int warp = threadIdx.x >> 5;
+  int64_t* q = s_q[warp];
   if (blockIdx.x == 0 && threadIdx.x == 0 && n > 0) atomicAdd(&out.ctr->screen_exact, (unsigned long long)n);
   const int64_t n_warps = (n + 31) / 32;
-  for (int64_t wi = blockIdx.x * (int64_t)kStaticWarps + warp; wi < n_warps;
-       wi += (int64_t)gridDim.x * kStaticWarps) {
-    const int64_t ci = wi * 32 + lane;
+  unsigned long long decided = 0;
+  // the decision of a row known to be at or below (hit) its threshold or
+  // not: resting record (fine) or flagged parent (coarse); warp-uniform
+  auto act = [&](bool have, int64_t ci, bool hit) {
     bool flagged = false;
     Parent P{};
-    if (ci < n) {
+    if (have && hit) {
       const Cand c = front[ci];
       const double* wa = world + (size_t)c.ia * kWorld;
       const double* wb = world + (size_t)c.ib * kWorld;
-      const double h = add(__ldg(wa + 9), __ldg(wb + 9));
-#if LTSG_STATIC_LITE
-      stage_pair_lite(st, load_world(wa), load_world(wb));
-      const double d = __dsqrt_rn(staged_dist_sq_lite(st));
-#else
-      stage_pair(st, load_world(wa), load_world(wb));
-      const double d = __dsqrt_rn(staged_dist_sq(st));
-#endif
       if (c.la == 0 && c.lb == 0) {
-        if (d <= add(h, kRestSlop)) {
-          const PairInfo p = pairs[c.pair];
-          const unsigned long long slot = atomicAdd(&out.ctr->resting, 1ULL);
-          if (slot < out.rest_cap)
-            out.resting[slot] = RestRec{c.pair, (int32_t)(c.ia - woff[p.ba]), (int32_t)(c.ib - woff[p.bb]), 0, h};
-        }
-      } else if (d <= h) {
+        const PairInfo p = pairs[c.pair];
+        const double h = add(__ldg(wa + 9), __ldg(wb + 9));
+        const unsigned long long slot = atomicAdd(&out.ctr->resting, 1ULL);
+        if (slot < out.rest_cap)
+          out.resting[slot] = RestRec{c.pair, (int32_t)(c.ia - woff[p.ba]), (int32_t)(c.ib - woff[p.bb]), 0, h};
+      } else {
         int a0 = c.ia, b0c = c.ib, na = 1, nb = 1;
         if (c.la > 0) {
           const int2 cr = *reinterpret_cast<const int2*>(wa + 11);
@@ -1258,7 +1260,64 @@ k_screen_static(const Cand* __restrict__ front, int64_t n, const PairInfo* __res
     if (lane == 0 && m) base = atomicAdd(n_par, (unsigned long long)__popc(m));
     base = __shfl_sync(0xffffffffu, base, 0);
     if (flagged) par[base + __popc(m & ((1u << lane) - 1u))] = P;
+  };
+  // exact 15-feature distance of a queued row: is it at or below its threshold?
+  auto exact_hit = [&](int64_t ci) {
+    const Cand c = front[ci];
+    const double* wa = world + (size_t)c.ia * kWorld;
+    const double* wb = world + (size_t)c.ib * kWorld;
+    const double h = add(__ldg(wa + 9), __ldg(wb + 9));
+    stage_pair_lite(st, load_world(wa), load_world(wb));
+    const double d = __dsqrt_rn(staged_dist_sq_lite(st));
+    return (c.la == 0 && c.lb == 0) ? d <= add(h, kRestSlop) : d <= h;
+  };
+  int nq = 0;
+  for (int64_t wi = blockIdx.x * (int64_t)kStaticWarps + warp; wi < n_warps;
+       wi += (int64_t)gridDim.x * kStaticWarps) {
+    const int64_t ci = wi * 32 + lane;
+    // pass 1: the certified FP32 upper bound decides rows certainly at or
+    // below the threshold (ccd.py:407 resting, :410-411 flag with dt = 0)
+    bool pend = false, hit = false;
+    if (ci < n) {
+      pend = true;
+#if LTSG_BOUND
+      const Cand c = front[ci];
+      const double* wa = world + (size_t)c.ia * kWorld;
+      const double* wb = world + (size_t)c.ib * kWorld;
+      if (__ldg(wa + 15) >= 0.0 && __ldg(wb + 15) >= 0.0) {
+        const double h = add(__ldg(wa + 9), __ldg(wb + 9));
+        const double T = (c.la == 0 && c.lb == 0) ? add(h, kRestSlop) : h;
+        double ub, margin;
+        if (feature_ub(load_world(wa), load_world(wb), &ub, &margin) && ub + margin <= T) {
+          pend = false;
+          hit = true;
+        }
+      }
+#endif
+    }
+    decided += hit;
+    act(hit, ci, true);
+    // pass 2: the undecided rows, queued per warp, exact 32 at a time
+    const unsigned m = __ballot_sync(0xffffffffu, pend);
+    if (pend) q[nq + __popc(m & ((1u << lane) - 1u))] = ci;
+    nq += __popc(m);
+    __syncwarp();
+    if (nq >= 32) {
+      const int64_t x = q[lane];
+      act(true, x, exact_hit(x));
+      __syncwarp();
+      if (lane < nq - 32) q[lane] = q[32 + lane];
+      nq -= 32;
+      __syncwarp();
+    }
   }
+  if (nq > 0) {
+    const bool have = lane < nq;
+    const int64_t x = have ? q[lane] : 0;
+    act(have, x, have && exact_hit(x));
+  }
+  for (int o = 16; o > 0; o >>= 1) decided += __shfl_xor_sync(0xffffffffu, decided, o);
+  if (lane == 0 && decided) atomicAdd(&out.ctr->bound_rows, decided);
 }
 
 // Children of the flagged rows of one static generation (ccd.py:418-427),
@@ -2270,6 +2329,7 @@ static int run_search(const ltsg_scene* sc, ltsg_result* out, ltsg_workspace* ws
   out->launches = 0;
   out->ms_screen = out->ms_refine = out->ms_contacts = 0.0;
   out->rows_screen_exact = 0;
+  out->rows_bound = 0;
   out->ms_exact = out->ms_expand = 0.0;
   if (np == 0) return LTSG_OK;
 
@@ -2428,7 +2488,8 @@ static int run_search(const ltsg_scene* sc, ltsg_result* out, ltsg_workspace* ws
       const size_t e = 3 * n_timed++;
       LTSG_CUDA(cudaEventRecord(ws->event(e), st));
       k_mexact<<<148 * LTSG_MEXACT_MINB * 4, kMExactThreads, kMExactStageBytes, st>>>(in, pr.pairs, pr.bodies,
-                                                                                    sc->tris, poses, rl);
+                                                                                    sc->tris, poses, rl,
+                                                                                    &d_ctr->bound_rows);
       LTSG_LAUNCHED();
       LTSG_CUDA(cudaEventRecord(ws->event(e + 1), st));
       k_mdecide<<<148 * 8, 32 * kMDecideWarps, 0, st>>>(in, pr.pairs, pr.bodies, sc->tris, rl, so);
@@ -2552,8 +2613,12 @@ static int run_search(const ltsg_scene* sc, ltsg_result* out, ltsg_workspace* ws
     const char* fname[2] = {"front0", "front1"};
     size_t max_front = (size_t)n_front;
     while (n_front > 0) {
+      // next frontier: at most n_front * fan children, usually far fewer --
+      // start from the history and grow (re-running the generation) if short
       Cand* next;
-      LTSG_TRY(ws_get(ws, fname[fsel ^ 1], (size_t)(n_front * fan), &next));
+      size_t next_cap = std::min((size_t)(n_front * fan),
+                                 std::max((size_t)n_front * 2, (size_t)(1.25 * (double)ws->hint_front)) + 4096);
+      LTSG_TRY(ws_get(ws, fname[fsel ^ 1], next_cap, &next));
       Cand* xbuf = nullptr;
       if (all_static) LTSG_TRY(ws_get(ws, "frontx", (size_t)n_front, &xbuf));
       if (!all_static && !legacy_moving) {
@@ -2568,7 +2633,7 @@ static int run_search(const ltsg_scene* sc, ltsg_result* out, ltsg_workspace* ws
         LTSG_CUDA(cudaMemsetAsync(gen_cnt + 1, 0, sizeof(unsigned long long), st));
         LTSG_CUDA(cudaMemsetAsync(x_cnt, 0, sizeof(unsigned long long), st));
         t_screen.start(st);
-        LTSG_TRY(launch_screen(front, n_front, nullptr, next, (unsigned long long)(n_front * fan), gen_cnt + 1, xbuf,
+        LTSG_TRY(launch_screen(front, n_front, nullptr, next, (unsigned long long)next_cap, gen_cnt + 1, xbuf,
                                x_cnt));
         t_screen.stop(st);
         LTSG_TRY(read_ctr(d_ctr, &h, st));
@@ -2588,6 +2653,16 @@ static int run_search(const ltsg_scene* sc, ltsg_result* out, ltsg_workspace* ws
           cross_cap = (size_t)h.cross * 2;
           LTSG_TRY(ws_get(ws, "cross", cross_cap, &cross, true));
           grow = true;
+        }
+        {
+          unsigned long long nn_now = 0;
+          LTSG_CUDA(cudaMemcpyAsync(&nn_now, gen_cnt + 1, sizeof(nn_now), cudaMemcpyDeviceToHost, st));
+          LTSG_CUDA(cudaStreamSynchronize(st));
+          if (nn_now > next_cap) {
+            next_cap = (size_t)(1.25 * (double)nn_now) + 4096;
+            LTSG_TRY(ws_get(ws, fname[fsel ^ 1], next_cap, &next));
+            grow = true;
+          }
         }
         if (!all_static && !legacy_moving) {
           unsigned long long nx = 0;
@@ -2711,7 +2786,8 @@ static int run_search(const ltsg_scene* sc, ltsg_result* out, ltsg_workspace* ws
   out->rows_zoom = (int64_t)h.zoom_rows;
   out->rows_bisect = n_br * kBisectIters;
   out->rows_executed = (int64_t)(h.screen_exact + h.zoom_exec) + n_br * kBisectIters;
-  out->rows_screen_exact = (int64_t)h.screen_exact;
+  out->rows_screen_exact = (int64_t)(h.screen_exact - h.bound_rows);
+  out->rows_bound = (int64_t)h.bound_rows;
   out->n_raw = n_rec;
 
   int32_t* prob_count;

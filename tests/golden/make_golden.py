@@ -12,6 +12,8 @@ Outputs (all small, committed):
   scenes_ccd.npz       the reference's own test_ccd.py known-answer scenes
   scenes_crit2.npz     acceptance criterion 2's 200 seeded pairs (replayed)
   scenes_configs.npz   small c1..c5-shaped scenes (reference-built trees)
+  engine_sweeps.npz    the reference engine's sweeps on its "pairs" scenario:
+                       every cluster's cache key, result and cache hit/miss
   scenes_baseline.npz  c4 pairs and c5 clusters drawn from the bench workloads
                        at their BASELINE shapes (1280-tri spinning pairs;
                        20480-tri icospheres against 12-tri boxes)
@@ -545,6 +547,89 @@ def gen_scenes_baseline(workers=8):
     return {"cases": cases}
 
 
+# ------------------------------------------------------------------ engine sweeps
+
+def gen_engine_sweeps(n_sweeps=30):
+    """The reference engine (`ltsdem.engine.step`, engine.py:146-261) on its
+    own "stacks" scenario (one row of boxes on a floor: clusters fall out of
+    step, so held-back clusters are reused from the engine's cache).  Per
+    sweep: every cluster with its cache-key fields, its result and whether
+    the engine computed it (cache miss) -- recorded by wrapping the module
+    globals `compute_effective_dt` and `mask_clusters` that step() resolves
+    at call time -- plus the particle states the narrow phase saw.
+    tests/test_gpu_sweep.py replays the sweeps through
+    paper_2309_15417_b200.sweep.SweepDriver."""
+    from ltsdem import engine
+    from ltsdem.scenarios import ScenarioConfig, build_world
+
+    world = build_world(ScenarioConfig("stacks", rows=1, seed=3))
+    calls = {}
+    sweeps = []
+    bodies0 = []
+    f_ced, f_mask = engine.compute_effective_dt, engine.mask_clusters
+
+    def ced(cluster, particles, statics, pairs, **kw):
+        res = f_ced(cluster, particles, statics, pairs, **kw)
+        calls[tuple(cluster.members)] = [tuple(p) for p in pairs]
+        return res
+
+    def soa(rows, n3=False):
+        return np.array(rows, dtype=np.float64).reshape(-1, 3) if n3 else np.array(rows)
+
+    def mask(clusters, results):
+        parts = world.particles
+        ids = sorted(parts)
+        cur = [parts[pid].timeline.current for pid in ids]
+        rec = {"ids": np.array(ids, dtype=np.int64),
+               "position": np.array([c.position for c in cur]), "velocity": np.array([c.velocity for c in cur]),
+               "rotation": np.array([c.rotation for c in cur]),
+               "angular_velocity": np.array([c.angular_velocity for c in cur]),
+               "t": np.array([c.t for c in cur]),
+               "version": np.array([parts[pid].timeline.version for pid in ids], dtype=np.int64)}
+        if not sweeps:
+            bodies0[:] = [SC.encode_body(parts[pid]) for pid in ids]
+        mem, moff, sta, soff, prs, poff, cts, coff = [], [0], [], [0], [], [0], [], [0]
+        for c, r in zip(clusters, results):
+            m = tuple(c.members)
+            mem += list(m)
+            moff.append(len(mem))
+            sta += list(c.statics)
+            soff.append(len(sta))
+            prs += calls.get(m, [])
+            poff.append(len(prs))
+            cts += list(r.contacts)
+            coff.append(len(cts))
+        rec.update({
+            "members": np.array(mem, dtype=np.int64), "members_off": np.array(moff, dtype=np.int64),
+            "statics": np.array(sta, dtype=np.int64), "statics_off": np.array(soff, dtype=np.int64),
+            "t_current": np.array([c.t_current for c in clusters]), "dt": np.array([c.dt for c in clusters]),
+            "computed": np.array([tuple(c.members) in calls for c in clusters]),
+            "pairs": np.array(prs, dtype=np.int64).reshape(-1, 2), "pairs_off": np.array(poff, dtype=np.int64),
+            "res_dt": np.array([r.dt for r in results]),
+            "res_collision": np.array([r.collision for r in results]),
+            "res_first": np.array([np.nan if r.first_contact is None else r.first_contact for r in results]),
+            "res_narrowing": np.array([r.narrowing_iters for r in results], dtype=np.int64),
+            "contacts": SC.encode_contacts(cts), "contacts_off": np.array(coff, dtype=np.int64)})
+        sweeps.append(rec)
+        calls.clear()
+        return f_mask(clusters, results)
+
+    engine.compute_effective_dt, engine.mask_clusters = ced, mask
+    try:
+        for _ in range(n_sweeps):
+            engine.step(world)
+    finally:
+        engine.compute_effective_dt, engine.mask_clusters = f_ced, f_mask
+    statics = [SC.encode_body(s) for s in world.statics.values()]
+    n_comp = sum(int(sw["computed"].sum()) for sw in sweeps)
+    n_all = sum(len(sw["dt"]) for sw in sweeps)
+    n_coll = sum(int(sw["res_collision"].sum()) for sw in sweeps)
+    n_spin = sum(int(np.any(sw["angular_velocity"] != 0.0)) for sw in sweeps)
+    print(f"engine sweeps: {len(sweeps)} sweeps, {n_all} clusters, {n_comp} computed, {n_coll} colliding, "
+          f"{n_spin} sweeps with spinning particles", flush=True)
+    return {"sweeps": sweeps, "statics": statics, "bodies": bodies0}
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--only", default="")
@@ -560,6 +645,7 @@ def main():
         "scenes_configs": lambda: gen_scenes_configs(np.random.default_rng(105)),
         "scenes_crit2": lambda: gen_scenes_crit2(limit=40 if args.quick else 200),
         "scenes_baseline": gen_scenes_baseline,
+        "engine_sweeps": gen_engine_sweeps,
     }
     del rng
     for name, job in jobs.items():

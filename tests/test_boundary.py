@@ -42,7 +42,7 @@ def _c_struct_sizes():
 #include "ltsgpu.h"
 int main(void) {
   printf("%zu %zu %zu %zu\n", sizeof(ltsg_scene), offsetof(ltsg_scene, max_children),
-         sizeof(ltsg_result), offsetof(ltsg_result, ms_expand));
+         sizeof(ltsg_result), offsetof(ltsg_result, rows_bound));
   return 0;
 }
 '''
@@ -60,7 +60,7 @@ def test_ctypes_structs_match_the_header():
     assert ctypes.sizeof(_lib.Scene) == s
     assert _lib.Scene.max_children.offset == s_last
     assert ctypes.sizeof(_lib.Result) == r
-    assert _lib.Result.ms_expand.offset == r_last
+    assert _lib.Result.rows_bound.offset == r_last
 
 
 def test_missing_device_fails_loudly():
