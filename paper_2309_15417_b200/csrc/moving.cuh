@@ -53,11 +53,166 @@ __device__ __forceinline__ double cand_tau(const MCandInfo& c, int i) {
   return linspace_at(c.w0, c.dt, c.count, i);
 }
 
+#ifndef LTSG_PLANE_CULL
+#define LTSG_PLANE_CULL 0  // measured: costs more than it saves
+#endif
 #ifndef LTSG_MSCREEN_MINB
 #define LTSG_MSCREEN_MINB 3
 #endif
 constexpr int kMWarps = 8;
 constexpr int kMRows = 32 * kMaxSamples;  // rows of one warp's 32 candidates, at most
+
+// Pose for the culls at sample i of linspace(w0, dt, n) (= tau): the pose
+// table entry when the sample is on the body's table grid, else the
+// regrouped Rodrigues rotation from the body's cull constants with sin/cos
+// of w tau on the fly (fewer operations than the reference-rounded
+// rotation_at; culls only, the margins cover the rounding).
+__device__ __forceinline__ void mcull_pose(const BodyInfo* bodies, int b, double tau, bool use_tab, int n, int i,
+                                           const PoseTable& pt, double R[9], double pos[3]) {
+  if (pt.cm == nullptr || (use_tab && pt.tab != nullptr)) {
+    // on the body's table grid the pose entry (6 vector loads) is cheaper
+    // than the regrouped form (27 constants + 2 trig values)
+    pose_at(bodies[b], b, tau, use_tab, n, i, pt, R, pos);
+    return;
+  }
+  const double* cm = pt.cm + (size_t)b * kCullM;
+#pragma unroll
+  for (int k = 0; k < 3; ++k) pos[k] = fma(tau, __ldg(cm + 3 + k), __ldg(cm + k));
+  if (__ldg(cm + 34) == 0.0) {
+#pragma unroll
+    for (int k = 0; k < 9; ++k) R[k] = __ldg(cm + 6 + k);
+    return;
+  }
+  double sn, co;
+  sincos(__ldg(cm + 33) * tau, &sn, &co);
+  const double c = 1.0 - co;
+#pragma unroll
+  for (int k = 0; k < 9; ++k) R[k] = fma(c, __ldg(cm + 24 + k), fma(sn, __ldg(cm + 15 + k), __ldg(cm + 6 + k)));
+}
+
+// Bounding-sphere gap at sample i (see sphere_gap_at), on the cull poses.
+__device__ __forceinline__ double msphere_gap(const BodyInfo* bodies, int ba, int bb, const double* ra,
+                                              const double* rb, double tau, int tab, int n, int i,
+                                              const PoseTable& pt, double* scale) {
+  double c[6];
+#pragma unroll
+  for (int side = 0; side < 2; ++side) {
+    const double* r = side ? rb : ra;
+    double R[9], pos[3];
+    mcull_pose(bodies, side ? bb : ba, tau, (tab >> side) & 1, n, i, pt, R, pos);
+    const double x = __ldg(r + 12), y = __ldg(r + 13), z = __ldg(r + 14);
+    c[3 * side] = fma(R[0], x, fma(R[1], y, fma(R[2], z, pos[0])));
+    c[3 * side + 1] = fma(R[3], x, fma(R[4], y, fma(R[5], z, pos[1])));
+    c[3 * side + 2] = fma(R[6], x, fma(R[7], y, fma(R[8], z, pos[2])));
+  }
+  const double dx = c[0] - c[3], dy = c[1] - c[4], dz = c[2] - c[5];
+  const double rA = __ldg(ra + 15), rB = __ldg(rb + 15);
+  *scale = 1.0 + fabs(c[0]) + fabs(c[1]) + fabs(c[2]) + fabs(c[3]) + fabs(c[4]) + fabs(c[5]) + rA + rB;
+  return sqrt(fma(dx, dx, fma(dy, dy, dz * dz))) - (rA + rB);
+}
+
+// Separating-axis cull of one row (see sat_cull_posed), on the cull poses.
+__device__ __forceinline__ bool msat_cull(const BodyInfo* bodies, int ba, int bb, const double* ra, const double* rb,
+                                          double tau, int tab, int n, int i, const PoseTable& pt, double thr) {
+  if (__ldg(ra + 15) < 0.0 || __ldg(rb + 15) < 0.0) return false;  // slivers are never culled
+  double a[9], b[9];
+  {
+    double R[9], pos[3];
+    mcull_pose(bodies, ba, tau, tab & 1, n, i, pt, R, pos);
+    world_corners_fast(R, pos, ra, a);
+    mcull_pose(bodies, bb, tau, (tab >> 1) & 1, n, i, pt, R, pos);
+    world_corners_fast(R, pos, rb, b);
+  }
+  double scale = 1.0 + __ldg(ra + 15) + __ldg(rb + 15);
+#pragma unroll
+  for (int k = 0; k < 3; ++k) scale += fabs(a[k]) + fabs(b[k]);
+  const double T = thr + kCullMargin * scale;
+  auto normal_gap = [&](const double* x, const double* y) {  // x's face normal
+    const double e1x = x[3] - x[0], e1y = x[4] - x[1], e1z = x[5] - x[2];
+    const double e2x = x[6] - x[0], e2y = x[7] - x[1], e2z = x[8] - x[2];
+    const double nx = fma(e1y, e2z, -e1z * e2y), ny = fma(e1z, e2x, -e1x * e2z), nz = fma(e1x, e2y, -e1y * e2x);
+    const double len = sqrt(fma(nx, nx, fma(ny, ny, nz * nz)));
+    return axis_gap(nx, ny, nz, x, y) - T * len;
+  };
+  if (normal_gap(a, b) > 0.0) return true;
+  if (normal_gap(b, a) > 0.0) return true;
+  const double ux = (b[0] + b[3] + b[6]) - (a[0] + a[3] + a[6]);
+  const double uy = (b[1] + b[4] + b[7]) - (a[1] + a[4] + a[7]);
+  const double uz = (b[2] + b[5] + b[8]) - (a[2] + a[5] + a[8]);
+  const double len = sqrt(fma(ux, ux, fma(uy, uy, uz * uz)));
+  return axis_gap(ux, uy, uz, a, b) > T * len;
+}
+
+// Per-row moved-sphere cull, without the square root: the bounding spheres
+// of both triangles moved to tau (same rigid motion as the triangles) are
+// certainly farther apart than T when |c_a - c_b|^2 > (r_a + r_b + T + m)^2,
+// m the cull margin (cull arithmetic, FMA allowed).
+__device__ __forceinline__ bool sphere_clear_at(const BodyInfo* bodies, int ba, int bb, const double* ra,
+                                                const double* rb, double tau, int tab, int n, int i,
+                                                const PoseTable& pt, double T) {
+  double c[6];
+#pragma unroll
+  for (int side = 0; side < 2; ++side) {
+    const int b = side ? bb : ba;
+    const double* r = side ? rb : ra;
+    double R[9], pos[3];
+    mcull_pose(bodies, b, tau, (tab >> side) & 1, n, i, pt, R, pos);
+    const double x = __ldg(r + 12), y = __ldg(r + 13), z = __ldg(r + 14);
+    c[3 * side] = fma(R[0], x, fma(R[1], y, fma(R[2], z, pos[0])));
+    c[3 * side + 1] = fma(R[3], x, fma(R[4], y, fma(R[5], z, pos[1])));
+    c[3 * side + 2] = fma(R[6], x, fma(R[7], y, fma(R[8], z, pos[2])));
+  }
+  const double dx = c[0] - c[3], dy = c[1] - c[4], dz = c[2] - c[5];
+  const double rr = __ldg(ra + 15) + __ldg(rb + 15);
+  const double scale = 1.0 + fabs(c[0]) + fabs(c[1]) + fabs(c[2]) + fabs(c[3]) + fabs(c[4]) + fabs(c[5]) + rr;
+  const double lim = rr + T + kCullMargin * scale;
+  return fma(dx, dx, fma(dy, dy, dz * dz)) > lim * lim;
+}
+
+// Plane-sphere cull of one row: the plane of each triangle at tau against
+// the other triangle's moved bounding sphere.  The triangle lies in its
+// plane, so a sphere entirely on one side by more than T + m certifies a
+// distance above T.  Body-frame normal from the record's corners (rotation
+// keeps |n| and n . v0), so only R n and n . pos are per row; compared in
+// squares, no square root (cull arithmetic, FMA allowed).
+__device__ __forceinline__ bool plane_sphere_clear(const BodyInfo* bodies, int ba, int bb, const double* ra,
+                                                   const double* rb, double tau, int tab, int n, int i,
+                                                   const PoseTable& pt, double T) {
+  double c[6], Rs[2][9], ps[2][3];
+#pragma unroll
+  for (int side = 0; side < 2; ++side) {
+    const int b = side ? bb : ba;
+    const double* r = side ? rb : ra;
+    mcull_pose(bodies, b, tau, (tab >> side) & 1, n, i, pt, Rs[side], ps[side]);
+    const double* R = Rs[side];
+    const double x = __ldg(r + 12), y = __ldg(r + 13), z = __ldg(r + 14);
+    c[3 * side] = fma(R[0], x, fma(R[1], y, fma(R[2], z, ps[side][0])));
+    c[3 * side + 1] = fma(R[3], x, fma(R[4], y, fma(R[5], z, ps[side][1])));
+    c[3 * side + 2] = fma(R[6], x, fma(R[7], y, fma(R[8], z, ps[side][2])));
+  }
+  const double scale = 1.0 + fabs(c[0]) + fabs(c[1]) + fabs(c[2]) + fabs(c[3]) + fabs(c[4]) + fabs(c[5]) +
+                       __ldg(ra + 15) + __ldg(rb + 15);
+#pragma unroll
+  for (int side = 0; side < 2; ++side) {
+    const double* r = side ? rb : ra;    // the plane's triangle
+    const double* q = side ? c : c + 3;  // the other sphere's centre
+    const double rad = __ldg((side ? ra : rb) + 15);
+    const double* R = Rs[side];
+    const double v0x = __ldg(r), v0y = __ldg(r + 1), v0z = __ldg(r + 2);
+    const double e1x = __ldg(r + 3) - v0x, e1y = __ldg(r + 4) - v0y, e1z = __ldg(r + 5) - v0z;
+    const double e2x = __ldg(r + 6) - v0x, e2y = __ldg(r + 7) - v0y, e2z = __ldg(r + 8) - v0z;
+    const double lx = fma(e1y, e2z, -e1z * e2y), ly = fma(e1z, e2x, -e1x * e2z), lz = fma(e1x, e2y, -e1y * e2x);
+    const double nx = fma(R[0], lx, fma(R[1], ly, R[2] * lz));
+    const double ny = fma(R[3], lx, fma(R[4], ly, R[5] * lz));
+    const double nz = fma(R[6], lx, fma(R[7], ly, R[8] * lz));
+    // n . (x - (R v0 + pos)) = n . x - (l . v0 + n . pos)
+    const double o = fma(lx, v0x, fma(ly, v0y, lz * v0z)) + fma(nx, ps[side][0], fma(ny, ps[side][1], nz * ps[side][2]));
+    const double dist_n = fma(nx, q[0], fma(ny, q[1], nz * q[2])) - o;  // signed distance times |n|
+    const double lim = rad + T + kCullMargin * scale;
+    if (lim > 0.0 && dist_n * dist_n > lim * lim * fma(lx, lx, fma(ly, ly, lz * lz))) return true;
+  }
+  return false;
+}
 
 __device__ __forceinline__ int owner_of(const MCandInfo* info, int r) {
   int o = 0;  // last lane with first <= r among lanes that own rows
@@ -117,12 +272,12 @@ k_mscreen(const Cand* __restrict__ front, int64_t n, const PairInfo* __restrict_
       if (__ldg(ra_ + 15) >= 0.0 && __ldg(rb_ + 15) >= 0.0) {
         const double T = fmax(me.thr, add(me.h, kRestSlop));
         double sc0 = 0.0, sc1 = 0.0;
-        const double gap0 = sphere_gap_at(bodies, p.ba, p.bb, ra_, rb_, c.w0, me.tab, me.count, 0, pt, &sc0);
+        const double gap0 = msphere_gap(bodies, p.ba, p.bb, ra_, rb_, c.w0, me.tab, me.count, 0, pt, &sc0);
         const double g0 = gap0 - (T + kCullMargin * sc0);
         double g1 = g0;
         if (p.dt > c.w0) {
-          const double gap1 = sphere_gap_at(bodies, p.ba, p.bb, ra_, rb_, p.dt, me.tab, me.count, me.count - 1, pt,
-                                            &sc1);
+          const double gap1 = msphere_gap(bodies, p.ba, p.bb, ra_, rb_, p.dt, me.tab, me.count, me.count - 1, pt,
+                                          &sc1);
           g1 = gap1 - (T + kCullMargin * sc1);
         }
         if (sp > 0.0) {
@@ -158,11 +313,9 @@ k_mscreen(const Cand* __restrict__ front, int64_t n, const PairInfo* __restrict_
         keep = !(tau < c.cull_lo || tau > c.cull_hi);
         const double* ra_ = tris + c.off_a * kRecord;
         const double* rb_ = tris + c.off_b * kRecord;
-        if (keep && __ldg(ra_ + 15) >= 0.0 && __ldg(rb_ + 15) >= 0.0) {
-          double scale;
-          const double gap = sphere_gap_at(bodies, c.ba, c.bb, ra_, rb_, tau, c.tab, c.count, i, pt, &scale);
-          keep = !(gap > fmax(c.thr, add(c.h, kRestSlop)) + kCullMargin * scale);
-        }
+        if (keep && __ldg(ra_ + 15) >= 0.0 && __ldg(rb_ + 15) >= 0.0)
+          keep = !sphere_clear_at(bodies, c.ba, c.bb, ra_, rb_, tau, c.tab, c.count, i, pt,
+                                  fmax(c.thr, add(c.h, kRestSlop)));
       }
       const unsigned m = __ballot_sync(0xffffffffu, keep);
       if (keep) queue[nq + __popc(m & ((1u << lane) - 1u))] = (uint16_t)(r | (o << 11));
@@ -170,6 +323,31 @@ k_mscreen(const Cand* __restrict__ front, int64_t n, const PairInfo* __restrict_
     }
     __syncwarp();
     const int nq_sphere = nq;
+#if LTSG_PLANE_CULL
+    // (b0) plane-sphere cull of the sphere survivors, compacted in place
+    {
+      int nq2 = 0;
+      for (int q0 = 0; q0 < nq; q0 += 32) {
+        const int q = q0 + lane;
+        bool keep = false;
+        uint16_t e = 0;
+        if (q < nq) {
+          e = queue[q];
+          const int r = e & 2047, o = e >> 11;
+          const MCandInfo& c = info[o];
+          const int i = r - c.first;
+          keep = !plane_sphere_clear(bodies, c.ba, c.bb, tris + c.off_a * kRecord, tris + c.off_b * kRecord,
+                                     cand_tau(c, i), c.tab, c.count, i, pt, fmax(c.thr, add(c.h, kRestSlop)));
+        }
+        const unsigned m = __ballot_sync(0xffffffffu, keep);
+        __syncwarp();
+        if (keep) queue[nq2 + __popc(m & ((1u << lane) - 1u))] = e;
+        nq2 += __popc(m);
+      }
+      nq = nq2;
+    }
+    __syncwarp();
+#endif
     // (b) separating-axis cull of the sphere survivors, compacted in place
     {
       int nq2 = 0;
@@ -182,8 +360,8 @@ k_mscreen(const Cand* __restrict__ front, int64_t n, const PairInfo* __restrict_
           const int r = e & 2047, o = e >> 11;
           const MCandInfo& c = info[o];
           const int i = r - c.first;
-          keep = !sat_cull_posed(bodies, c.ba, c.bb, tris + c.off_a * kRecord, tris + c.off_b * kRecord,
-                                 cand_tau(c, i), c.tab, c.count, i, pt, fmax(c.thr, add(c.h, kRestSlop)));
+          keep = !msat_cull(bodies, c.ba, c.bb, tris + c.off_a * kRecord, tris + c.off_b * kRecord,
+                            cand_tau(c, i), c.tab, c.count, i, pt, fmax(c.thr, add(c.h, kRestSlop)));
         }
         const unsigned m = __ballot_sync(0xffffffffu, keep);
         __syncwarp();

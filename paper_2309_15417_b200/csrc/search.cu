@@ -28,7 +28,7 @@
 #include <vector>
 
 #ifndef LTSG_BOUND
-#define LTSG_BOUND 1  // certified FP32 upper-bound pre-decision in the exact kernels
+#define LTSG_BOUND 0  // certified FP32 upper-bound pre-decision in the exact kernels (measured: no net gain)
 #endif
 
 namespace ltsg {
@@ -336,9 +336,18 @@ constexpr int kPoseEntries = kMaxSamples * (kMaxSamples + 1) / 2;  // 561
 constexpr int kPose = 12;
 
 struct PoseTable {
-  const double* tab;  // n_bodies x kPoseEntries x kPose, or null
-  const double* tdt;  // per body: the dt its table was built for (NaN: none)
+  const double* tab;   // n_bodies x kPoseEntries x kPose, or null
+  const double* tdt;   // per body: the dt its table was built for (NaN: none)
+  const double* cm;    // n_bodies x kCullM: cull-path motion constants (k_cull_prep), or null
 };
+
+// Cull-path motion constants per body: the Rodrigues rotation regrouped as
+// R(tau) = base + sin(w tau) (K base) + (1 - cos(w tau)) (K^2 base), for
+// cull samples off the pose-table grid (cull arithmetic: FMA allowed, the
+// certified margins cover the rounding).
+// Layout: [0..2] x0, [3..5] v, [6..14] base, [15..23] K base, [24..32] K^2 base,
+// [33] omega, [34] spinning (0/1), [35] pad.
+constexpr int kCullM = 36;
 
 __device__ __forceinline__ int grid_entry(int n, int i) { return n * (n - 1) / 2 + i; }
 
@@ -372,6 +381,26 @@ __global__ void k_pose_fill(const BodyInfo* __restrict__ bodies, int n_bodies, c
 #pragma unroll
     for (int k = 0; k < 3; ++k) o[9 + k] = pos[k];
   }
+}
+
+__global__ void k_cull_prep(const BodyInfo* __restrict__ bodies, int n, double* __restrict__ cm) {
+  const int b = blockIdx.x * blockDim.x + threadIdx.x;
+  if (b >= n) return;
+  const Motion& m = bodies[b].m;
+  double* o = cm + (size_t)b * kCullM;
+  for (int k = 0; k < 3; ++k) {
+    o[k] = m.x0[k];
+    o[3 + k] = m.v[k];
+  }
+  for (int r = 0; r < 3; ++r)
+    for (int c = 0; c < 3; ++c) {
+      o[6 + 3 * r + c] = m.base[3 * r + c];
+      o[15 + 3 * r + c] = fma(m.K[3 * r + 2], m.base[6 + c], fma(m.K[3 * r + 1], m.base[3 + c], m.K[3 * r] * m.base[c]));
+      o[24 + 3 * r + c] = fma(m.KK[3 * r + 2], m.base[6 + c], fma(m.KK[3 * r + 1], m.base[3 + c], m.KK[3 * r] * m.base[c]));
+    }
+  o[33] = m.omega;
+  o[34] = m.spinning ? 1.0 : 0.0;
+  o[35] = 0.0;
 }
 
 // Pose of body slot `b` at sample i of linspace(w0, dt, n) (= tau).
@@ -2385,7 +2414,14 @@ static int run_search(const ltsg_scene* sc, ltsg_result* out, ltsg_workspace* ws
 
   tr.mark("world");
   // ---- pose tables for moving batches
-  PoseTable poses{nullptr, nullptr};
+  PoseTable poses{nullptr, nullptr, nullptr};
+  if (!all_static && sc->n_pairs > 0 && sc->n_bodies > 0) {
+    double* cm;
+    LTSG_TRY(ws_get(ws, "cull_m", (size_t)sc->n_bodies * kCullM, &cm));
+    k_cull_prep<<<grid_for(sc->n_bodies, 128), 128, 0, st>>>(pr.bodies, sc->n_bodies, cm);
+    LTSG_LAUNCHED();
+    poses.cm = cm;
+  }
   if (!all_static && sc->n_pairs > 0 && sc->n_bodies > 0 && !getenv("LTSG_NO_POSES")) {
     const size_t bytes = (size_t)sc->n_bodies * kPoseEntries * kPose * sizeof(double);
     if (bytes <= ws->budget / 4) {
@@ -2397,7 +2433,8 @@ static int run_search(const ltsg_scene* sc, ltsg_result* out, ltsg_workspace* ws
       LTSG_LAUNCHED();
       k_pose_fill<<<148 * 16, 128, 0, st>>>(pr.bodies, sc->n_bodies, tdt, tab);
       LTSG_LAUNCHED();
-      poses = PoseTable{tab, tdt};
+      poses.tab = tab;
+      poses.tdt = tdt;
     }
   }
 
