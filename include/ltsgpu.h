@@ -244,6 +244,62 @@ int ltsg_exhaustive_distances(const ltsg_scene* scene, double* out_dist, int64_t
  * the achieved FP64 FLOP/s (2 per DFMA) -- the roofline denominator. */
 int ltsg_fp64_peak(double* tflops, double* ms, void* stream);
 
+
+/* ---------------------------------------------------------------------------
+ * Space-time broad phase: ltsdem.broadphase.build_collision_graph
+ * (broadphase.py:198-252), the step before the narrow phase.  It produces the
+ * candidate pairs (edges) and static links the narrow phase screens.
+ *
+ * particle: (n_particles, 28) float64 records, particles in ascending id
+ *   order: [0:3] old.position [3:7] old.rotation [7] old.t
+ *          [8:11] current.position [11:15] current.rotation [15] current.t
+ *          [16:19] current.velocity [19:22] current.angular_velocity
+ *          [22:25] sphere.center (body frame) [25] sphere.radius [26:28] unused
+ *   (the fields _Trajectory.of_particle reads, :83-95, with particle_dt's
+ *   timeline stamps, :46-50).
+ * statics: (n_statics, 4) float64 world spheres (center, radius) in ascending
+ *   static-id order (_Trajectory.of_static, :97-99).
+ * Body index i < n_particles is particle i, n_particles + k is static k; the
+ * reference's `ids = pids + sids` (:220).
+ */
+typedef struct {
+  const double* particle;
+  const double* statics;
+  int32_t n_particles;
+  int32_t n_statics;
+  double dt_max;  /* TimeStepPolicy.dt_max (:36) */
+  double growth;  /* TimeStepPolicy.growth (:37) */
+} ltsg_broad_input;
+
+typedef struct {
+  double* dts;        /* n_particles: particle_dt per particle (graph.dts); may be NULL */
+  int32_t* edge;      /* (cap_edges, 2) particle indices a < b, in the reference's edge-dict order */
+  double* window;     /* (cap_edges, 2) the pair window of each edge (graph.edges values) */
+  int32_t* link;      /* (cap_links, 2) (particle index, static index), sorted: graph.static_links */
+  int64_t cap_edges;
+  int64_t cap_links;
+  /* filled by the call */
+  int64_t n_edges;
+  int64_t n_links;
+  int64_t candidates; /* body pairs that passed Check 1 (the boxes overlap) */
+  int32_t launches;
+  int32_t pad;
+  double ms;          /* device time of the call (CUDA events) */
+} ltsg_broad_output;
+
+/* Build the collision graph.  Blocks until `stream` has finished the call
+ * (the output counts are read back).  LTSG_ECAPACITY when n_edges/n_links
+ * exceed the capacities: the counts are set, grow and call again. */
+int ltsg_broadphase(const ltsg_broad_input* in, ltsg_broad_output* out, ltsg_workspace* ws, void* stream);
+
+/* check_spacetime_tube / _min_distance_over_window (broadphase.py:128-158) on
+ * explicit trajectory rows: t (n,3) knot times, c (n,3,3) centres, r (n,)
+ * radius, nt (n,) knot count (3 for a particle, 1 for a static); win (n,2).
+ * Writes the minimum centre distance and the Check-2 verdict per row. */
+int ltsg_tube_rows(const double* t1, const double* c1, const double* r1, const int32_t* nt1,
+                   const double* t2, const double* c2, const double* r2, const int32_t* nt2,
+                   const double* win, int64_t n, double* dist, int32_t* hit, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -57,6 +57,19 @@ class Result(C.Structure):
     ]
 
 
+class BroadInput(C.Structure):
+    """ltsg_broad_input (include/ltsgpu.h)."""
+    _fields_ = [("particle", P), ("statics", P), ("n_particles", I32), ("n_statics", I32),
+                ("dt_max", F64), ("growth", F64)]
+
+
+class BroadOutput(C.Structure):
+    """ltsg_broad_output (include/ltsgpu.h)."""
+    _fields_ = [("dts", P), ("edge", P), ("window", P), ("link", P), ("cap_edges", I64), ("cap_links", I64),
+                ("n_edges", I64), ("n_links", I64), ("candidates", I64), ("launches", I32), ("pad", I32),
+                ("ms", F64)]
+
+
 _lock = threading.Lock()
 _lib = None
 
@@ -101,6 +114,8 @@ def lib():
             "ltsg_fuse_contacts": [C.POINTER(Result), I64, P, P, P],
             "ltsg_fp64_peak": [C.POINTER(F64), C.POINTER(F64), P],
             "ltsg_unpack_trees": [C.POINTER(TreeUpload), P, P],
+            "ltsg_broadphase": [C.POINTER(BroadInput), C.POINTER(BroadOutput), P, P],
+            "ltsg_tube_rows": [P, P, P, P, P, P, P, P, P, I64, P, P, P],
         }.items():
             fn = getattr(h, name)
             fn.argtypes = args
@@ -120,7 +135,7 @@ EXPORTED = (
     "ltsg_segment_segment_closest", "ltsg_feature_distances", "ltsg_closest_feature",
     "ltsg_overlap_centroid", "ltsg_workspace_create", "ltsg_workspace_destroy",
     "ltsg_workspace_bytes", "ltsg_search", "ltsg_exhaustive_rows", "ltsg_exhaustive_distances", "ltsg_fuse_contacts", "ltsg_fp64_peak",
-    "ltsg_unpack_trees",
+    "ltsg_unpack_trees", "ltsg_broadphase", "ltsg_tube_rows",
 )
 
 

@@ -93,6 +93,12 @@ class ParticleTimeline:
 
 
 @dataclass
+class BoundingSphere:
+    center: np.ndarray
+    radius: float                       # includes the epsilon halo
+
+
+@dataclass
 class Particle:
     pid: int
     tree: SurrogateTree
@@ -100,12 +106,18 @@ class Particle:
     radius: float                       # bounding-sphere radius about the COM, incl. epsilon
     timeline: ParticleTimeline
 
+    @property
+    def sphere(self) -> BoundingSphere:
+        """make_particle pins the sphere at the mass centre (body.py:73-83)."""
+        return BoundingSphere(center=np.zeros(3), radius=self.radius)
+
 
 @dataclass
 class StaticBody:
     sid: int                            # negative
     tree: SurrogateTree
     epsilon: float
+    sphere: BoundingSphere | None = None  # world frame (body.py:50); the broad phase reads it
 
 
 @dataclass
@@ -165,6 +177,19 @@ def make_particle(pid: int, vertices, triangles, epsilon: float, st: ParticleSta
                     timeline=timeline(st))
 
 
+def bounding_sphere(vertices, epsilon: float) -> BoundingSphere:
+    """Near-minimal sphere around the vertices plus the halo (mesh.py:335-352):
+    from the box centre, 256 shrinking steps toward the farthest vertex."""
+    v = np.asarray(vertices, dtype=np.float64)
+    center = 0.5 * (v.min(axis=0) + v.max(axis=0))
+    for k in range(256):
+        delta = v - center
+        far = int(np.argmax(np.einsum("ij,ij->i", delta, delta)))
+        center = center + delta[far] / (k + 2.0)
+    radius = float(np.linalg.norm(v - center, axis=1).max()) + epsilon
+    return BoundingSphere(center=center, radius=radius)
+
+
 def make_static(sid: int, vertices, triangles, epsilon: float, fanout: int = 4) -> StaticBody:
     from .surrogate import build_surrogate_tree
 
@@ -174,4 +199,4 @@ def make_static(sid: int, vertices, triangles, epsilon: float, fanout: int = 4) 
     t = np.asarray(triangles, dtype=np.int64)
     corners = np.stack([v[t[:, 0]], v[t[:, 1]], v[t[:, 2]]], axis=1)
     return StaticBody(sid=sid, tree=build_surrogate_tree(corners, epsilon, fanout=fanout),
-                      epsilon=float(epsilon))
+                      epsilon=float(epsilon), sphere=bounding_sphere(v, epsilon))

@@ -21,7 +21,7 @@ PKG = os.path.dirname(os.path.abspath(__file__))
 REPO = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
 LIB = os.path.join(PKG, "libltsgpu.so")
-SOURCES = ["rows.cu", "search.cu", "unpack.cu"]
+SOURCES = ["rows.cu", "search.cu", "unpack.cu", "broad.cu"]
 HEADERS = ["common.cuh", "geom.cuh", "dist_staged.cuh", "dist_tile.cuh", "moving.cuh", "bound32.cuh"]
 
 NVCC_FLAGS = [

@@ -61,6 +61,7 @@ struct ltsg_workspace {
   // sizes seen by earlier calls: the async traversal preallocates from them
   size_t hint_front = 0, hint_rest = 0, hint_entries = 0, hint_cross = 0, hint_seed = 0;
   size_t hint_mrows = 0;  // moving path: most surviving rows of one generation
+  size_t hint_bp_cand = 0;  // broad phase: most Check-1 candidates seen
   int hint_gens = 0;  // deepest traversal seen: async mode launches one generation more
 
   int get(const char* name, size_t bytes, void** out, bool keep = false);

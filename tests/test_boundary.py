@@ -41,8 +41,10 @@ def _c_struct_sizes():
 #include <stddef.h>
 #include "ltsgpu.h"
 int main(void) {
-  printf("%zu %zu %zu %zu\n", sizeof(ltsg_scene), offsetof(ltsg_scene, max_children),
-         sizeof(ltsg_result), offsetof(ltsg_result, rows_bound));
+  printf("%zu %zu %zu %zu %zu %zu %zu %zu\n", sizeof(ltsg_scene), offsetof(ltsg_scene, max_children),
+         sizeof(ltsg_result), offsetof(ltsg_result, rows_bound),
+         sizeof(ltsg_broad_input), offsetof(ltsg_broad_input, growth),
+         sizeof(ltsg_broad_output), offsetof(ltsg_broad_output, ms));
   return 0;
 }
 '''
@@ -56,11 +58,15 @@ int main(void) {
 
 
 def test_ctypes_structs_match_the_header():
-    s, s_last, r, r_last = _c_struct_sizes()
+    s, s_last, r, r_last, bi, bi_last, bo, bo_last = _c_struct_sizes()
     assert ctypes.sizeof(_lib.Scene) == s
     assert _lib.Scene.max_children.offset == s_last
     assert ctypes.sizeof(_lib.Result) == r
     assert _lib.Result.rows_bound.offset == r_last
+    assert ctypes.sizeof(_lib.BroadInput) == bi
+    assert _lib.BroadInput.growth.offset == bi_last
+    assert ctypes.sizeof(_lib.BroadOutput) == bo
+    assert _lib.BroadOutput.ms.offset == bo_last
 
 
 def test_missing_device_fails_loudly():
