@@ -57,9 +57,73 @@ __device__ __forceinline__ double cand_tau(const MCandInfo& c, int i) {
 #define LTSG_PLANE_CULL 0  // measured: costs more than it saves
 #endif
 #ifndef LTSG_MSCREEN_MINB
-#define LTSG_MSCREEN_MINB 3
+#define LTSG_MSCREEN_MINB 5
 #endif
-constexpr int kMWarps = 8;
+#ifndef LTSG_MSCREEN_WARPS
+#define LTSG_MSCREEN_WARPS 4
+#endif
+constexpr int kMWarps = LTSG_MSCREEN_WARPS;
+
+// Per-candidate sphere-centre trajectory for the window and per-row sphere
+// culls.  With the body's cull constants (k_cull_prep: x0, v, and the
+// regrouped Rodrigues base / K base / K^2 base) a triangle's bounding-sphere
+// centre s moves as
+//   c(tau) = (x0 + base s) + tau v + sin(w tau) (K base s) + (1 - cos(w tau)) (K^2 base s),
+// so the centre difference of the two triangles is 18 constants plus the
+// two angular speeds; a row evaluates it from shared memory with two
+// sincos and no rotation matrix.  The cull margin's scale uses a bound of
+// |c| over [0, dt] (|x0 + base s| + dt |v| + |K base s| + 2 |K^2 base s|),
+// so it never underestimates the per-row scale.
+// Layout (SoA over the warp's 32 candidates): [0..2] dP0, [3..5] dV,
+// [6..8] Ba, [9..11] Ca, [12..14] Bb, [15..17] Cb, [18] wa, [19] wb,
+// [20] lim^2 of the row test (+inf: slivers are never culled), [21] scale bound.
+constexpr int kTraj = 22;
+
+struct TrajSide {
+  double p0[3], v[3], b[3], c[3], w, bound;
+};
+
+__device__ __forceinline__ TrajSide traj_side(const double* cm, const double* r, double dt) {
+  TrajSide t;
+  const double x = __ldg(r + 12), y = __ldg(r + 13), z = __ldg(r + 14);
+  const bool spin = __ldg(cm + 34) != 0.0;
+  t.w = spin ? __ldg(cm + 33) : 0.0;
+  t.bound = 0.0;
+#pragma unroll
+  for (int k = 0; k < 3; ++k) {
+    t.p0[k] = fma(__ldg(cm + 6 + 3 * k), x, fma(__ldg(cm + 7 + 3 * k), y, fma(__ldg(cm + 8 + 3 * k), z, __ldg(cm + k))));
+    t.v[k] = __ldg(cm + 3 + k);
+    t.b[k] = spin ? fma(__ldg(cm + 15 + 3 * k), x, fma(__ldg(cm + 16 + 3 * k), y, __ldg(cm + 17 + 3 * k) * z)) : 0.0;
+    t.c[k] = spin ? fma(__ldg(cm + 24 + 3 * k), x, fma(__ldg(cm + 25 + 3 * k), y, __ldg(cm + 26 + 3 * k) * z)) : 0.0;
+    t.bound += fabs(t.p0[k]) + dt * fabs(t.v[k]) + fabs(t.b[k]) + 2.0 * fabs(t.c[k]);
+  }
+  return t;
+}
+
+// squared centre distance at tau from a warp's trajectory table (candidate o)
+__device__ __forceinline__ double traj_d2(const double (*tr)[32], int o, double tau) {
+  double sa = 0.0, ca = 0.0, sb = 0.0, cb = 0.0;
+  const double wa = tr[18][o], wb = tr[19][o];
+  if (wa != 0.0) {
+    sincos(wa * tau, &sa, &ca);
+    ca = 1.0 - ca;
+  }
+  if (wb != 0.0) {
+    sincos(wb * tau, &sb, &cb);
+    cb = 1.0 - cb;
+  }
+  double d2 = 0.0;
+#pragma unroll
+  for (int k = 0; k < 3; ++k) {
+    double d = fma(tau, tr[3 + k][o], tr[k][o]);
+    d = fma(sa, tr[6 + k][o], d);
+    d = fma(ca, tr[9 + k][o], d);
+    d = fma(-sb, tr[12 + k][o], d);
+    d = fma(-cb, tr[15 + k][o], d);
+    d2 = fma(d, d, d2);
+  }
+  return d2;
+}
 constexpr int kMRows = 32 * kMaxSamples;  // rows of one warp's 32 candidates, at most
 
 // Pose for the culls at sample i of linspace(w0, dt, n) (= tau): the pose
@@ -230,11 +294,13 @@ k_mscreen(const Cand* __restrict__ front, int64_t n, const PairInfo* __restrict_
   if (out.n_in) n = (int64_t)min(*out.n_in, out.next_cap);
   __shared__ MCandInfo s_info[kMWarps][32];
   __shared__ uint16_t s_queue[kMWarps][kMRows];  // row (11 bits) | owner lane << 11
+  __shared__ double s_traj[kMWarps][kTraj][32];
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
   const int64_t n_warps = (n + 31) / 32;
   MCandInfo* info = s_info[warp];
   uint16_t* queue = s_queue[warp];
+  double(*traj)[32] = s_traj[warp];
   unsigned long long acc_rows = 0, acc_exact = 0, acc_window = 0, acc_sphere = 0;
 
   for (int64_t wi = blockIdx.x * (int64_t)kMWarps + warp; wi < n_warps; wi += (int64_t)gridDim.x * kMWarps) {
@@ -269,17 +335,29 @@ k_mscreen(const Cand* __restrict__ front, int64_t n, const PairInfo* __restrict_
       // `speed`-Lipschitz, evaluated at both window ends
       me.cull_lo = -1.0;
       me.cull_hi = 2.0 * p.dt + 1.0;
-      if (__ldg(ra_ + 15) >= 0.0 && __ldg(rb_ + 15) >= 0.0) {
-        const double T = fmax(me.thr, add(me.h, kRestSlop));
-        double sc0 = 0.0, sc1 = 0.0;
-        const double gap0 = msphere_gap(bodies, p.ba, p.bb, ra_, rb_, c.w0, me.tab, me.count, 0, pt, &sc0);
-        const double g0 = gap0 - (T + kCullMargin * sc0);
+      // the sphere-centre trajectories (see kTraj)
+      const TrajSide sa_ = traj_side(pt.cm + (size_t)p.ba * kCullM, ra_, p.dt);
+      const TrajSide sb_ = traj_side(pt.cm + (size_t)p.bb * kCullM, rb_, p.dt);
+#pragma unroll
+      for (int k = 0; k < 3; ++k) {
+        traj[k][lane] = sa_.p0[k] - sb_.p0[k];
+        traj[3 + k][lane] = sa_.v[k] - sb_.v[k];
+        traj[6 + k][lane] = sa_.b[k];
+        traj[9 + k][lane] = sa_.c[k];
+        traj[12 + k][lane] = sb_.b[k];
+        traj[15 + k][lane] = sb_.c[k];
+      }
+      traj[18][lane] = sa_.w;
+      traj[19][lane] = sb_.w;
+      const double rA = __ldg(ra_ + 15), rB = __ldg(rb_ + 15);
+      const double scale = 1.0 + sa_.bound + sb_.bound + fabs(rA) + fabs(rB);
+      const double T = fmax(me.thr, add(me.h, kRestSlop));
+      const double lim = rA + rB + T + kCullMargin * scale;
+      traj[20][lane] = (rA >= 0.0 && rB >= 0.0) ? lim * lim : CUDART_INF;
+      if (rA >= 0.0 && rB >= 0.0) {
+        const double g0 = sqrt(traj_d2(traj, lane, c.w0)) - lim;
         double g1 = g0;
-        if (p.dt > c.w0) {
-          const double gap1 = msphere_gap(bodies, p.ba, p.bb, ra_, rb_, p.dt, me.tab, me.count, me.count - 1, pt,
-                                          &sc1);
-          g1 = gap1 - (T + kCullMargin * sc1);
-        }
+        if (p.dt > c.w0) g1 = sqrt(traj_d2(traj, lane, p.dt)) - lim;
         if (sp > 0.0) {
           me.cull_lo = c.w0 + g0 / sp;
           me.cull_hi = p.dt - g1 / sp;
@@ -311,11 +389,7 @@ k_mscreen(const Cand* __restrict__ front, int64_t n, const PairInfo* __restrict_
         const int i = r - c.first;
         const double tau = cand_tau(c, i);
         keep = !(tau < c.cull_lo || tau > c.cull_hi);
-        const double* ra_ = tris + c.off_a * kRecord;
-        const double* rb_ = tris + c.off_b * kRecord;
-        if (keep && __ldg(ra_ + 15) >= 0.0 && __ldg(rb_ + 15) >= 0.0)
-          keep = !sphere_clear_at(bodies, c.ba, c.bb, ra_, rb_, tau, c.tab, c.count, i, pt,
-                                  fmax(c.thr, add(c.h, kRestSlop)));
+        if (keep) keep = !(traj_d2(traj, o, tau) > traj[20][o]);
       }
       const unsigned m = __ballot_sync(0xffffffffu, keep);
       if (keep) queue[nq + __popc(m & ((1u << lane) - 1u))] = (uint16_t)(r | (o << 11));

@@ -21,6 +21,7 @@
 #include "dist_tile.cuh"
 
 #include <cub/cub.cuh>
+#include <math_constants.h>
 
 #include <algorithm>
 #include <cstdlib>
@@ -2518,8 +2519,9 @@ static int run_search(const ltsg_scene* sc, ltsg_result* out, ltsg_workspace* ws
         return LTSG_ECAPACITY;
       }
       const RowList rl{mrows, mrows_cap, xcnt};
-      const int64_t mblocks = n_in ? 148LL * LTSG_MSCREEN_MINB * 8 : (n + 32 * kMWarps - 1) / (32 * kMWarps);
-      k_mscreen<<<(int)std::max<int64_t>(1, std::min<int64_t>(mblocks, 148LL * LTSG_MSCREEN_MINB * 8)),
+      const int64_t mcap = 148LL * LTSG_MSCREEN_MINB * 64 / kMWarps;
+      const int64_t mblocks = n_in ? mcap : (n + 32 * kMWarps - 1) / (32 * kMWarps);
+      k_mscreen<<<(int)std::max<int64_t>(1, std::min<int64_t>(mblocks, mcap)),
                   32 * kMWarps, 0, st>>>(in, n, pr.pairs, pr.bodies, sc->tris, so, poses, rl);
       LTSG_LAUNCHED();
       const size_t e = 3 * n_timed++;
