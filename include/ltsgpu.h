@@ -300,6 +300,81 @@ int ltsg_tube_rows(const double* t1, const double* c1, const double* r1, const i
                    const double* t2, const double* c2, const double* r2, const int32_t* nt2,
                    const double* win, int64_t n, double* dist, int32_t* hit, void* stream);
 
+/* ---------------------------------------------------------------------------
+ * Contact consumers: ltsdem.contacts (contacts.py), the step after the narrow
+ * phase, for many clusters ("problems") in one launch.  A dynamic body may
+ * appear in the contacts of one problem only (engine clusters are disjoint).
+ *
+ * body: (n_bodies, 24) float64 records of the bodies' current snapshots:
+ *   [0:3] position [3:6] velocity [6:10] rotation [10:13] angular_velocity
+ *   [13] t [14] 1 / mass [15:24] body-frame inverse inertia (row-major)
+ *   (what _contact_arm reads, contacts.py:100-111, body.py:39-41).
+ * Contacts of problem p are [contact_offset[p], contact_offset[p+1]) in the
+ * caller's order; side (n, 2) holds each side's body index, -1 for a static.
+ */
+typedef struct {
+  const double* body;
+  int32_t n_bodies;
+  int32_t n_problems;
+  const int64_t* contact_offset; /* n_problems + 1 */
+  const int32_t* side;           /* (n_contacts, 2) */
+  const double* position;        /* (n_contacts, 3) ContactPoint.position */
+  const double* normal;          /* (n_contacts, 3) ContactPoint.normal */
+  const double* t;               /* (n_contacts) ContactPoint.t */
+  int64_t n_contacts;
+  double restitution, friction, relaxation, penalty, threshold; /* SolverConfig (contacts.py:26-33) */
+  int32_t max_iterations;
+  int32_t pad;
+} ltsg_solve_input;
+
+typedef struct {
+  double* velocity;          /* (n_bodies, 3) post-impulse velocity of every touched body */
+  double* angular_velocity;  /* (n_bodies, 3) */
+  int32_t* touched;          /* (n_bodies) 1 if the body is a dynamic side of some contact */
+  double* normal_impulse;    /* (n_contacts) ImpulseSolution.normal_impulses */
+  double* friction_impulse;  /* (n_contacts, 3) ImpulseSolution.friction_impulses */
+  int32_t* color;            /* (n_contacts) colour class (color_contact_graph) */
+  int32_t* iterations;       /* (n_problems) */
+  int32_t* converged;        /* (n_problems) */
+  int32_t launches;
+  int32_t pad;
+  double ms;                 /* device time of the call */
+} ltsg_solve_output;
+
+/* solve_impulses (contacts.py:114-198) per problem, with color_contact_graph
+ * (:58-78).  Blocks until `stream` has finished the call. */
+int ltsg_solve_impulses(const ltsg_solve_input* in, ltsg_solve_output* out, ltsg_workspace* ws, void* stream);
+
+typedef struct {
+  const double* body;            /* (n_bodies, 24) as ltsg_solve_input */
+  int32_t n_bodies;
+  int32_t n_problems;
+  const int64_t* member_offset;  /* n_problems + 1 */
+  const int32_t* member;         /* body indices of each problem's cluster members */
+  const double* t_new;           /* (n_problems) cluster.t_current + result.dt */
+  const int64_t* contact_offset; /* n_problems + 1: the committed contacts */
+  const int32_t* side;           /* (n_contacts, 2) body index or -1 */
+  const int64_t* id;             /* (n_contacts, 2) body ids (ContactPoint.body_a/b; statics negative) */
+  const double* normal;          /* (n_contacts, 3) */
+  const double* t;               /* (n_contacts) */
+  const double* depth;           /* (n_contacts) */
+  int64_t n_contacts;
+  const double* velocity;        /* solution (ltsg_solve_output), or NULL for none */
+  const double* angular_velocity;
+  const int32_t* touched;
+  double beta;                   /* SolverConfig.beta */
+  const double* new_state_in;    /* NULL: integrate; else (n_bodies, 14) new snapshots to start from
+                                    (apply_separation alone, contacts.py:256-285) */
+  int32_t separate;              /* 1: apply_separation after the integration */
+  int32_t pad;
+} ltsg_integrate_input;
+
+/* integrate_cluster (contacts.py:225-253) then apply_separation (:256-285)
+ * per problem: new_state (n_bodies, 14) receives each member's prospective
+ * snapshot [0:3] position [3:6] velocity [6:10] rotation [10:13]
+ * angular_velocity [13] t (rows of non-members are untouched). */
+int ltsg_integrate(const ltsg_integrate_input* in, double* new_state, ltsg_workspace* ws, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

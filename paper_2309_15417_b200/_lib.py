@@ -70,6 +70,29 @@ class BroadOutput(C.Structure):
                 ("ms", F64)]
 
 
+class SolveInput(C.Structure):
+    """ltsg_solve_input (include/ltsgpu.h)."""
+    _fields_ = [("body", P), ("n_bodies", I32), ("n_problems", I32), ("contact_offset", P), ("side", P),
+                ("position", P), ("normal", P), ("t", P), ("n_contacts", I64), ("restitution", F64),
+                ("friction", F64), ("relaxation", F64), ("penalty", F64), ("threshold", F64),
+                ("max_iterations", I32), ("pad", I32)]
+
+
+class SolveOutput(C.Structure):
+    """ltsg_solve_output (include/ltsgpu.h)."""
+    _fields_ = [("velocity", P), ("angular_velocity", P), ("touched", P), ("normal_impulse", P),
+                ("friction_impulse", P), ("color", P), ("iterations", P), ("converged", P), ("launches", I32),
+                ("pad", I32), ("ms", F64)]
+
+
+class IntegrateInput(C.Structure):
+    """ltsg_integrate_input (include/ltsgpu.h)."""
+    _fields_ = [("body", P), ("n_bodies", I32), ("n_problems", I32), ("member_offset", P), ("member", P),
+                ("t_new", P), ("contact_offset", P), ("side", P), ("id", P), ("normal", P), ("t", P), ("depth", P),
+                ("n_contacts", I64), ("velocity", P), ("angular_velocity", P), ("touched", P), ("beta", F64),
+                ("new_state_in", P), ("separate", I32), ("pad", I32)]
+
+
 _lock = threading.Lock()
 _lib = None
 
@@ -116,6 +139,8 @@ def lib():
             "ltsg_unpack_trees": [C.POINTER(TreeUpload), P, P],
             "ltsg_broadphase": [C.POINTER(BroadInput), C.POINTER(BroadOutput), P, P],
             "ltsg_tube_rows": [P, P, P, P, P, P, P, P, P, I64, P, P, P],
+            "ltsg_solve_impulses": [C.POINTER(SolveInput), C.POINTER(SolveOutput), P, P],
+            "ltsg_integrate": [C.POINTER(IntegrateInput), P, P, P],
         }.items():
             fn = getattr(h, name)
             fn.argtypes = args
@@ -135,7 +160,7 @@ EXPORTED = (
     "ltsg_segment_segment_closest", "ltsg_feature_distances", "ltsg_closest_feature",
     "ltsg_overlap_centroid", "ltsg_workspace_create", "ltsg_workspace_destroy",
     "ltsg_workspace_bytes", "ltsg_search", "ltsg_exhaustive_rows", "ltsg_exhaustive_distances", "ltsg_fuse_contacts", "ltsg_fp64_peak",
-    "ltsg_unpack_trees", "ltsg_broadphase", "ltsg_tube_rows",
+    "ltsg_unpack_trees", "ltsg_broadphase", "ltsg_tube_rows", "ltsg_solve_impulses", "ltsg_integrate",
 )
 
 

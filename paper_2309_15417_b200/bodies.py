@@ -91,6 +91,10 @@ class ParticleTimeline:
     new: ParticleState | None = None
     version: int = field(default=0, compare=False)
 
+    def touch(self) -> None:
+        """Bumped on every mutation so caches keyed on timelines stay honest (state.py:70-75)."""
+        self.version += 1
+
 
 @dataclass
 class BoundingSphere:

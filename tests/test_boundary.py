@@ -41,10 +41,13 @@ def _c_struct_sizes():
 #include <stddef.h>
 #include "ltsgpu.h"
 int main(void) {
-  printf("%zu %zu %zu %zu %zu %zu %zu %zu\n", sizeof(ltsg_scene), offsetof(ltsg_scene, max_children),
+  printf("%zu %zu %zu %zu %zu %zu %zu %zu %zu %zu %zu %zu %zu %zu\n", sizeof(ltsg_scene), offsetof(ltsg_scene, max_children),
          sizeof(ltsg_result), offsetof(ltsg_result, rows_bound),
          sizeof(ltsg_broad_input), offsetof(ltsg_broad_input, growth),
-         sizeof(ltsg_broad_output), offsetof(ltsg_broad_output, ms));
+         sizeof(ltsg_broad_output), offsetof(ltsg_broad_output, ms),
+         sizeof(ltsg_solve_input), offsetof(ltsg_solve_input, max_iterations),
+         sizeof(ltsg_solve_output), offsetof(ltsg_solve_output, ms),
+         sizeof(ltsg_integrate_input), offsetof(ltsg_integrate_input, separate));
   return 0;
 }
 '''
@@ -58,7 +61,7 @@ int main(void) {
 
 
 def test_ctypes_structs_match_the_header():
-    s, s_last, r, r_last, bi, bi_last, bo, bo_last = _c_struct_sizes()
+    s, s_last, r, r_last, bi, bi_last, bo, bo_last, si, si_last, so, so_last, ii, ii_last = _c_struct_sizes()
     assert ctypes.sizeof(_lib.Scene) == s
     assert _lib.Scene.max_children.offset == s_last
     assert ctypes.sizeof(_lib.Result) == r
@@ -67,6 +70,9 @@ def test_ctypes_structs_match_the_header():
     assert _lib.BroadInput.growth.offset == bi_last
     assert ctypes.sizeof(_lib.BroadOutput) == bo
     assert _lib.BroadOutput.ms.offset == bo_last
+    assert ctypes.sizeof(_lib.SolveInput) == si and _lib.SolveInput.max_iterations.offset == si_last
+    assert ctypes.sizeof(_lib.SolveOutput) == so and _lib.SolveOutput.ms.offset == so_last
+    assert ctypes.sizeof(_lib.IntegrateInput) == ii and _lib.IntegrateInput.separate.offset == ii_last
 
 
 def test_missing_device_fails_loudly():
