@@ -530,6 +530,168 @@ def summarize(m, steps, peak, cpu, par, world, total_ms=None, e2e_total=None, te
     }
 
 
+# ------------------------------------------------------------------ broad phase
+
+BROAD_WORKLOADS = (("broadphase_c5", "c5", 0.1), ("broadphase_c3", "c3", 0.1))
+
+
+def broad_workload(label, scene, dt_max, steps, warmup, cpu):
+    """The broad phase (ltsg_broadphase) over a scene's bodies: device time of
+    the call, e2e through broadphase.build_collision_graph from the host
+    bodies, and parity of the graph against the oracle (which is also the CPU
+    baseline, one process)."""
+    import numpy as np
+    import torch
+
+    from paper_2309_15417_b200 import broadphase as BP
+
+    pol = BP.TimeStepPolicy(dt_max=dt_max)
+    parts = scene.particles
+    statics = scene.statics
+    pids, sids = sorted(parts), sorted(statics)
+    rec, srec = BP.pack_particles(parts, pids), BP.pack_statics(statics, sids)
+    d_in = (torch.from_numpy(rec).cuda(), torch.from_numpy(srec).cuda())
+    for _ in range(warmup):
+        ga = BP.graph_arrays(rec, srec, pol, device_inputs=d_in)
+    dev_ms = []
+    for _ in range(steps):
+        ga = BP.graph_arrays(rec, srec, pol, device_inputs=d_in)
+        dev_ms.append(ga.ms)
+    for _ in range(2):
+        g = BP.build_collision_graph(parts, statics, pol)
+    e2e_ms = []
+    for _ in range(steps):
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        g = BP.build_collision_graph(parts, statics, pol)
+        e2e_ms.append(1e3 * (time.perf_counter() - t0))
+    n = len(pids) + len(sids)
+    out = {"value": n / (np.median(dev_ms) * 1e-3), "unit": "bodies/s", "ms_per_step": float(np.median(dev_ms)),
+           "bodies": n, "particles": len(pids), "statics": len(sids), "dt_max": dt_max,
+           "check1_pairs": ga.candidates, "edges": len(ga.edge), "links": len(ga.link),
+           "gpu_launches": ga.launches,
+           "e2e": {"value": n / (np.median(e2e_ms) * 1e-3), "unit": "bodies/s",
+                   "ms_per_step": float(np.median(e2e_ms)), "h2d_bytes_per_step": int(rec.nbytes + srec.nbytes),
+                   "d2h_bytes_per_step": int(ga.edge.nbytes + ga.window.nbytes + ga.link.nbytes + ga.dts.nbytes),
+                   "path": "broadphase.build_collision_graph(particles, statics, policy) from the host bodies"},
+           "description": f"collision graph (broadphase.py:198-252) of the {scene.name} bodies, dt_max {dt_max}"}
+    if cpu:
+        from oracle import broad_oracle as BO
+
+        t0 = time.perf_counter()
+        o = BO.build_collision_graph(rec, srec, np.asarray(pids), np.asarray(sids), dt_max, pol.growth)
+        wall = time.perf_counter() - t0
+        same = list(o.edges.items()) == list(g.edges.items()) and o.static_links == g.static_links \
+            and o.dts == g.dts
+        out["cpu_baseline"] = {"value": n / wall, "unit": "bodies/s", "cores": 1, "kind": "port",
+                               "sample": f"the whole scene through the numpy oracle (all-pairs Check 1), "
+                                         f"{wall:.2f} s", "cpu_model": cpu_model()}
+        out["parity"] = {"checked": 1, "bit_exact": int(same), "edges": len(o.edges), "ok": bool(same)}
+    return out
+
+
+# ------------------------------------------------------------------ contact consumers
+
+def contacts_workload(scene, batch, steps, warmup, cpu):
+    """The contact consumers (ltsg_solve_impulses + ltsg_integrate) on the
+    fused contacts the narrow phase found for the scene's clusters: every
+    cluster of the sweep in one launch each.  The scene bodies carry no mass
+    properties, so each gets a solid sphere's of its bounding radius (unit
+    density).  CPU baseline and parity: the contact oracle on the same
+    clusters."""
+    import numpy as np
+    import torch
+    from types import SimpleNamespace as NS
+
+    from paper_2309_15417_b200 import contacts as CS
+    from paper_2309_15417_b200.ccd import ContactPoint
+
+    parts = scene.particles
+    for p in parts.values():
+        if getattr(p, "mass", None) is None:
+            r = float(p.radius)
+            m = (4.0 / 3.0) * np.pi * r ** 3
+            p.mass = NS(mass=m, inverse_inertia=np.eye(3) / (0.4 * m * r * r))
+    off = batch.fused_offset
+    live = [q for q in range(len(batch)) if off[q + 1] > off[q]]
+    cl = batch.contacts
+    lists = [[ContactPoint(body_a=int(cl["body_a"][i]), body_b=int(cl["body_b"][i]), position=cl["position"][i],
+                           normal=cl["normal"][i], depth=float(cl["depth"][i]), t=float(cl["t"][i]),
+                           tri_a=int(cl["tri_a"][i]), tri_b=int(cl["tri_b"][i]), threshold=float(cl["threshold"][i]))
+              for i in range(off[q], off[q + 1])] for q in live]
+    order = np.argsort(scene.problem, kind="stable")
+    bounds = np.searchsorted(scene.problem[order], np.arange(scene.n_problems + 1))
+    members = []
+    for q in live:
+        ids = set()
+        for i in order[bounds[q]:bounds[q + 1]]:
+            ids.update(b for b in scene.pairs[i] if b >= 0)
+        members.append(tuple(sorted(ids)))
+    cfg = CS.SolverConfig()
+    pk = CS._Packed(lists, parts)
+    n_c = pk.n
+    for _ in range(warmup):
+        r = CS.solve_arrays(pk.body, pk.side, pk.position, pk.normal, pk.t, pk.offset, cfg)
+    dev_ms = []
+    for _ in range(steps):
+        r = CS.solve_arrays(pk.body, pk.side, pk.position, pk.normal, pk.t, pk.offset, cfg)
+        dev_ms.append(r["ms"])
+    clusters = [NS(members=ms, t_current=0.0, dt=float(batch.dt[q])) for ms, q in zip(members, live)]
+    results = [NS(dt=float(batch.dt[q]), contacts=c) for q, c in zip(live, lists)]
+    e2e_ms = []
+    sols = None
+    for i in range(warmup + steps):
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        sols = CS.solve_batch(lists, parts, cfg)
+        CS.integrate_batch(clusters, parts, results, sols, beta=cfg.beta)
+        if i >= warmup:
+            e2e_ms.append(1e3 * (time.perf_counter() - t0))
+    iters = [s.iterations for s in sols]
+    out = {"value": n_c / (np.median(dev_ms) * 1e-3), "unit": "contacts/s", "ms_per_step": float(np.median(dev_ms)),
+           "clusters": len(live), "contacts": n_c, "iterations_mean": float(np.mean(iters)),
+           "iterations_max": int(np.max(iters)), "gpu_launches": 2,
+           "e2e": {"value": n_c / (np.median(e2e_ms) * 1e-3), "unit": "contacts/s",
+                   "ms_per_step": float(np.median(e2e_ms)),
+                   "h2d_bytes_per_step": int(pk.body.nbytes + pk.side.nbytes + pk.position.nbytes + pk.normal.nbytes
+                                             + pk.t.nbytes + pk.offset.nbytes),
+                   "d2h_bytes_per_step": int(len(pk.ids) * (6 * 8 + 4 + 14 * 8) + n_c * 4 * 8),
+                   "path": "contacts.solve_batch + contacts.integrate_batch (integrate_cluster + apply_separation) "
+                           "from the host bodies, every cluster of the sweep in one launch each"},
+           "description": f"solve_impulses / integrate_cluster / apply_separation (contacts.py:114-285) on the fused "
+                          f"contacts of the {scene.name} clusters (synthetic unit-density sphere masses)"}
+    if cpu:
+        from oracle import contact_oracle as CO
+
+        bodies = {b: pk.body[i] for b, i in pk.index.items()}
+        ocfg = {k: getattr(cfg, k) for k in ("restitution", "friction", "relaxation", "penalty", "threshold",
+                                             "max_iterations")}
+        t0 = time.perf_counter()
+        done, worst, exact = 0, 0.0, 0
+        budget = 20.0
+        for q, lst in enumerate(lists):
+            if time.perf_counter() - t0 > budget:
+                break
+            oc = [{"body_a": c.body_a, "body_b": c.body_b, "position": c.position, "normal": c.normal, "t": c.t,
+                   "depth": c.depth} for c in lst]
+            vel, ang, it, conv, lam, fric = CO.solve_impulses(oc, bodies, ocfg)
+            done += 1
+            same = it == sols[q].iterations and list(vel) == list(sols[q].velocities)
+            err = max([float(np.max(np.abs(sols[q].velocities[b] - vel[b]) / (1.0 + np.abs(vel[b]))))
+                       for b in vel] + [0.0])
+            worst = max(worst, err)
+            exact += same and err == 0.0
+        wall = time.perf_counter() - t0
+        n_done = sum(len(lists[q]) for q in range(done))
+        out["cpu_baseline"] = {"value": n_done / wall, "unit": "contacts/s", "cores": 1, "kind": "port",
+                               "sample": f"the first {done} of {len(lists)} clusters ({n_done} contacts) through "
+                                         f"the numpy contact oracle, {wall:.1f} s", "cpu_model": cpu_model()}
+        out["parity"] = {"checked": done, "bit_exact": exact, "max_velocity_rel_err": worst,
+                         "contract": "spinning bodies (sin/cos): velocities within 1e-12 relative",
+                         "ok": bool(worst <= 1e-12)}
+    return out
+
+
 def run_ours(args, rank, world, local_rank):
     import ctypes as C
 
@@ -609,6 +771,7 @@ def run_ours(args, rank, world, local_rank):
 
     clocks = ClockSampler(local_rank).__enter__()
     results = {}
+    c5_batch = None
     for i, (label, config, exhaustive, scene, problems, hs, cpu, idx, ores, spinning, setup_s) in enumerate(prep):
         steps = args.steps if i == 0 else min(args.steps, args.secondary_steps)
         m = gpu_workload(label, config, exhaustive, scene, problems, hs, steps, args.warmup, flush, dist,
@@ -630,7 +793,19 @@ def run_ours(args, rank, world, local_rank):
         s["setup_s"] = setup_s
         s["description"] = CONFIG_DOC[config] + (", exhaustive (every fine x fine row screened)" if exhaustive else "")
         results[label] = (m, s)
+        if label == "c5" and full and rank == 0:
+            c5_batch = m["last"]
         del m["last"]
+    broad = {}
+    consumers = None
+    if full and rank == 0 and c5_batch is not None:
+        consumers = {"contacts_c5": contacts_workload(built["c5"][0], c5_batch, min(args.steps, 10), args.warmup,
+                                                      not args.no_cpu)}
+    if full and rank == 0:
+        for label, config, dt_max in BROAD_WORKLOADS:
+            if config in built:
+                broad[label] = broad_workload(label, built[config][0], dt_max, min(args.steps, 10), args.warmup,
+                                              not args.no_cpu)
     clocks.__exit__(None, None, None)
 
     if rank == 0:
@@ -680,6 +855,10 @@ def run_ours(args, rank, world, local_rank):
         }
         if len(results) > 1:
             line["configs"] = {lab: s for lab, (m, s) in results.items() if lab != label0}
+        if broad:
+            line["broadphase"] = broad
+        if consumers:
+            line["contact_consumers"] = consumers
         print(json.dumps(line), flush=True)
     if dist is not None:
         dist.destroy_process_group()

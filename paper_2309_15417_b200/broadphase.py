@@ -87,9 +87,19 @@ def _sphere(body):
     return np.zeros(3), float(body.radius)
 
 
-def pack_particles(particles: dict, pids=None) -> np.ndarray:
+try:  # the C gather of the records (csrc/fastpack.c), built in-tree by build.build_fastpack
+    from . import _fastpack
+except ImportError:  # pragma: no cover
+    _fastpack = None
+
+
+def pack_particles(particles: dict, pids=None, out=None) -> np.ndarray:
     """(n, 28) records of the particles in ascending id order."""
     pids = sorted(particles) if pids is None else pids
+    if _fastpack is not None:
+        rec = np.empty((len(pids), RECORD), dtype=np.float64) if out is None else out
+        _fastpack.gather_broad([particles[p] for p in pids], rec)
+        return rec
     rec = np.zeros((len(pids), RECORD), dtype=np.float64)
     for k, pid in enumerate(pids):
         p = particles[pid]
@@ -183,14 +193,14 @@ def build_collision_graph(particles: dict, statics: dict, policy: TimeStepPolicy
     if not pids:
         return CollisionGraph()
     ga = graph_arrays(pack_particles(particles, pids), pack_statics(statics, sids), policy)
-    graph = CollisionGraph(dts={pid: float(d) for pid, d in zip(pids, ga.dts)})
+    graph = CollisionGraph(dts=dict(zip(pids, ga.dts.tolist())))
     pid_arr = np.asarray(pids)
-    ea, eb = pid_arr[ga.edge[:, 0]], pid_arr[ga.edge[:, 1]]
-    graph.edges = {(int(a), int(b)): (float(w[0]), float(w[1])) for a, b, w in zip(ea, eb, ga.window)}
+    ea, eb = pid_arr[ga.edge[:, 0]].tolist(), pid_arr[ga.edge[:, 1]].tolist()
+    graph.edges = dict(zip(zip(ea, eb), map(tuple, ga.window.tolist())))
     links: dict = {}
     sid_arr = np.asarray(sids)
-    for i, s in ga.link:
-        links.setdefault(int(pid_arr[i]), []).append(int(sid_arr[s]))
+    for p, s in zip(pid_arr[ga.link[:, 0]].tolist(), sid_arr[ga.link[:, 1]].tolist()):
+        links.setdefault(p, []).append(s)
     graph.static_links = {p: tuple(v) for p, v in links.items()}
     graph.stats = {"candidates": ga.candidates, "ms": ga.ms, "launches": ga.launches}
     return graph

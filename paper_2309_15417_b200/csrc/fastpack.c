@@ -118,6 +118,13 @@ static PyObject *gather_states(PyObject *self, PyObject *args) {
     /* level 3: the four field objects; level 4: their data */
     for (int f = 0; f < 4; ++f)
       for (Py_ssize_t i = 0; i < m; ++i) fld[f][i] = cur[i] ? PyObject_GetAttr(cur[i], s_fields[f]) : NULL;
+    /* prefetch pass: the array headers are read (independent misses) and
+       their data lines requested, so the copy pass below finds them cached */
+    for (Py_ssize_t i = 0; i < m; ++i) {
+      if (!cur[i]) continue;
+      for (int f = 0; f < 4; ++f)
+        if (fld[f][i] && PyArray_Check(fld[f][i])) __builtin_prefetch(PyArray_DATA((PyArrayObject *)fld[f][i]));
+    }
     int err = 0;
     for (Py_ssize_t i = 0; i < m; ++i) {
       if (!cur[i]) continue;
@@ -167,6 +174,85 @@ static PyObject *pairs_are(PyObject *self, PyObject *args) {
   return PyBool_FromLong(same);
 }
 
+static PyObject *s_old, *s_t, *s_sphere, *s_center, *s_radius;
+
+static int copy_attr(PyObject *obj, PyObject *name, double *dst, Py_ssize_t n) {
+  PyObject *v = PyObject_GetAttr(obj, name);
+  if (!v) return -1;
+  const int rc = copy_field(v, dst, n);
+  Py_DECREF(v);
+  return rc;
+}
+
+static int copy_float(PyObject *obj, PyObject *name, double *dst) {
+  PyObject *v = PyObject_GetAttr(obj, name);
+  if (!v) return -1;
+  *dst = PyFloat_AsDouble(v);
+  Py_DECREF(v);
+  return (*dst == -1.0 && PyErr_Occurred()) ? -1 : 0;
+}
+
+/* gather_broad(particles, out): the broad phase's (n, 28) particle records
+   (include/ltsgpu.h, ltsg_broad_input): old / current snapshots, current
+   velocities, and the bounding sphere (`sphere.center`, `sphere.radius`). */
+static PyObject *gather_broad(PyObject *self, PyObject *args) {
+  PyObject *parts, *out;
+  if (!PyArg_ParseTuple(args, "OO", &parts, &out)) return NULL;
+  PyObject *seq = PySequence_Fast(parts, "particles must be a sequence");
+  if (!seq) return NULL;
+  const Py_ssize_t n = PySequence_Fast_GET_SIZE(seq);
+  Py_buffer ob;
+  if (PyObject_GetBuffer(out, &ob, PyBUF_C_CONTIGUOUS | PyBUF_WRITABLE) != 0) {
+    Py_DECREF(seq);
+    return NULL;
+  }
+  if (ob.len != n * 28 * 8) {
+    PyBuffer_Release(&ob);
+    Py_DECREF(seq);
+    PyErr_SetString(PyExc_ValueError, "out must hold len(particles) x 28 float64");
+    return NULL;
+  }
+  double *rows = (double *)ob.buf;
+  memset(rows, 0, (size_t)n * 28 * 8);
+  PyObject **items = PySequence_Fast_ITEMS(seq);
+  for (Py_ssize_t i = 0; i < n; ++i) {
+    double *r = rows + i * 28;
+    PyObject *tl = PyObject_GetAttr(items[i], s_timeline);
+    if (!tl) goto fail;
+    PyObject *o = PyObject_GetAttr(tl, s_old);
+    PyObject *c = o ? PyObject_GetAttr(tl, s_current) : NULL;
+    Py_DECREF(tl);
+    if (!c) {
+      Py_XDECREF(o);
+      goto fail;
+    }
+    int err = copy_attr(o, s_fields[0], r, 3) || copy_attr(o, s_fields[2], r + 3, 4) || copy_float(o, s_t, r + 7) ||
+              copy_attr(c, s_fields[0], r + 8, 3) || copy_attr(c, s_fields[2], r + 11, 4) ||
+              copy_float(c, s_t, r + 15) || copy_attr(c, s_fields[1], r + 16, 3) ||
+              copy_attr(c, s_fields[3], r + 19, 3);
+    Py_DECREF(o);
+    Py_DECREF(c);
+    if (err) goto fail;
+    PyObject *sph = PyObject_GetAttr(items[i], s_sphere);
+    if (sph) {
+      err = copy_attr(sph, s_center, r + 22, 3) || copy_float(sph, s_radius, r + 25);
+      Py_DECREF(sph);
+    } else {  /* no sphere: a radius about the mass centre */
+      if (!PyErr_ExceptionMatches(PyExc_AttributeError)) goto fail;
+      PyErr_Clear();
+      err = copy_float(items[i], s_radius, r + 25);
+    }
+    if (err) goto fail;
+  }
+  PyBuffer_Release(&ob);
+  Py_DECREF(seq);
+  Py_RETURN_NONE;
+fail:
+  PyBuffer_Release(&ob);
+  Py_DECREF(seq);
+  return NULL;
+}
+
 /* trees_are(bodies, trees): bodies[i].tree is trees[i] for every i */
 static PyObject *trees_are(PyObject *self, PyObject *args) {
   PyObject *bodies, *trees;
@@ -198,6 +284,7 @@ static PyObject *trees_are(PyObject *self, PyObject *args) {
 static PyMethodDef methods[] = {
     {"gather_states", gather_states, METH_VARARGS, "Pack body kinematic states into an (n, 16) float64 buffer."},
     {"pairs_are", pairs_are, METH_VARARGS, "Identity check of a pair list against a flattened previous one."},
+    {"gather_broad", gather_broad, METH_VARARGS, "Pack the broad phase's (n, 28) particle records."},
     {"trees_are", trees_are, METH_VARARGS, "Identity check of the bodies' trees against a previous list."},
     {NULL, NULL, 0, NULL}};
 
@@ -208,6 +295,11 @@ PyMODINIT_FUNC PyInit__fastpack(void) {
   s_timeline = PyUnicode_InternFromString("timeline");
   s_current = PyUnicode_InternFromString("current");
   s_tree = PyUnicode_InternFromString("tree");
+  s_old = PyUnicode_InternFromString("old");
+  s_t = PyUnicode_InternFromString("t");
+  s_sphere = PyUnicode_InternFromString("sphere");
+  s_center = PyUnicode_InternFromString("center");
+  s_radius = PyUnicode_InternFromString("radius");
   s_fields[0] = PyUnicode_InternFromString("position");
   s_fields[1] = PyUnicode_InternFromString("velocity");
   s_fields[2] = PyUnicode_InternFromString("rotation");
