@@ -375,6 +375,45 @@ typedef struct {
  * angular_velocity [13] t (rows of non-members are untouched). */
 int ltsg_integrate(const ltsg_integrate_input* in, double* new_state, ltsg_workspace* ws, void* stream);
 
+/* ---------------------------------------------------------------------------
+ * Surrogate-tree construction: ltsdem.surrogate.build_surrogate_tree
+ * (surrogate.py:71-119, with _fit_parent_triangle :49-68 and
+ * kernels.morton_order kernels.py:118-135) for many meshes in one call --
+ * the narrow phase's input format (ltsg_scene.tris / ltsg_unpack_trees).
+ *
+ * All records of all meshes live in one table: `rec` (n_records, 9) float64
+ * corners, `eps` (n_records) halo widths, `kids` (n_records) int32.  The
+ * caller lays the levels out (level l+1 of a mesh has ceil(size_l / fanout)
+ * records; coarsening stops at one record or max_levels), fills the level-0
+ * rows of `rec` and `eps`, and describes each (mesh, coarse level) as a row
+ * of the device table `steps` (n_steps, 6) int64:
+ *   [in_off, n_in, out_off, n_out, key_off, group_off]
+ * in_off/n_in: the finer level's records; out_off/n_out: the coarse level's;
+ * key_off/group_off: prefix sums of n_in / n_out over the rows of the same
+ * coarse level.  Rows are grouped by coarse level; rows of level l (1-based)
+ * are [level_steps[l-1], level_steps[l]) and level_keys / level_groups (host
+ * arrays, n_levels each) hold the sums of n_in / n_out over them.
+ * The call writes every coarse record's corners and epsilon and, for every
+ * record with a parent, kids[in_off + fanout*g + j] = the j-th entry of
+ * parent g's sorted child list (surrogate.py:115).  Bit-identical to the
+ * reference with numpy's bundled OpenBLAS/LAPACK (SkylakeX kernels); see
+ * csrc/lapack3.cuh.  fanout 2..8.  Blocks until `stream` has finished. */
+typedef struct {
+  double* rec;
+  double* eps;
+  int32_t* kids;
+  const int64_t* steps;        /* device */
+  const int64_t* level_steps;  /* host, n_levels + 1 */
+  const int64_t* level_keys;   /* host, n_levels */
+  const int64_t* level_groups; /* host, n_levels */
+  int32_t n_levels;
+  int32_t fanout;
+  int32_t launches;            /* filled by the call */
+  int32_t pad;
+} ltsg_tree_build;
+
+int ltsg_build_trees(ltsg_tree_build* b, ltsg_workspace* ws, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -93,6 +93,12 @@ class IntegrateInput(C.Structure):
                 ("new_state_in", P), ("separate", I32), ("pad", I32)]
 
 
+class TreeBuild(C.Structure):
+    """ltsg_tree_build (include/ltsgpu.h)."""
+    _fields_ = [("rec", P), ("eps", P), ("kids", P), ("steps", P), ("level_steps", P), ("level_keys", P),
+                ("level_groups", P), ("n_levels", I32), ("fanout", I32), ("launches", I32), ("pad", I32)]
+
+
 _lock = threading.Lock()
 _lib = None
 
@@ -141,6 +147,7 @@ def lib():
             "ltsg_tube_rows": [P, P, P, P, P, P, P, P, P, I64, P, P, P],
             "ltsg_solve_impulses": [C.POINTER(SolveInput), C.POINTER(SolveOutput), P, P],
             "ltsg_integrate": [C.POINTER(IntegrateInput), P, P, P],
+            "ltsg_build_trees": [C.POINTER(TreeBuild), P, P],
         }.items():
             fn = getattr(h, name)
             fn.argtypes = args
@@ -161,6 +168,7 @@ EXPORTED = (
     "ltsg_overlap_centroid", "ltsg_workspace_create", "ltsg_workspace_destroy",
     "ltsg_workspace_bytes", "ltsg_search", "ltsg_exhaustive_rows", "ltsg_exhaustive_distances", "ltsg_fuse_contacts", "ltsg_fp64_peak",
     "ltsg_unpack_trees", "ltsg_broadphase", "ltsg_tube_rows", "ltsg_solve_impulses", "ltsg_integrate",
+    "ltsg_build_trees",
 )
 
 

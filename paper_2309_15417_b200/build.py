@@ -21,8 +21,8 @@ PKG = os.path.dirname(os.path.abspath(__file__))
 REPO = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
 LIB = os.path.join(PKG, "libltsgpu.so")
-SOURCES = ["rows.cu", "search.cu", "unpack.cu", "broad.cu", "contacts.cu"]
-HEADERS = ["common.cuh", "geom.cuh", "dist_staged.cuh", "dist_tile.cuh", "moving.cuh", "bound32.cuh", "quat.cuh"]
+SOURCES = ["rows.cu", "search.cu", "unpack.cu", "broad.cu", "contacts.cu", "tree.cu"]
+HEADERS = ["common.cuh", "geom.cuh", "dist_staged.cuh", "dist_tile.cuh", "moving.cuh", "bound32.cuh", "quat.cuh", "lapack3.cuh"]
 
 NVCC_FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",
