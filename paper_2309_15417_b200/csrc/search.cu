@@ -1231,17 +1231,154 @@ struct Parent {
 static_assert(sizeof(Parent) == 16, "Parent layout");
 static_assert(sizeof(Parent) <= sizeof(Cand), "parents are stored in a candidate buffer");
 
+// The decision of a static row known to be at or below its threshold
+// (`hit`): a resting record for a fine row (ccd.py:407-409), a Parent for a
+// flagged coarse row (ccd.py:410-411), appended with one atomic per warp.
+// Warp-uniform call (every lane of the warp calls it; `hit` false for idle lanes).
+__device__ __forceinline__ void static_row_hit(bool hit, int64_t ci, const Cand* __restrict__ front,
+                                               const PairInfo* __restrict__ pairs, const double* __restrict__ world,
+                                               const int64_t* __restrict__ woff, const ScreenOut& out,
+                                               Parent* __restrict__ par, unsigned long long* n_par, int lane) {
+  bool flagged = false;
+  Parent P{};
+  if (hit) {
+    const Cand c = front[ci];
+    const double* wa = world + (size_t)c.ia * kWorld;
+    const double* wb = world + (size_t)c.ib * kWorld;
+    if (c.la == 0 && c.lb == 0) {
+      const PairInfo p = pairs[c.pair];
+      const double h = add(__ldg(wa + 9), __ldg(wb + 9));
+      const unsigned long long slot = atomicAdd(&out.ctr->resting, 1ULL);
+      if (slot < out.rest_cap)
+        out.resting[slot] = RestRec{c.pair, (int32_t)(c.ia - woff[p.ba]), (int32_t)(c.ib - woff[p.bb]), 0, h};
+    } else {
+      int a0 = c.ia, b0c = c.ib, na = 1, nb = 1;
+      if (c.la > 0) {
+        const int2 cr = *reinterpret_cast<const int2*>(wa + 11);
+        a0 = cr.x;
+        na = cr.y;
+      }
+      if (c.lb > 0) {
+        const int2 cr = *reinterpret_cast<const int2*>(wb + 11);
+        b0c = cr.x;
+        nb = cr.y;
+      }
+      P = Parent{c.pair, a0, b0c, (uint8_t)na, (uint8_t)nb, (uint8_t)(c.la > 0 ? c.la - 1 : 0),
+                 (uint8_t)(c.lb > 0 ? c.lb - 1 : 0)};
+      flagged = true;
+    }
+  }
+  // per-warp append: only this warp waits for the atomic
+  const unsigned m = __ballot_sync(0xffffffffu, flagged);
+  unsigned long long base = 0;
+  if (lane == 0 && m) base = atomicAdd(n_par, (unsigned long long)__popc(m));
+  base = __shfl_sync(0xffffffffu, base, 0);
+  if (flagged) par[base + __popc(m & ((1u << lane) - 1u))] = P;
+}
+
+#ifndef LTSG_GUIDE
+#define LTSG_GUIDE 1  // guided single-feature pre-decision before the exact pass of a static generation
+#endif
+#ifndef LTSG_GUIDE_EDGES
+#define LTSG_GUIDE_EDGES 1  // the guide also ranks the nine edge-edge features
+#endif
+#ifndef LTSG_GUIDE_CULL
+#define LTSG_GUIDE_CULL 1  // rows the guide places above the threshold: certified by one separating direction
+#endif
+#ifndef LTSG_GUIDE_MINB
+#define LTSG_GUIDE_MINB 5
+#endif
+constexpr int kGuideThreads = 128;
+
+// One exact feature of ccd._feature_distances (ccd.py:135-153), squared,
+// from the world records: feature k as numbered by Guide.  The operands are
+// the ones feature_dist_sq passes (edges e_k = v[k+1] - v[k]; ab = e0,
+// ac = v2 - v0 = -e2 exactly, bc = e1), so the value is bit for bit the
+// reference's value of that feature.
+__device__ __forceinline__ double one_feature_sq(const double* wa, const double* wb, int k) {
+  auto ld = [](const double* p) { return V3{__ldg(p), __ldg(p + 1), __ldg(p + 2)}; };
+  if (k < 6) {
+    const double* pp = (k < 3 ? wa + 3 * k : wb + 3 * (k - 3));
+    const double* tt = k < 3 ? wb : wa;
+    const V3 p = ld(pp), a = ld(tt), b = ld(tt + 3), c = ld(tt + 6);
+    return point_triangle_sq<false, false>(p, a, b, c, b - a, c - a, c - b);
+  }
+  const int i = (k - 6) / 3, j = (k - 6) % 3;
+  const V3 p1 = ld(wa + 3 * i), q1 = ld(wa + 3 * (i == 2 ? 0 : i + 1));
+  const V3 p2 = ld(wb + 3 * j), q2 = ld(wb + 3 * (j == 2 ? 0 : j + 1));
+  const V3 u = q1 - p1, w = q2 - p2;
+  return segment_segment_sq<false>(p1, u, dot_simd(u, u), p2, w, dot_simd(w, w));
+}
+
+// Guided pre-decision of a static generation, one thread per frontier row.
+// The FP32 guide (bound32.cuh) names the feature most likely to be the
+// row's minimum; that one feature is evaluated with the reference's FP64
+// arithmetic, and a row whose exact feature distance is at or below the
+// row's threshold is decided: the reference's minimum over 15 features is
+// at most this feature (sqrt is monotone and correctly rounded, so
+// sqrt(d_k^2) <= T implies sqrt(min d^2) <= T).  Decided rows act here
+// (resting record / flagged parent); the others are compacted, one atomic
+// per warp, into `rest` for the exact 15-feature pass.  The guide never
+// decides anything by itself, so a wrong guess only costs time.
+__global__ void __launch_bounds__(kGuideThreads, LTSG_GUIDE_MINB)
+k_guide_static(const Cand* __restrict__ front, int64_t n, const PairInfo* __restrict__ pairs,
+               const double* __restrict__ world, const int64_t* __restrict__ woff, ScreenOut out,
+               Parent* __restrict__ par, unsigned long long* n_par, Cand* __restrict__ rest,
+               unsigned long long* n_rest) {
+  if (out.n_in) n = (int64_t)min(*out.n_in, out.next_cap);
+  const int lane = threadIdx.x & 31;
+  if (blockIdx.x == 0 && threadIdx.x == 0 && n > 0) atomicAdd(&out.ctr->screen_exact, (unsigned long long)n);
+  const int64_t n_warps = (n + 31) / 32;
+  const int wpb = kGuideThreads / 32;
+  unsigned long long decided = 0;
+  for (int64_t wi = blockIdx.x * (int64_t)wpb + (threadIdx.x >> 5); wi < n_warps; wi += (int64_t)gridDim.x * wpb) {
+    const int64_t ci = wi * 32 + lane;
+    bool hit = false, miss = false;
+    Cand c{};
+    if (ci < n) {
+      c = front[ci];
+      const double* wa = world + (size_t)c.ia * kWorld;
+      const double* wb = world + (size_t)c.ib * kWorld;
+      const double h = add(__ldg(wa + 9), __ldg(wb + 9));
+      const double T = (c.la == 0 && c.lb == 0) ? add(h, kRestSlop) : h;
+      const Guide g = feature_guide<LTSG_GUIDE_EDGES != 0>(wa, wb);
+      const float Tf = (float)T;
+      if (g.k >= 0) {
+        if (g.d2 <= Tf * Tf * 1.002f) {
+          hit = __dsqrt_rn(one_feature_sq(wa, wb, g.k)) <= T;
+        } else if (LTSG_GUIDE_CULL) {
+          // certainly above the threshold: nothing to record for this row
+          miss = direction_cull(wa, wb, guide_direction(wa, wb, g.k), add(h, kRestSlop));
+        }
+      }
+    }
+    decided += hit || miss;
+    static_row_hit(hit, ci, front, pairs, world, woff, out, par, n_par, lane);
+    const bool pend = ci < n && !hit && !miss;
+    const unsigned m = __ballot_sync(0xffffffffu, pend);
+    unsigned long long base = 0;
+    if (lane == 0 && m) base = atomicAdd(n_rest, (unsigned long long)__popc(m));
+    base = __shfl_sync(0xffffffffu, base, 0);
+    if (pend) rest[base + __popc(m & ((1u << lane) - 1u))] = c;
+  }
+  for (int o = 16; o > 0; o >>= 1) decided += __shfl_xor_sync(0xffffffffu, decided, o);
+  if (lane == 0 && decided) atomicAdd(&out.ctr->bound_rows, decided);
+}
+
 // Exact pass of a static generation.  The frontier holds only rows that
-// survived the certified culls, so every row gets the exact 15-feature
-// distance, one per lane, from shared-memory staging.  Fine rows apply the
-// resting test (ccd.py:407-409); a flagged coarse row (ccd.py:410-411)
-// becomes a Parent, appended with one atomic per block iteration.  The
-// children are generated and culled by k_expand_filter at full occupancy.
+// survived the certified culls (and, with LTSG_GUIDE, the guided
+// pre-decision), so every row gets the exact 15-feature distance, one per
+// lane, from shared-memory staging.  Fine rows apply the resting test
+// (ccd.py:407-409); a flagged coarse row (ccd.py:410-411) becomes a Parent,
+// appended with one atomic per warp.  The children are generated and culled
+// by k_expand_filter at full occupancy.  `count`: add the frontier size to
+// the exact-row counter (off when k_guide_static already counted the
+// generation's rows).
 __global__ void __launch_bounds__(32 * kStaticWarps, LTSG_STATIC_MINB)
 k_screen_static(const Cand* __restrict__ front, int64_t n, const PairInfo* __restrict__ pairs,
                 const BodyInfo* __restrict__ bodies, const double* __restrict__ world,
                 const int64_t* __restrict__ woff, ScreenOut out, Parent* __restrict__ par,
-                unsigned long long* n_par) {
+                unsigned long long* n_par, bool count) {
   if (out.n_in) n = (int64_t)min(*out.n_in, out.next_cap);
   extern __shared__ double s_stage[];  // kStaged x (32 * kStaticWarps)
   __shared__ int64_t s_q[kStaticWarps][64];
@@ -1249,47 +1386,12 @@ k_screen_static(const Cand* __restrict__ front, int64_t n, const PairInfo* __res
   const int lane = threadIdx.x & 31;
   const int warp = threadIdx.x >> 5;
   int64_t* q = s_q[warp];
-  if (blockIdx.x == 0 && threadIdx.x == 0 && n > 0) atomicAdd(&out.ctr->screen_exact, (unsigned long long)n);
+  if (count && blockIdx.x == 0 && threadIdx.x == 0 && n > 0)
+    atomicAdd(&out.ctr->screen_exact, (unsigned long long)n);
   const int64_t n_warps = (n + 31) / 32;
   unsigned long long decided = 0;
-  // the decision of a row known to be at or below (hit) its threshold or
-  // not: resting record (fine) or flagged parent (coarse); warp-uniform
   auto act = [&](bool have, int64_t ci, bool hit) {
-    bool flagged = false;
-    Parent P{};
-    if (have && hit) {
-      const Cand c = front[ci];
-      const double* wa = world + (size_t)c.ia * kWorld;
-      const double* wb = world + (size_t)c.ib * kWorld;
-      if (c.la == 0 && c.lb == 0) {
-        const PairInfo p = pairs[c.pair];
-        const double h = add(__ldg(wa + 9), __ldg(wb + 9));
-        const unsigned long long slot = atomicAdd(&out.ctr->resting, 1ULL);
-        if (slot < out.rest_cap)
-          out.resting[slot] = RestRec{c.pair, (int32_t)(c.ia - woff[p.ba]), (int32_t)(c.ib - woff[p.bb]), 0, h};
-      } else {
-        int a0 = c.ia, b0c = c.ib, na = 1, nb = 1;
-        if (c.la > 0) {
-          const int2 cr = *reinterpret_cast<const int2*>(wa + 11);
-          a0 = cr.x;
-          na = cr.y;
-        }
-        if (c.lb > 0) {
-          const int2 cr = *reinterpret_cast<const int2*>(wb + 11);
-          b0c = cr.x;
-          nb = cr.y;
-        }
-        P = Parent{c.pair, a0, b0c, (uint8_t)na, (uint8_t)nb, (uint8_t)(c.la > 0 ? c.la - 1 : 0),
-                   (uint8_t)(c.lb > 0 ? c.lb - 1 : 0)};
-        flagged = true;
-      }
-    }
-    // per-warp append: only this warp waits for the atomic
-    const unsigned m = __ballot_sync(0xffffffffu, flagged);
-    unsigned long long base = 0;
-    if (lane == 0 && m) base = atomicAdd(n_par, (unsigned long long)__popc(m));
-    base = __shfl_sync(0xffffffffu, base, 0);
-    if (flagged) par[base + __popc(m & ((1u << lane) - 1u))] = P;
+    static_row_hit(have && hit, ci, front, pairs, world, woff, out, par, n_par, lane);
   };
   // exact 15-feature distance of a queued row: is it at or below its threshold?
   auto exact_hit = [&](int64_t ci) {
@@ -2461,7 +2563,7 @@ static int run_search(const ltsg_scene* sc, ltsg_result* out, ltsg_workspace* ws
   constexpr int kMaxGen = 2 * kMaxLevels;
   unsigned long long *gen_cnt, *x_cnt;
   LTSG_TRY(ws_get(ws, "gen_cnt", kMaxGen + 1, &gen_cnt));
-  LTSG_TRY(ws_get(ws, "x_cnt", kMaxGen + 1, &x_cnt));  // static: flagged parents per generation
+  LTSG_TRY(ws_get(ws, "x_cnt", 2 * (kMaxGen + 1), &x_cnt));  // static: flagged parents per generation
   const int64_t fan = (int64_t)sc->max_children * sc->max_children;
   size_t rest_cap = std::max<size_t>(1 << 16, ws->hint_rest), entry_cap = std::max<size_t>(1 << 14, ws->hint_entries),
          cross_cap = std::max<size_t>(1 << 14, ws->hint_cross);
@@ -2488,6 +2590,8 @@ static int run_search(const ltsg_scene* sc, ltsg_result* out, ltsg_workspace* ws
     }
     return LTSG_OK;
   };
+  Cand* gbuf = nullptr;  // static generations: rows the guided pre-decision left for the exact pass
+  const bool use_guide = LTSG_GUIDE && all_static && !getenv("LTSG_NO_GUIDE");
   auto launch_screen = [&](const Cand* in, int64_t n, const unsigned long long* n_in, Cand* next,
                            unsigned long long cap, unsigned long long* n_out, Cand* xbuf,
                            unsigned long long* xcnt) -> int {
@@ -2495,12 +2599,27 @@ static int run_search(const ltsg_scene* sc, ltsg_result* out, ltsg_workspace* ws
     if (all_static) {
       // exact pass of the frontier (parents into xbuf, count in xcnt), then
       // the culled expansion of the parents into the next frontier
-      const int64_t blocks = n_in ? 148LL * LTSG_STATIC_GRID : (n + 32 * kStaticWarps - 1) / (32 * kStaticWarps);
       const size_t e = 3 * n_timed++;
       LTSG_CUDA(cudaEventRecord(ws->event(e), st));
+      const Cand* exact_in = in;
+      const unsigned long long* exact_n = n_in;
+      ScreenOut so_exact = so;
+      if (use_guide) {
+        // guided pre-decision: decided rows act at once, the rest are compacted into gbuf
+        unsigned long long* gcnt = xcnt + (kMaxGen + 1);
+        const int64_t gb = n_in ? 148LL * LTSG_GUIDE_MINB * 2 : (n + kGuideThreads - 1) / kGuideThreads;
+        k_guide_static<<<(int)std::max<int64_t>(1, std::min<int64_t>(gb, 148LL * LTSG_GUIDE_MINB * 2)), kGuideThreads, 0,
+                         st>>>(in, n, pr.pairs, world, woff, so, reinterpret_cast<Parent*>(xbuf), xcnt, gbuf, gcnt);
+        LTSG_LAUNCHED();
+        exact_in = gbuf;
+        exact_n = gcnt;
+        so_exact.n_in = gcnt;
+        so_exact.next_cap = n_in ? cap : (unsigned long long)n;  // gbuf holds at most the frontier
+      }
+      const int64_t blocks = exact_n ? 148LL * LTSG_STATIC_GRID : (n + 32 * kStaticWarps - 1) / (32 * kStaticWarps);
       k_screen_static<<<(int)std::max<int64_t>(1, std::min<int64_t>(blocks, 148LL * LTSG_STATIC_GRID)), 32 * kStaticWarps,
-                        kStaticStageBytes, st>>>(in, n, pr.pairs, pr.bodies, world, woff, so,
-                                                 reinterpret_cast<Parent*>(xbuf), xcnt);
+                        kStaticStageBytes, st>>>(exact_in, n, pr.pairs, pr.bodies, world, woff, so_exact,
+                                                 reinterpret_cast<Parent*>(xbuf), xcnt, !use_guide);
       LTSG_LAUNCHED();
       LTSG_CUDA(cudaEventRecord(ws->event(e + 1), st));
       k_expand_filter<<<148 * LTSG_EXP_GRID, kExpThreads, 0, st>>>(reinterpret_cast<const Parent*>(xbuf), xcnt, cap, (int)fan,
@@ -2566,7 +2685,7 @@ static int run_search(const ltsg_scene* sc, ltsg_result* out, ltsg_workspace* ws
     n_timed = 0;
     LTSG_CUDA(cudaMemsetAsync(d_ctr, 0, sizeof(Counters), st));
     LTSG_CUDA(cudaMemsetAsync(gen_cnt, 0, sizeof(unsigned long long) * (kMaxGen + 1), st));
-    LTSG_CUDA(cudaMemsetAsync(x_cnt, 0, sizeof(unsigned long long) * (kMaxGen + 1), st));
+    LTSG_CUDA(cudaMemsetAsync(x_cnt, 0, sizeof(unsigned long long) * 2 * (kMaxGen + 1), st));
     LTSG_TRY(ws_get(ws, "resting", rest_cap, &resting));
     LTSG_TRY(ws_get(ws, "entries", entry_cap, &entries));
     LTSG_TRY(ws_get(ws, "cross", cross_cap, &cross));
@@ -2596,6 +2715,7 @@ static int run_search(const ltsg_scene* sc, ltsg_result* out, ltsg_workspace* ws
       LTSG_TRY(ws_get(ws, "front1", cap_async, &buf[1]));
       Cand* xbuf = nullptr;
       if (all_static) LTSG_TRY(ws_get(ws, "frontx", cap_async, &xbuf));
+      if (all_static && use_guide) LTSG_TRY(ws_get(ws, "frontg", cap_async, &gbuf));
       if (!all_static && !legacy_moving) {
         mrows_cap = std::max(cap_async, (size_t)(1.25 * (double)ws->hint_mrows) + 1024);
         LTSG_TRY(ws_get(ws, "mrows", mrows_cap, &mrows));
@@ -2660,6 +2780,7 @@ static int run_search(const ltsg_scene* sc, ltsg_result* out, ltsg_workspace* ws
       LTSG_TRY(ws_get(ws, fname[fsel ^ 1], next_cap, &next));
       Cand* xbuf = nullptr;
       if (all_static) LTSG_TRY(ws_get(ws, "frontx", (size_t)n_front, &xbuf));
+      if (all_static && use_guide) LTSG_TRY(ws_get(ws, "frontg", (size_t)n_front, &gbuf));
       if (!all_static && !legacy_moving) {
         mrows_cap = std::max(mrows_cap, std::max((size_t)n_front, ws->hint_mrows) + 1024);
         LTSG_TRY(ws_get(ws, "mrows", mrows_cap, &mrows));
@@ -2671,6 +2792,7 @@ static int run_search(const ltsg_scene* sc, ltsg_result* out, ltsg_workspace* ws
         LTSG_CUDA(cudaMemcpyAsync(d_ctr, &before, sizeof(Counters), cudaMemcpyHostToDevice, st));
         LTSG_CUDA(cudaMemsetAsync(gen_cnt + 1, 0, sizeof(unsigned long long), st));
         LTSG_CUDA(cudaMemsetAsync(x_cnt, 0, sizeof(unsigned long long), st));
+        LTSG_CUDA(cudaMemsetAsync(x_cnt + (kMaxGen + 1), 0, sizeof(unsigned long long), st));
         t_screen.start(st);
         LTSG_TRY(launch_screen(front, n_front, nullptr, next, (unsigned long long)next_cap, gen_cnt + 1, xbuf,
                                x_cnt));
