@@ -223,8 +223,8 @@ def _oracle_job(idx):
 
 class OraclePool:
     """`workers` single-threaded oracle processes forked over `problems`
-    (started before the timed region; forked before this process touches
-    CUDA)."""
+    (started before the timed region; the workers run numpy only and never
+    touch CUDA)."""
 
     def __init__(self, problems, workers: int, exhaustive: bool = False):
         import multiprocessing as mp
@@ -315,6 +315,12 @@ def run_reference(args, rank, world):
     """--impl reference: the CPU oracle on this host's cores."""
     if rank != 0:
         return 0
+    # this arm is the CPU implementation end to end: its scene trees come from
+    # the CPU tree oracle too (bit-identical to the GPU builder's), no device
+    from oracle import tree_oracle
+    from paper_2309_15417_b200 import scenes
+
+    scenes.TREE_BUILDER = tree_oracle.build_many
     scene = build_scene(args.config, 0, args.pairs)
     problems = scene_problems(scene)
     workers = max(1, min(cpu_cores(), args.cpu_workers or cpu_cores()))
@@ -473,7 +479,7 @@ def gpu_workload(label, config, exhaustive, scene, problems, hs, steps, warmup, 
     kern_ms = tot("ms_exact") if (static or moving_split) else tot("ms_screen")
     return {"label": label, "config": config, "exhaustive": exhaustive, "step_ms": step_ms, "stats": stats,
             "tot": tot, "e2e_ms": e2e_ms, "phases": phases, "h2d": h2d, "d2h": d2h, "cold": cold,
-            "kernel": "k_screen_static" if static else ("k_mexact" if moving_split else "k_screen"),
+            "kernel": "k_guide_static+k_screen_static" if static else ("k_mexact" if moving_split else "k_screen"),
             "kern_ms": kern_ms, "last": res,
             "problems": len(problems), "pairs": len(hs.pair_problem), "tris": int(hs.n_tris)}
 
@@ -487,8 +493,9 @@ def summarize(m, steps, peak, cpu, par, world, total_ms=None, e2e_total=None, te
     contacts_all = tot("n_raw") if contacts_all is None else contacts_all
     exact_rows = tot("rows_screen_exact")
     bound_rows = tot("rows_bound")
-    # the exact kernel decides every row that survived the culls: by the
-    # certified FP32 upper bound or by the bit-exact distance
+    # the decide phase settles every row that survived the culls: by the
+    # guided single-feature / separating-direction certificates or by the
+    # bit-exact 15-feature distance
     decided = exact_rows + bound_rows
     achieved = decided * FLOPS_PER_TEST / (m["kern_ms"] * 1e-3) / 1e12 if m["kern_ms"] > 0 else 0.0
     achieved_exact = exact_rows * FLOPS_PER_TEST / (m["kern_ms"] * 1e-3) / 1e12 if m["kern_ms"] > 0 else 0.0
@@ -516,9 +523,10 @@ def summarize(m, steps, peak, cpu, par, world, total_ms=None, e2e_total=None, te
                      "bound_rows_per_step": bound_rows / steps,
                      "achieved_exact_only": achieved_exact,
                      "frac_exact_only": achieved_exact / peak if peak else None,
-                     "accounting": "achieved = rows the kernel decided (certified FP32 upper bound or bit-exact "
-                                   "15-feature distance) x 984 flops / kernel time; *_exact_only counts the "
-                                   "bit-exact rows alone"},
+                     "accounting": "achieved = rows the decide phase settled (static: k_guide_static's single exact "
+                                   "feature or separating direction, else k_screen_static's bit-exact 15-feature "
+                                   "distance) x 984 flops / the phase's device time; *_exact_only counts the rows "
+                                   "that ran all 15 features"},
         "breakdown_ms_per_step": {
             "screen": tot("ms_screen") / steps, "exact": tot("ms_exact") / steps,
             "expand": tot("ms_expand") / steps, "refine": tot("ms_refine") / steps,
@@ -587,6 +595,85 @@ def broad_workload(label, scene, dt_max, steps, warmup, cpu):
                                "sample": f"the whole scene through the numpy oracle (all-pairs Check 1), "
                                          f"{wall:.2f} s", "cpu_model": cpu_model()}
         out["parity"] = {"checked": 1, "bit_exact": int(same), "edges": len(o.edges), "ok": bool(same)}
+    return out
+
+
+# ------------------------------------------------------------------ surrogate-tree construction
+
+def tree_workload(steps, warmup, cpu, n_meshes=2048, subdiv=3):
+    """Surrogate-tree construction (ltsg_build_trees) of the c1/c4 mesh family:
+    `n_meshes` noisy icospheres of 20*4^subdiv triangles, every coarse level of
+    every mesh in one call.  Device time of the call with the fine level
+    resident; e2e through treebuild.build_surrogate_trees from host meshes to
+    SurrogateTree objects; CPU baseline and parity: the CPU tree oracle on a
+    sample of the same meshes."""
+    import numpy as np
+    import torch
+
+    from paper_2309_15417_b200 import scenes, treebuild
+
+    rng = np.random.default_rng(scenes.SEED + 31)
+    v0, f0 = scenes.icosphere(subdiv)
+    meshes = []
+    for _ in range(n_meshes):
+        v = v0 * (1.0 + rng.uniform(-0.05, 0.05, size=len(v0)))[:, None]
+        meshes.append(np.ascontiguousarray(np.stack([v[f0[:, 0]], v[f0[:, 1]], v[f0[:, 2]]], axis=1)))
+    eps = np.full(n_meshes, 0.01)
+    job = treebuild.DeviceTreeBuild(meshes, eps, 4, 8)
+    for _ in range(warmup):
+        job.run()
+    torch.cuda.synchronize()
+    dev_ms = []
+    for _ in range(steps):
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        job.run()
+        e1.record()
+        e1.synchronize()
+        dev_ms.append(e0.elapsed_time(e1))
+    job.fetch()
+    h2d, d2h = job.h2d_bytes, job.d2h_bytes
+    e2e_ms = []
+    trees = None
+    for i in range(1 + min(steps, 3)):
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        trees = treebuild.build_surrogate_trees(meshes, eps)
+        if i:
+            e2e_ms.append(1e3 * (time.perf_counter() - t0))
+    tris = int(sum(len(m) for m in meshes))
+    records = int(job.lay.n_records)
+    out = {"value": tris / (np.median(dev_ms) * 1e-3), "unit": "fine triangles/s",
+           "ms_per_step": float(np.median(dev_ms)), "meshes": n_meshes, "fine_triangles": tris,
+           "records_built": records - tris, "levels": int(job.lay.n_levels) + 1, "gpu_launches": 3 * int(job.lay.n_levels),
+           "e2e": {"value": tris / (np.median(e2e_ms) * 1e-3), "unit": "fine triangles/s",
+                   "ms_per_step": float(np.median(e2e_ms)), "h2d_bytes_per_step": int(h2d),
+                   "d2h_bytes_per_step": int(d2h),
+                   "path": "treebuild.build_surrogate_trees(meshes, eps): H2D of the fine level, ltsg_build_trees, "
+                           "D2H of every level, SurrogateTree objects"},
+           "description": f"build_surrogate_tree (surrogate.py:71-119) of {n_meshes} noisy {len(f0)}-triangle "
+                          f"icospheres, fanout 4, 8 levels"}
+    if cpu:
+        from oracle import tree_oracle as TO
+
+        k = min(256, n_meshes)
+        t0 = time.perf_counter()
+        want = TO.build_surrogate_trees(np.stack(meshes[:k]), 0.01)
+        wall = time.perf_counter() - t0
+        same = 0
+        for a, b in zip(trees[:k], want):
+            ok = len(a.levels) == len(b.levels)
+            for la, lb in zip(a.levels, b.levels):
+                ok = ok and np.array_equal(np.asarray(la.corners).view(np.uint64), np.asarray(lb.corners).view(np.uint64)) \
+                    and np.array_equal(np.asarray(la.epsilon).view(np.uint64), np.asarray(lb.epsilon).view(np.uint64))
+                if lb.children is not None:
+                    ok = ok and all(np.array_equal(x, y) for x, y in zip(la.children, lb.children))
+            same += bool(ok)
+        out["cpu_baseline"] = {"value": k * len(f0) / wall, "unit": "fine triangles/s", "cores": 1, "kind": "port",
+                               "sample": f"the first {k} meshes through the numpy tree oracle (vectorised over "
+                                         f"groups, LAPACK SVD), {wall:.2f} s", "cpu_model": cpu_model()}
+        out["parity"] = {"checked": k, "bit_exact": same, "ok": same == k,
+                         "contract": "bit-exact where the host's OpenBLAS selects the SkylakeX kernels lapack3.cuh restates"}
     return out
 
 
@@ -703,8 +790,10 @@ def run_ours(args, rank, world, local_rank):
     plan = list(WORKLOADS) if full else \
         [(args.config + ("_exhaustive" if args.exhaustive else ""), args.config, args.exhaustive)]
 
-    # ---- host phase, before this process starts CUDA (the scene builders and
-    # the CPU legs fork worker processes): scenes, packing, CPU baselines
+    # ---- setup phase: scenes (their surrogate trees come from the product's GPU
+    # builder, treebuild.py), packing, and the CPU baselines (forked oracle
+    # processes that never touch CUDA)
+    torch.cuda.set_device(local_rank)
     t_build = time.perf_counter()
     built = {}
     prep = []
@@ -725,9 +814,7 @@ def run_ours(args, rank, world, local_rank):
             and float(max(scene.dt)) > 0.0
         prep.append((label, config, exhaustive, scene, problems, hs, cpu, idx, ores, spinning, setup_s))
     t_build = time.perf_counter() - t_build
-    scenes.MP_CONTEXT = "forkserver"  # nothing forks from a CUDA process below
 
-    torch.cuda.set_device(local_rank)
     dist = None
     if world > 1:
         import torch.distributed as dist
@@ -806,6 +893,9 @@ def run_ours(args, rank, world, local_rank):
             if config in built:
                 broad[label] = broad_workload(label, built[config][0], dt_max, min(args.steps, 10), args.warmup,
                                               not args.no_cpu)
+    tree_build = None
+    if full and rank == 0:
+        tree_build = {"treebuild_c1": tree_workload(min(args.steps, 10), args.warmup, not args.no_cpu)}
     clocks.__exit__(None, None, None)
 
     if rank == 0:
@@ -840,8 +930,9 @@ def run_ours(args, rank, world, local_rank):
             "roofline": dict(s0["roofline"], peak_source="in-run DFMA microbenchmark (ltsg_fp64_peak); "
                                                          "MEASURED_PEAKS.json has no FP64 entry",
                              flops_per_test=FLOPS_PER_TEST,
-                             note="achieved counts only rows that ran the exact 15-feature distance; "
-                                  "rows settled by the certified culls count in `value`"),
+                             note="achieved counts the rows that reached the decide phase (984 algorithmic flops "
+                                  "each, SURVEY 8(d)); rows settled earlier by the certified culls count only in "
+                                  "`value`"),
             "roofline_distance_kernel": allpairs,
             "gpu_launches": s0["gpu_launches"],
             "breakdown_ms_per_step": s0["breakdown_ms_per_step"],
@@ -859,6 +950,8 @@ def run_ours(args, rank, world, local_rank):
             line["broadphase"] = broad
         if consumers:
             line["contact_consumers"] = consumers
+        if tree_build:
+            line["tree_build"] = tree_build
         print(json.dumps(line), flush=True)
     if dist is not None:
         dist.destroy_process_group()

@@ -1,6 +1,6 @@
 """Correctly rounded fused multiply-add for float64 numpy arrays.
 
-Used only by host-side input construction (`surrogate.py`) to reproduce
+Used only by the tree oracle (`tree_oracle.py`) to reproduce
 OpenBLAS's FMA-based `dgemv` order.  Error-free product (Dekker/Veltkamp)
 and sum (Knuth TwoSum); the two low parts are combined with
 round-to-odd before the final rounding, which makes the result correctly

@@ -1,27 +1,27 @@
-"""Host-side surrogate-tree construction (the narrow phase's input format).
+"""CPU oracle of surrogate-tree construction.  TEST INFRASTRUCTURE: only
+`tests/`, `__graft_entry__.smoke()` and `bench.py`'s CPU legs may import it;
+the product builds trees on the GPU (`paper_2309_15417_b200/treebuild.py`,
+csrc/tree.cu) and has no CPU path.
 
 Restates `ltsdem.surrogate.build_surrogate_tree` (surrogate.py:71-119) with
 `_fit_parent_triangle` (surrogate.py:49-68) and `kernels.morton_order`
-(kernels.py:118-135), vectorised over the groups of a level so that the
-20k-particle synthetic scenes build in seconds instead of minutes.  Tree
-construction is input setup and sits outside the hot path (SURVEY.md
-§8(f) item 3 lists a GPU builder as a later row).
+(kernels.py:118-135), vectorised over the groups of a level.  The
+arithmetic matches the reference op for op (centroids by sequential row
+sums, the 3x3 `dgemv` order ``fma(r2,u2, fma(r0,u0, r1*u1))`` for
+``rel @ u``, batched LAPACK SVD which equals the per-group call).
 
-The arithmetic matches the reference op for op (centroids by sequential
-row sums, the 3x3 `dgemv` order ``fma(r2,u2, fma(r0,u0, r1*u1))`` for
-``rel @ u``, batched LAPACK SVD which equals the per-group call), so on the
-build container the trees are bit-identical to the reference's
-(`tests/test_host_inputs.py` checks this against reference-built goldens).
-On another host, LAPACK may differ in the last bits; that only changes the
-synthetic input, never the GPU-vs-oracle comparison, which always runs on
-one shared set of trees.
+Pinned: `tests/test_tree_oracle.py` checks it bit for bit against trees the
+reference itself built (tests/golden/trees_gpu.npz, trees.npz; generator
+tests/golden/make_golden_trees.py).  The plane fit calls numpy's SVD, i.e.
+the host's LAPACK; `oracle/lapack_svd.py` restates that routine explicitly
+and is what csrc/lapack3.cuh implements.
 """
 
 from __future__ import annotations
 
 import numpy as np
 
-from .bodies import ChildIndex, SurrogateLevel, SurrogateTree
+from paper_2309_15417_b200.bodies import ChildIndex, SurrogateLevel, SurrogateTree
 
 _EPS_PAD = 1e-12
 _TINY = 1e-300
@@ -228,3 +228,22 @@ def build_surrogate_trees(corners, epsilon: float, fanout: int = 4, max_levels: 
         size = G
         depth += 1
     return [SurrogateTree(levels=lv) for lv in levels]
+
+
+def build_many(corners_list, epsilons, fanout: int = 4, max_levels: int = 8) -> list:
+    """Trees of arbitrary meshes (the signature of treebuild.build_surrogate_trees):
+    meshes with equal triangle count and epsilon go through the batched builder."""
+    corners_list = [np.ascontiguousarray(np.asarray(c, dtype=np.float64).reshape(-1, 3, 3)) for c in corners_list]
+    eps = np.broadcast_to(np.asarray(epsilons, dtype=np.float64), (len(corners_list),))
+    groups = {}
+    for k, c in enumerate(corners_list):
+        groups.setdefault((len(c), float(eps[k])), []).append(k)
+    out = [None] * len(corners_list)
+    for (n, e), idx in groups.items():
+        for lo in range(0, len(idx), 256):
+            part = idx[lo:lo + 256]
+            trees = build_surrogate_trees(np.stack([corners_list[k] for k in part]), e, fanout=fanout,
+                                          max_levels=max_levels)
+            for k, t in zip(part, trees):
+                out[k] = t
+    return out

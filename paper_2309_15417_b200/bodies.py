@@ -168,7 +168,7 @@ def make_particle(pid: int, vertices, triangles, epsilon: float, st: ParticleSta
                   fanout: int = 4, tree=None) -> Particle:
     """Recentre the mesh on its mass centre and build its surrogate tree
     (body.py:56-85).  `tree` may be supplied to reuse a cached build."""
-    from .surrogate import build_surrogate_tree
+    from .treebuild import build_surrogate_tree
 
     v = np.asarray(vertices, dtype=np.float64)
     t = np.asarray(triangles, dtype=np.int64)
@@ -195,7 +195,7 @@ def bounding_sphere(vertices, epsilon: float) -> BoundingSphere:
 
 
 def make_static(sid: int, vertices, triangles, epsilon: float, fanout: int = 4) -> StaticBody:
-    from .surrogate import build_surrogate_tree
+    from .treebuild import build_surrogate_tree
 
     if sid >= 0:
         raise ValueError(f"static ids are negative, got {sid}")

@@ -4,8 +4,9 @@ No dataset is involved: BASELINE.json describes each configuration by its
 shapes, sizes and value distributions, and these generators reproduce
 them with `np.random.default_rng(230915417 + config_index)` (SURVEY.md
 §8(d)).  Every generator takes a scale argument so tests can build the
-same distribution at small size.  Building bodies (mass centre, recentring,
-surrogate trees) is host setup and is not timed by `bench.py`.
+same distribution at small size.  Building bodies (mass centre, recentring)
+is host setup; their surrogate trees come from the GPU builder (treebuild.py).
+Scene setup is not timed by `bench.py`.
 
 c1  static pairs of 3x-subdivided noisy icospheres (1280 tris), eps 0.01
 c2  dominoes: 12-tri boxes 0.1 x 0.5 x 1.0 in a row, gap 0.08, tilts, eps 1e-3
@@ -23,24 +24,6 @@ import numpy as np
 from . import bodies as B
 
 SEED = 230915417
-
-# Process-pool start method of the scene builders.  "fork" is cheapest; a
-# caller that has already initialised CUDA (bench.py building its second
-# workload) switches to "forkserver" so no worker inherits a CUDA context.
-MP_CONTEXT = "fork"
-
-
-def _pool(workers):
-    import multiprocessing as mp
-
-    return mp.get_context(MP_CONTEXT).Pool(workers)
-
-
-def _workers(workers=None):
-    import os
-
-    return workers or min(os.cpu_count() or 1, 32)
-
 
 # ---------------------------------------------------------------- meshes
 
@@ -154,10 +137,31 @@ def _noisy_icosphere_trees(rng, n, subdiv, noise, eps, radius=1.0):
     return out
 
 
-def _tree_chunk(args):
-    corners, eps = args
-    from .surrogate import build_surrogate_trees
-    return build_surrogate_trees(corners, eps)
+# The surrogate trees of a scene: `TREE_BUILDER(corners_list, epsilons)` ->
+# list of SurrogateTree.  None selects the product builder, the GPU
+# (`treebuild.build_surrogate_trees`, one device call for all meshes).
+# CPU-only test runs install the CPU oracle's builder here (tests/conftest.py);
+# both give bit-identical trees (tests/test_gpu_treebuild.py).
+TREE_BUILDER = None
+
+
+def build_trees(corners_list, eps) -> list:
+    if TREE_BUILDER is not None:
+        return TREE_BUILDER(corners_list, eps)
+    from .treebuild import build_surrogate_trees
+
+    out = []
+    # bounded device batches: ~2M fine triangles per call
+    lo = 0
+    eps = np.broadcast_to(np.asarray(eps, dtype=np.float64), (len(corners_list),))
+    while lo < len(corners_list):
+        hi, tris = lo, 0
+        while hi < len(corners_list) and (hi == lo or tris + len(corners_list[hi]) <= (1 << 21)):
+            tris += len(corners_list[hi])
+            hi += 1
+        out += build_surrogate_trees(corners_list[lo:hi], eps[lo:hi])
+        lo = hi
+    return out
 
 
 def _recentre(meshes, eps):
@@ -177,36 +181,19 @@ def _recentre(meshes, eps):
 
 def make_particles(ids, meshes, eps, states, workers=None):
     """Batched make_particle for meshes sharing one triangle topology:
-    centres of mass, recentring and surrogate trees vectorised across
-    particles, trees built on `workers` processes for large batches."""
+    centres of mass and recentring vectorised across particles, all trees
+    in one builder call."""
     corners, radius = _recentre(meshes, eps)
-    P = len(meshes)
-    workers = _workers(workers)
-    # worker processes only for big batches (bench setup)
-    if P >= 1024 and workers > 1:
-        chunks = np.array_split(np.arange(P), min(workers * 4, P))
-        with _pool(workers) as pool:
-            parts = pool.map(_tree_chunk, [(corners[ch], eps) for ch in chunks])
-        trees = [t for part in parts for t in part]
-    else:
-        trees = _tree_chunk((corners, eps))
+    trees = build_trees(list(corners), eps)
     return [B.Particle(pid=int(i), tree=t, epsilon=float(eps), radius=float(r), timeline=B.timeline(st))
             for i, t, r, st in zip(ids, trees, radius, states)]
 
 
-def _each_chunk(specs):
-    out = []
-    for pid, v, f, eps, st, key in specs:
-        out.append(B.make_particle(pid, v, f, eps, st))
-    return out
-
-
 def make_particles_each(specs, workers=None, share=None):
     """B.make_particle for every (pid, vertices, faces, eps, state, key) of
-    `specs` (meshes of any topology), on worker processes for big batches.
-    Specs with an equal non-None `key` share the tree of the first one
-    (identical meshes).  Same particles as the serial loop."""
-    workers = _workers(workers)
+    `specs` (meshes of any topology), all trees in one builder call.  Specs
+    with an equal non-None `key` share the tree of the first one (identical
+    meshes).  Same particles as the serial loop."""
     first = {}
     todo = []
     for sp in specs:
@@ -215,20 +202,18 @@ def make_particles_each(specs, workers=None, share=None):
             if key is not None:
                 first[key] = sp[0]
             todo.append(sp)
-    if len(todo) >= 256 and workers > 1:
-        chunks = [todo[i::workers * 4] for i in range(workers * 4)]
-        with _pool(workers) as pool:
-            parts = pool.map(_each_chunk, chunks)
-        built = {p.pid: p for part in parts for p in part}
-    else:
-        built = {p.pid: p for p in _each_chunk(todo)}
+    corners = []
+    for pid, v, f, eps, st, key in todo:
+        v = np.asarray(v, dtype=np.float64)
+        f = np.asarray(f, dtype=np.int64)
+        c = v - B.centre_of_mass(v, f)
+        corners.append(np.stack([c[f[:, 0]], c[f[:, 1]], c[f[:, 2]]], axis=1))
+    trees = build_trees(corners, [sp[3] for sp in todo])
+    tree_of = {sp[0]: t for sp, t in zip(todo, trees)}
     out = {}
     for pid, v, f, eps, st, key in specs:
-        if pid in built:
-            out[pid] = built[pid]
-        else:
-            src = built[first[key]]
-            out[pid] = B.make_particle(pid, v, f, eps, st, tree=src.tree)
+        tree = tree_of[pid] if pid in tree_of else tree_of[first[key]]
+        out[pid] = B.make_particle(pid, v, f, eps, st, tree=tree)
     return out
 
 
@@ -256,13 +241,12 @@ def config2(n_boxes: int = 4096, seed_offset: int = 2) -> Scene:
     v, f = box((0.1, 0.5, 1.0))
     tilt = rng.uniform(0.0, 0.3, size=n_boxes)
     particles = {}
-    tree = None
+    c = v - B.centre_of_mass(v, f)
+    tree = build_trees([np.stack([c[f[:, 0]], c[f[:, 1]], c[f[:, 2]]], axis=1)], eps)[0]
     for i in range(n_boxes):
         q = np.array([np.cos(0.5 * tilt[i]), 0.0, np.sin(0.5 * tilt[i]), 0.0])
         st = B.state((0.18 * i, 0.0, 0.5), rotation=q)
-        p = B.make_particle(i, v, f, eps, st, tree=tree)
-        tree = p.tree
-        particles[i] = p
+        particles[i] = B.make_particle(i, v, f, eps, st, tree=tree)
     r = particles[0].radius
     pairs = []
     for i in range(n_boxes):

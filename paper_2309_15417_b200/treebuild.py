@@ -75,10 +75,74 @@ class TreeLayout:
         self.n_levels = depth - 1
 
 
+class DeviceTreeBuild:
+    """The inputs of one `ltsg_build_trees` call resident on the device:
+    `run()` launches the build (idempotent: the fine level is input, the
+    coarse levels are rewritten), `fetch()` reads the records back."""
+
+    def __init__(self, corners, eps, fanout: int, max_levels: int, stream=None):
+        torch = _lib.require_cuda()
+        self.torch = torch
+        self.corners = corners
+        self.eps = eps
+        self.lay = lay = TreeLayout([len(c) for c in corners], fanout, max_levels)
+        rec = np.zeros((lay.n_records, 9))
+        epsv = np.zeros(lay.n_records)
+        for p, c in enumerate(corners):
+            o = lay.level_off[p][0]
+            rec[o:o + len(c)] = c.reshape(-1, 9)
+            epsv[o:o + len(c)] = eps[p]
+        self.h2d_bytes = rec.nbytes + epsv.nbytes + lay.steps.nbytes
+        dev = torch.device("cuda", torch.cuda.current_device())
+        self.stream = stream if stream is not None else torch.cuda.current_stream()
+        with torch.cuda.stream(self.stream):
+            self.d_rec = torch.from_numpy(rec).to(dev, non_blocking=False)
+            self.d_eps = torch.from_numpy(epsv).to(dev)
+            self.d_kids = torch.full((max(lay.n_records, 1),), -1, dtype=torch.int32, device=dev)
+            self.d_steps = torch.from_numpy(lay.steps if len(lay.steps) else np.zeros((1, 6), np.int64)).to(dev)
+        self.b = _lib.TreeBuild(rec=self.d_rec.data_ptr(), eps=self.d_eps.data_ptr(), kids=self.d_kids.data_ptr(),
+                                steps=self.d_steps.data_ptr(), level_steps=lay.level_steps.ctypes.data,
+                                level_keys=lay.level_keys.ctypes.data if lay.n_levels else 0,
+                                level_groups=lay.level_groups.ctypes.data if lay.n_levels else 0,
+                                n_levels=lay.n_levels, fanout=fanout)
+        if lay.n_levels == 0:  # every mesh is a single triangle: nothing to coarsen
+            self.b.level_keys = self.b.level_groups = lay.level_steps.ctypes.data
+
+    def run(self) -> None:
+        with self.torch.cuda.stream(self.stream):
+            _lib.check(_lib.lib().ltsg_build_trees(C.byref(self.b), _lib.workspace().handle,
+                                                   C.c_void_p(self.stream.cuda_stream)), "ltsg_build_trees")
+
+    def fetch(self):
+        with self.torch.cuda.stream(self.stream):
+            rec_out = self.d_rec.cpu().numpy()
+            eps_out = self.d_eps.cpu().numpy()
+            kids_out = self.d_kids.cpu().numpy().astype(np.int64)
+        self.d2h_bytes = rec_out.nbytes + eps_out.nbytes + self.d_kids.numel() * 4
+        return rec_out, eps_out, kids_out
+
+    def trees(self) -> list:
+        rec_out, eps_out, kids_out = self.fetch()
+        lay, fanout = self.lay, self.lay.fanout
+        trees = []
+        for p, c in enumerate(self.corners):
+            lv, off = lay.levels[p], lay.level_off[p]
+            levels = [SurrogateLevel(corners=c, epsilon=np.full(len(c), float(self.eps[p])), children=None)]
+            for l in range(1, len(lv)):
+                o, n = off[l], lv[l]
+                fo, fn = off[l - 1], lv[l - 1]
+                ptr = np.minimum(np.arange(n + 1, dtype=np.int64) * fanout, fn)
+                levels.append(SurrogateLevel(corners=rec_out[o:o + n].reshape(n, 3, 3).copy(),
+                                             epsilon=eps_out[o:o + n].copy(),
+                                             children=ChildIndex(ptr, kids_out[fo:fo + fn])))
+            trees.append(SurrogateTree(levels=levels))
+        return trees
+
+
 def build_surrogate_trees(meshes, epsilons, fanout: int = 4, max_levels: int = 8,
                           stream=None) -> list:
     """build_surrogate_tree for every (mesh, epsilon) in one device call."""
-    torch = _lib.require_cuda()
+    _lib.require_cuda()
     corners = [_corners_of(m) for m in meshes]
     eps = np.broadcast_to(np.asarray(epsilons, dtype=np.float64), (len(corners),))
     for e in eps:
@@ -93,45 +157,9 @@ def build_surrogate_trees(meshes, epsilons, fanout: int = 4, max_levels: int = 8
     for c in corners:
         if len(c) == 0:
             raise ValueError("mesh has no triangles")
-    lay = TreeLayout([len(c) for c in corners], fanout, max_levels)
-    rec = np.zeros((lay.n_records, 9))
-    epsv = np.zeros(lay.n_records)
-    for p, c in enumerate(corners):
-        o = lay.level_off[p][0]
-        rec[o:o + len(c)] = c.reshape(-1, 9)
-        epsv[o:o + len(c)] = eps[p]
-    dev = torch.device("cuda", torch.cuda.current_device())
-    st = stream if stream is not None else torch.cuda.current_stream()
-    with torch.cuda.stream(st):
-        d_rec = torch.from_numpy(rec).to(dev, non_blocking=False)
-        d_eps = torch.from_numpy(epsv).to(dev)
-        d_kids = torch.full((max(lay.n_records, 1),), -1, dtype=torch.int32, device=dev)
-        d_steps = torch.from_numpy(lay.steps if len(lay.steps) else np.zeros((1, 6), np.int64)).to(dev)
-        b = _lib.TreeBuild(rec=d_rec.data_ptr(), eps=d_eps.data_ptr(), kids=d_kids.data_ptr(),
-                           steps=d_steps.data_ptr(), level_steps=lay.level_steps.ctypes.data,
-                           level_keys=lay.level_keys.ctypes.data if lay.n_levels else 0,
-                           level_groups=lay.level_groups.ctypes.data if lay.n_levels else 0,
-                           n_levels=lay.n_levels, fanout=fanout)
-        if lay.n_levels == 0:  # every mesh is a single triangle: nothing to coarsen
-            b.level_keys = b.level_groups = lay.level_steps.ctypes.data
-        _lib.check(_lib.lib().ltsg_build_trees(C.byref(b), _lib.workspace().handle, C.c_void_p(st.cuda_stream)),
-                   "ltsg_build_trees")
-        rec_out = d_rec.cpu().numpy()
-        eps_out = d_eps.cpu().numpy()
-        kids_out = d_kids.cpu().numpy().astype(np.int64)
-    trees = []
-    for p, c in enumerate(corners):
-        lv, off = lay.levels[p], lay.level_off[p]
-        levels = [SurrogateLevel(corners=c, epsilon=np.full(len(c), float(eps[p])), children=None)]
-        for l in range(1, len(lv)):
-            o, n = off[l], lv[l]
-            fo, fn = off[l - 1], lv[l - 1]
-            ptr = np.minimum(np.arange(n + 1, dtype=np.int64) * fanout, fn)
-            levels.append(SurrogateLevel(corners=rec_out[o:o + n].reshape(n, 3, 3).copy(),
-                                         epsilon=eps_out[o:o + n].copy(),
-                                         children=ChildIndex(ptr, kids_out[fo:fo + fn])))
-        trees.append(SurrogateTree(levels=levels))
-    return trees
+    job = DeviceTreeBuild(corners, eps, fanout, max_levels, stream)
+    job.run()
+    return job.trees()
 
 
 def build_surrogate_tree(mesh, epsilon: float, fanout: int = 4, max_levels: int = 8) -> SurrogateTree:

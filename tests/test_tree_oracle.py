@@ -2,7 +2,7 @@
 
 * The reference-built fixtures (tests/golden/trees_gpu.npz, made by
   make_golden_trees.py from ltsdem.surrogate.build_surrogate_tree) equal
-  the host numpy restatement (surrogate.py) bit for bit on this host.
+  the CPU tree oracle (oracle/tree_oracle.py) bit for bit on this host.
 * The oracle's LAPACK restatement (oracle/lapack_svd.py, the algorithm
   csrc/lapack3.cuh implements) gives numpy's V^T bit for bit on every
   plane-fit group of the fixtures and on degenerate matrices.
@@ -16,7 +16,7 @@ import pytest
 from helpers import golden
 from golden import scene_codec as SC
 from oracle import lapack_svd as L
-from paper_2309_15417_b200 import surrogate as S
+from oracle import tree_oracle as S
 from paper_2309_15417_b200.treebuild import TreeLayout, level_sizes
 
 

