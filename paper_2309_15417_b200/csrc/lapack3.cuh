@@ -13,7 +13,7 @@
 // The LAPACK Fortran is compiled without FMA (separately rounded IEEE
 // operations, which -fmad=false plus the __d*_rn helpers give here).  The
 // BLAS calls inside it are OpenBLAS kernels with their own summation orders,
-// pinned by probing the library (tools/blas_probe.py, tools/svd_proto.py):
+// pinned by probing the library (tools/blas_probe.py, oracle/lapack_svd.py):
 //   dnrm2     x87 extended precision: four 64-bit-mantissa accumulators,
 //             fsqrt, one rounding to double (emulated exactly with integers)
 //   dgemv_t   SSE2 4x2 / 4x1 kernels over the rows m & ~3, then the scalar
@@ -21,7 +21,7 @@
 //   dgemv_n   (m <= 3 rows) one FMA chain per row over the columns
 //   dger      a[i,j] = fma(alpha*y[j], x[i], a[i,j])
 //   drot      x' = fma(c, x, s*y), y' = fma(c, y, -(s*x))
-// tools/svd_proto.py is the Python statement of the same algorithm; it and
+// oracle/lapack_svd.py is the Python statement of the same algorithm; it and
 // this file agree bit for bit with numpy on random, degenerate (tied and
 // zero singular values, exact zeros) and surrogate-tree matrices.
 #pragma once

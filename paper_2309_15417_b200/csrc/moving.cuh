@@ -124,6 +124,93 @@ __device__ __forceinline__ double traj_d2(const double (*tr)[32], int o, double 
   }
   return d2;
 }
+// The same trajectory from registers: tr[0..2] dP0, [3..5] dV, [6..8] Ba,
+// [9..11] Ca, [12..14] Bb, [15..17] Cb, [18] wa, [19] wb.
+__device__ __forceinline__ double traj_d2_regs(const double* tr, double tau) {
+  double sa = 0.0, ca = 0.0, sb = 0.0, cb = 0.0;
+  if (tr[18] != 0.0) {
+    sincos(tr[18] * tau, &sa, &ca);
+    ca = 1.0 - ca;
+  }
+  if (tr[19] != 0.0) {
+    sincos(tr[19] * tau, &sb, &cb);
+    cb = 1.0 - cb;
+  }
+  double d2 = 0.0;
+#pragma unroll
+  for (int k = 0; k < 3; ++k) {
+    double d = fma(tau, tr[3 + k], tr[k]);
+    d = fma(sa, tr[6 + k], d);
+    d = fma(ca, tr[9 + k], d);
+    d = fma(-sb, tr[12 + k], d);
+    d = fma(-cb, tr[15 + k], d);
+    d2 = fma(d, d, d2);
+  }
+  return d2;
+}
+
+// A candidate's trajectory constants and the limit of its per-row sphere
+// test (`lim`: radii + threshold + cull margin; +inf for slivers, which are
+// never culled) and the coordinate scale the margins are taken from.
+__device__ __forceinline__ void traj_build(const double* cma, const double* ra_, const double* cmb, const double* rb_,
+                                           double dt, double thr, double h, double* tr, double* lim, double* scale) {
+  const TrajSide sa_ = traj_side(cma, ra_, dt);
+  const TrajSide sb_ = traj_side(cmb, rb_, dt);
+#pragma unroll
+  for (int k = 0; k < 3; ++k) {
+    tr[k] = sa_.p0[k] - sb_.p0[k];
+    tr[3 + k] = sa_.v[k] - sb_.v[k];
+    tr[6 + k] = sa_.b[k];
+    tr[9 + k] = sa_.c[k];
+    tr[12 + k] = sb_.b[k];
+    tr[15 + k] = sb_.c[k];
+  }
+  tr[18] = sa_.w;
+  tr[19] = sb_.w;
+  const double rA = __ldg(ra_ + 15), rB = __ldg(rb_ + 15);
+  *scale = 1.0 + sa_.bound + sb_.bound + fabs(rA) + fabs(rB);
+  const double T = fmax(thr, add(h, kRestSlop));
+  *lim = (rA >= 0.0 && rB >= 0.0) ? rA + rB + T + kCullMargin * *scale : CUDART_INF;
+}
+
+#ifndef LTSG_MSCREEN_F32
+#define LTSG_MSCREEN_F32 1  // FP32 pre-test of the per-row sphere cull, FP64 only inside its error band
+#endif
+// FP32 evaluation of the trajectory distance.  Its error against the FP64
+// value is below 4e-6 * scale (conversion of the 20 constants and of tau,
+// ~20 roundings of partial sums bounded by `scale`, and the 4e-7 absolute
+// error of __sincosf on |w tau| < pi times the rotation coefficients, all
+// included in `scale`); the band below uses 1e-4 * scale, 25x that.  A row
+// is settled in FP32 only when its distance clears the band on either side:
+// culled above lim + E, kept below lim - E.  Rows inside the band take the
+// FP64 test, so the surviving rows are exactly those of the FP64 test.
+constexpr double kF32Band = 1e-4;
+constexpr int kTrajF = 22;  // 18 constants, wa, wb, (lim + E)^2, (lim - E)^2
+
+__device__ __forceinline__ float traj_d2f(const float (*tr)[32], int o, float tau) {
+  float sa = 0.f, ca = 0.f, sb = 0.f, cb = 0.f;
+  const float wa = tr[18][o], wb = tr[19][o];
+  if (wa != 0.f) {
+    __sincosf(wa * tau, &sa, &ca);
+    ca = 1.f - ca;
+  }
+  if (wb != 0.f) {
+    __sincosf(wb * tau, &sb, &cb);
+    cb = 1.f - cb;
+  }
+  float d2 = 0.f;
+#pragma unroll
+  for (int k = 0; k < 3; ++k) {
+    float d = __fmaf_rn(tau, tr[3 + k][o], tr[k][o]);
+    d = __fmaf_rn(sa, tr[6 + k][o], d);
+    d = __fmaf_rn(ca, tr[9 + k][o], d);
+    d = __fmaf_rn(-sb, tr[12 + k][o], d);
+    d = __fmaf_rn(-cb, tr[15 + k][o], d);
+    d2 = __fmaf_rn(d, d, d2);
+  }
+  return d2;
+}
+
 constexpr int kMRows = 32 * kMaxSamples;  // rows of one warp's 32 candidates, at most
 
 // Pose for the culls at sample i of linspace(w0, dt, n) (= tau): the pose
@@ -294,13 +381,21 @@ k_mscreen(const Cand* __restrict__ front, int64_t n, const PairInfo* __restrict_
   if (out.n_in) n = (int64_t)min(*out.n_in, out.next_cap);
   __shared__ MCandInfo s_info[kMWarps][32];
   __shared__ uint16_t s_queue[kMWarps][kMRows];  // row (11 bits) | owner lane << 11
+#if LTSG_MSCREEN_F32
+  __shared__ float s_traj[kMWarps][kTrajF][32];
+#else
   __shared__ double s_traj[kMWarps][kTraj][32];
+#endif
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
   const int64_t n_warps = (n + 31) / 32;
   MCandInfo* info = s_info[warp];
   uint16_t* queue = s_queue[warp];
+#if LTSG_MSCREEN_F32
+  float(*traj)[32] = s_traj[warp];
+#else
   double(*traj)[32] = s_traj[warp];
+#endif
   unsigned long long acc_rows = 0, acc_exact = 0, acc_window = 0, acc_sphere = 0;
 
   for (int64_t wi = blockIdx.x * (int64_t)kMWarps + warp; wi < n_warps; wi += (int64_t)gridDim.x * kMWarps) {
@@ -336,28 +431,32 @@ k_mscreen(const Cand* __restrict__ front, int64_t n, const PairInfo* __restrict_
       me.cull_lo = -1.0;
       me.cull_hi = 2.0 * p.dt + 1.0;
       // the sphere-centre trajectories (see kTraj)
-      const TrajSide sa_ = traj_side(pt.cm + (size_t)p.ba * kCullM, ra_, p.dt);
-      const TrajSide sb_ = traj_side(pt.cm + (size_t)p.bb * kCullM, rb_, p.dt);
+      double tr[20], lim, scale;
+      traj_build(pt.cm + (size_t)p.ba * kCullM, ra_, pt.cm + (size_t)p.bb * kCullM, rb_, p.dt, me.thr, me.h, tr, &lim,
+                 &scale);
+#if LTSG_MSCREEN_F32
 #pragma unroll
-      for (int k = 0; k < 3; ++k) {
-        traj[k][lane] = sa_.p0[k] - sb_.p0[k];
-        traj[3 + k][lane] = sa_.v[k] - sb_.v[k];
-        traj[6 + k][lane] = sa_.b[k];
-        traj[9 + k][lane] = sa_.c[k];
-        traj[12 + k][lane] = sb_.b[k];
-        traj[15 + k][lane] = sb_.c[k];
+      for (int k = 0; k < 20; ++k) traj[k][lane] = (float)tr[k];
+      {
+        const double E = kF32Band * scale;
+        const double hi = lim + E, lo = fmax(lim - E, 0.0);
+        // rounded outwards, so the FP32 limits never narrow the band
+        traj[20][lane] = lim < CUDART_INF ? __double2float_ru(hi * hi) : CUDART_INF_F;
+        traj[21][lane] = lim < CUDART_INF ? __double2float_rd(lo * lo) : CUDART_INF_F;
+        if (!(scale < 1e15) && lim < CUDART_INF) {  // beyond a safe FP32 range: every row takes the FP64 test
+          traj[20][lane] = CUDART_INF_F;
+          traj[21][lane] = 0.f;
+        }
       }
-      traj[18][lane] = sa_.w;
-      traj[19][lane] = sb_.w;
-      const double rA = __ldg(ra_ + 15), rB = __ldg(rb_ + 15);
-      const double scale = 1.0 + sa_.bound + sb_.bound + fabs(rA) + fabs(rB);
-      const double T = fmax(me.thr, add(me.h, kRestSlop));
-      const double lim = rA + rB + T + kCullMargin * scale;
-      traj[20][lane] = (rA >= 0.0 && rB >= 0.0) ? lim * lim : CUDART_INF;
-      if (rA >= 0.0 && rB >= 0.0) {
-        const double g0 = sqrt(traj_d2(traj, lane, c.w0)) - lim;
+#else
+#pragma unroll
+      for (int k = 0; k < 20; ++k) traj[k][lane] = tr[k];
+      traj[20][lane] = lim < CUDART_INF ? lim * lim : CUDART_INF;
+#endif
+      if (lim < CUDART_INF) {
+        const double g0 = sqrt(traj_d2_regs(tr, c.w0)) - lim;
         double g1 = g0;
-        if (p.dt > c.w0) g1 = sqrt(traj_d2(traj, lane, p.dt)) - lim;
+        if (p.dt > c.w0) g1 = sqrt(traj_d2_regs(tr, p.dt)) - lim;
         if (sp > 0.0) {
           me.cull_lo = c.w0 + g0 / sp;
           me.cull_hi = p.dt - g1 / sp;
@@ -389,7 +488,22 @@ k_mscreen(const Cand* __restrict__ front, int64_t n, const PairInfo* __restrict_
         const int i = r - c.first;
         const double tau = cand_tau(c, i);
         keep = !(tau < c.cull_lo || tau > c.cull_hi);
+#if LTSG_MSCREEN_F32
+        if (keep) {
+          const float d2f = traj_d2f(traj, o, (float)tau);
+          if (d2f > traj[20][o]) {
+            keep = false;  // certainly clear
+          } else if (!(d2f < traj[21][o])) {
+            // inside the FP32 error band: the FP64 test decides
+            double tr[20], lim, scale;
+            traj_build(pt.cm + (size_t)c.ba * kCullM, tris + c.off_a * kRecord, pt.cm + (size_t)c.bb * kCullM,
+                       tris + c.off_b * kRecord, c.dt, c.thr, c.h, tr, &lim, &scale);
+            keep = !(traj_d2_regs(tr, tau) > lim * lim);
+          }
+        }
+#else
         if (keep) keep = !(traj_d2(traj, o, tau) > traj[20][o]);
+#endif
       }
       const unsigned m = __ballot_sync(0xffffffffu, keep);
       if (keep) queue[nq + __popc(m & ((1u << lane) - 1u))] = (uint16_t)(r | (o << 11));
