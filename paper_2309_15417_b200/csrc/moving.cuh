@@ -174,18 +174,27 @@ __device__ __forceinline__ void traj_build(const double* cma, const double* ra_,
 }
 
 #ifndef LTSG_MSCREEN_F32
-#define LTSG_MSCREEN_F32 1  // FP32 pre-test of the per-row sphere cull, FP64 only inside its error band
+#define LTSG_MSCREEN_F32 0  // FP32 pre-test of the per-row sphere cull, FP64 only inside its error band (measured: no gain)
 #endif
-// FP32 evaluation of the trajectory distance.  Its error against the FP64
-// value is below 4e-6 * scale (conversion of the 20 constants and of tau,
-// ~20 roundings of partial sums bounded by `scale`, and the 4e-7 absolute
-// error of __sincosf on |w tau| < pi times the rotation coefficients, all
-// included in `scale`); the band below uses 1e-4 * scale, 25x that.  A row
+// FP32 evaluation of the trajectory distance.  With s32 the sum of the
+// magnitudes of the terms it adds (|dP0| + dt |dV| + |B| + 2 |C| per side,
+// plus lim), its error against the FP64 value is below 4e-6 * s32
+// (conversion of the 20 constants and of tau, ~20 roundings of partial sums
+// bounded by s32, and the 4e-7 absolute error of __sincosf on |w tau| < pi
+// times the rotation coefficients); the band below uses 1e-4 * s32, 25x that.  A row
 // is settled in FP32 only when its distance clears the band on either side:
 // culled above lim + E, kept below lim - E.  Rows inside the band take the
 // FP64 test, so the surviving rows are exactly those of the FP64 test.
 constexpr double kF32Band = 1e-4;
 constexpr int kTrajF = 22;  // 18 constants, wa, wb, (lim + E)^2, (lim - E)^2
+
+// the FP64 per-row sphere test from scratch (rows inside the FP32 band)
+__device__ __noinline__ bool sphere_keep_f64(const double* cma, const double* ra_, const double* cmb,
+                                             const double* rb_, double dt, double thr, double h, double tau) {
+  double tr[20], lim, scale;
+  traj_build(cma, ra_, cmb, rb_, dt, thr, h, tr, &lim, &scale);
+  return !(traj_d2_regs(tr, tau) > lim * lim);
+}
 
 __device__ __forceinline__ float traj_d2f(const float (*tr)[32], int o, float tau) {
   float sa = 0.f, ca = 0.f, sb = 0.f, cb = 0.f;
@@ -438,12 +447,19 @@ k_mscreen(const Cand* __restrict__ front, int64_t n, const PairInfo* __restrict_
 #pragma unroll
       for (int k = 0; k < 20; ++k) traj[k][lane] = (float)tr[k];
       {
-        const double E = kF32Band * scale;
+        // the magnitudes the FP32 evaluation actually handles: the centre
+        // DIFFERENCE and its rates (not the absolute positions in `scale`)
+        double s32 = lim < CUDART_INF ? lim : 0.0;
+#pragma unroll
+        for (int k = 0; k < 3; ++k)
+          s32 += fabs(tr[k]) + p.dt * fabs(tr[3 + k]) + fabs(tr[6 + k]) + 2.0 * fabs(tr[9 + k]) + fabs(tr[12 + k]) +
+                 2.0 * fabs(tr[15 + k]);
+        const double E = kF32Band * s32;
         const double hi = lim + E, lo = fmax(lim - E, 0.0);
         // rounded outwards, so the FP32 limits never narrow the band
         traj[20][lane] = lim < CUDART_INF ? __double2float_ru(hi * hi) : CUDART_INF_F;
         traj[21][lane] = lim < CUDART_INF ? __double2float_rd(lo * lo) : CUDART_INF_F;
-        if (!(scale < 1e15) && lim < CUDART_INF) {  // beyond a safe FP32 range: every row takes the FP64 test
+        if (!(s32 < 1e15) && lim < CUDART_INF) {  // beyond a safe FP32 range: every row takes the FP64 test
           traj[20][lane] = CUDART_INF_F;
           traj[21][lane] = 0.f;
         }
@@ -495,10 +511,8 @@ k_mscreen(const Cand* __restrict__ front, int64_t n, const PairInfo* __restrict_
             keep = false;  // certainly clear
           } else if (!(d2f < traj[21][o])) {
             // inside the FP32 error band: the FP64 test decides
-            double tr[20], lim, scale;
-            traj_build(pt.cm + (size_t)c.ba * kCullM, tris + c.off_a * kRecord, pt.cm + (size_t)c.bb * kCullM,
-                       tris + c.off_b * kRecord, c.dt, c.thr, c.h, tr, &lim, &scale);
-            keep = !(traj_d2_regs(tr, tau) > lim * lim);
+            keep = sphere_keep_f64(pt.cm + (size_t)c.ba * kCullM, tris + c.off_a * kRecord,
+                                   pt.cm + (size_t)c.bb * kCullM, tris + c.off_b * kRecord, c.dt, c.thr, c.h, tau);
           }
         }
 #else
