@@ -173,9 +173,6 @@ __device__ __forceinline__ void traj_build(const double* cma, const double* ra_,
   *lim = (rA >= 0.0 && rB >= 0.0) ? rA + rB + T + kCullMargin * *scale : CUDART_INF;
 }
 
-#ifndef LTSG_MSCREEN_PREFETCH
-#define LTSG_MSCREEN_PREFETCH 0
-#endif
 #ifndef LTSG_MSCREEN_F32
 #define LTSG_MSCREEN_F32 0  // FP32 pre-test of the per-row sphere cull, FP64 only inside its error band (measured: no gain)
 #endif
@@ -424,14 +421,6 @@ k_mscreen(const Cand* __restrict__ front, int64_t n, const PairInfo* __restrict_
       me.off_b = B.level_off[c.lb] + c.ib;
       const double* ra_ = tris + me.off_a * kRecord;
       const double* rb_ = tris + me.off_b * kRecord;
-#if LTSG_MSCREEN_PREFETCH
-      // the corner sectors of both records towards L2: the separating-axis
-      // stage gathers them much later, and its first touch otherwise waits on DRAM
-      asm volatile("prefetch.global.L2 [%0];" ::"l"(ra_));
-      asm volatile("prefetch.global.L2 [%0];" ::"l"(ra_ + 4));
-      asm volatile("prefetch.global.L2 [%0];" ::"l"(rb_));
-      asm volatile("prefetch.global.L2 [%0];" ::"l"(rb_ + 4));
-#endif
       me.h = add(__ldg(ra_ + 9), __ldg(rb_ + 9));  // ccd.py:339
       double sp = p.speed0;                        // ccd.py:340-345
       if (A.m.omega > 0.0) sp = add(sp, mul(A.m.omega, __ldg(ra_ + 10)));
