@@ -165,3 +165,61 @@ def test_interpenetrating_and_touching_vs_oracle(G):
         b = B.make_particle(101 + 2 * k, v, f, eps, B.state(pos, rotation=ident), tree=tree)
         pairs.append((a, b))
     _check_pairs_vs_oracle(G, pairs, "overlap/touch")
+
+
+def test_guide_on_equals_guide_off_random_poses(G, monkeypatch):
+    """400 random body pairs (icospheres, rocks and boxes of random size,
+    halo and pose; separated, grazing and deeply overlapping) in one batch:
+    guide on and off give identical arrays."""
+    from paper_2309_15417_b200 import bodies as B
+    from paper_2309_15417_b200 import scenes
+
+    rng = np.random.default_rng(2309)
+    protos = []
+    for sub in (0, 1, 2):
+        protos.append(scenes.icosphere(sub))
+    for _ in range(3):
+        protos.append(scenes.rock(rng))
+    protos.append(scenes.box((1.0, 0.6, 0.3)))
+    corners, eps_list, spec = [], [], []
+    for k in range(800):
+        v, f = protos[int(rng.integers(len(protos)))]
+        v = v * float(np.exp(rng.uniform(np.log(0.2), np.log(3.0))))
+        eps = float(10.0 ** rng.uniform(-4, -1.5))
+        c = v - B.centre_of_mass(v, f)
+        corners.append(np.stack([c[f[:, 0]], c[f[:, 1]], c[f[:, 2]]], axis=1))
+        eps_list.append(eps)
+        spec.append((v, f, eps))
+    trees = scenes.build_trees(corners, eps_list)
+    quats = scenes.random_quaternions(rng, 800)
+    pairs = []
+    for k in range(400):
+        (va, fa, ea), (vb, fb, eb) = spec[2 * k], spec[2 * k + 1]
+        ra = float(np.linalg.norm(corners[2 * k].reshape(-1, 3), axis=1).max())
+        rb = float(np.linalg.norm(corners[2 * k + 1].reshape(-1, 3), axis=1).max())
+        axis = rng.normal(size=3)
+        axis /= np.linalg.norm(axis)
+        dist = (ra + rb) * float(rng.choice([0.0, 0.3, 0.7, 0.95, 1.0, 1.02, 1.3]))
+        base = rng.normal(size=3) * 10.0
+        a = B.make_particle(2 * k, va, fa, ea, B.state(base, rotation=quats[2 * k]), tree=trees[2 * k])
+        b = B.make_particle(2 * k + 1, vb, fb, eb, B.state(base + dist * axis, rotation=quats[2 * k + 1]),
+                            tree=trees[2 * k + 1])
+        pairs.append((a, b))
+    runs = {}
+    for mode in ("on", "off"):
+        if mode == "off":
+            monkeypatch.setenv("LTSG_NO_GUIDE", "1")
+        else:
+            monkeypatch.delenv("LTSG_NO_GUIDE", raising=False)
+        runs[mode] = [G.earliest_contacts(pairs, 0.0, raw=True) for _ in range(2)]
+    for k in range(2):
+        _same_batch(runs["on"][k], runs["off"][k], f"random poses call {k}")
+    assert runs["on"][1].stats["rows_bound"] > 0
+    assert len(runs["on"][1].raw["t"]) > 1000  # the batch really produces contacts
+    # and a sample of the pairs against the oracle
+    for k in rng.choice(400, size=12, replace=False):
+        a, b = pairs[int(k)]
+        ref = O.pair_earliest_contact(a, b, 0.0)
+        got = runs["on"][1].result(int(k))
+        assert got.dt == ref.dt and got.collision == ref.collision
+        compare_contacts(got.contacts, SC.encode_contacts(ref.contacts), label=f"random pair {k}")
