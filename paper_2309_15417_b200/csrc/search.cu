@@ -1695,6 +1695,13 @@ __global__ void k_bisect(const Bracket* __restrict__ br, int64_t n, const PairIn
 
 // ---------------------------------------------------------------- finalize
 
+// 1 in *flag when any problem has a nonzero step (the batch is not static)
+__global__ void k_any_moving(const double* __restrict__ problem_dt, int n, int32_t* flag) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  const bool moving = i < n && problem_dt[i] != 0.0;
+  if (__any_sync(0xffffffffu, moving) && (threadIdx.x & 31) == 0) atomicOr(flag, 1);
+}
+
 __global__ void k_init_problems(unsigned long long* tau_min_bits, int n) {
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i < n) tau_min_bits[i] = 0x7ff0000000000000ULL;  // +inf
@@ -2480,38 +2487,54 @@ static int run_search(const ltsg_scene* sc, ltsg_result* out, ltsg_workspace* ws
   k_init_problems<<<grid_for(np, 128), 128, 0, st>>>(tau_min, np);
   LTSG_LAUNCHED();
 
-  // ---- static batches: tau = 0 world records, sphere data, culled seeds
+  // ---- static batches: tau = 0 world records, sphere data, culled seeds.
+  // Three host decisions are needed before the traversal can be sized: is
+  // every step zero, how many world records, how many seed rows.  Their
+  // inputs are computed back to back and read with ONE synchronisation.
   bool all_static = false;
   double* world = nullptr;
   double* wsph = nullptr;
   int64_t* woff = nullptr;
+  int64_t seed_total = 0;
+  int64_t *seed_cnt = nullptr, *seed_off = nullptr;
   if (sc->n_pairs > 0) {
-    std::vector<double> hdt(np);
-    LTSG_CUDA(cudaMemcpyAsync(hdt.data(), sc->problem_dt, sizeof(double) * np, cudaMemcpyDeviceToHost, st));
-    LTSG_CUDA(cudaStreamSynchronize(st));
-    all_static = std::all_of(hdt.begin(), hdt.end(), [](double d) { return d == 0.0; });
-    if (sc->max_children > 255) all_static = false;  // static parents hold 8-bit child counts
-    const char* env = getenv("LTSG_NO_STATIC");
-    if (env && env[0] == '1') all_static = false;
-  }
-  if (all_static) {
+    int32_t* d_moving;
     int64_t* wcnt;
+    LTSG_TRY(ws_get(ws, "any_moving", (size_t)1, &d_moving));
     LTSG_TRY(ws_get(ws, "world_cnt", (size_t)sc->n_bodies + 1, &wcnt));
     LTSG_TRY(ws_get(ws, "world_off", (size_t)sc->n_bodies + 1, &woff));
+    LTSG_TRY(ws_get(ws, "seed_cnt", (size_t)sc->n_pairs + 1, &seed_cnt));
+    LTSG_TRY(ws_get(ws, "seed_off", (size_t)sc->n_pairs + 1, &seed_off));
+    LTSG_CUDA(cudaMemsetAsync(d_moving, 0, sizeof(int32_t), st));
+    k_any_moving<<<grid_for(np, 128), 128, 0, st>>>(sc->problem_dt, np, d_moving);
+    LTSG_LAUNCHED();
     k_world_count<<<grid_for(sc->n_bodies + 1, 128), 128, 0, st>>>(pr.bodies, sc->n_bodies, wcnt);
     LTSG_LAUNCHED();
     LTSG_TRY(scan_exclusive(ws, wcnt, woff, sc->n_bodies + 1, st));
+    k_seed_count<<<grid_for(sc->n_pairs, 128), 128, 0, st>>>(pr.pairs, sc->n_pairs, pr.bodies,
+                                                             sc->exhaustive, seed_cnt);
+    LTSG_LAUNCHED();
+    LTSG_CUDA(cudaMemsetAsync(seed_cnt + sc->n_pairs, 0, sizeof(int64_t), st));
+    LTSG_TRY(scan_exclusive(ws, seed_cnt, seed_off, sc->n_pairs + 1, st));
+    int32_t h_moving = 1;
     int64_t n_world = 0;
+    LTSG_CUDA(cudaMemcpyAsync(&h_moving, d_moving, sizeof(int32_t), cudaMemcpyDeviceToHost, st));
     LTSG_CUDA(cudaMemcpyAsync(&n_world, woff + sc->n_bodies, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+    LTSG_CUDA(cudaMemcpyAsync(&seed_total, seed_off + sc->n_pairs, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
     LTSG_CUDA(cudaStreamSynchronize(st));
-    if (n_world >= (int64_t)1 << 31) {
-      all_static = false;  // world indices are int32 in the candidates
-    } else {
+    all_static = h_moving == 0;
+    if (sc->max_children > 255) all_static = false;  // static parents hold 8-bit child counts
+    const char* env = getenv("LTSG_NO_STATIC");
+    if (env && env[0] == '1') all_static = false;
+    if (n_world >= (int64_t)1 << 31) all_static = false;  // world indices are int32 in the candidates
+    if (all_static) {
       LTSG_TRY(ws_get(ws, "world", (size_t)std::max<int64_t>(n_world, 1) * (kWorld + kSph), &world));
       wsph = world + (size_t)std::max<int64_t>(n_world, 1) * kWorld;
       k_world_fill<<<(int)std::max<int64_t>(1, std::min<int64_t>((n_world + 127) / 128, 148 * 16)), 128, 0, st>>>(
           pr.bodies, sc->n_bodies, woff, sc->tris, world, wsph);
       LTSG_LAUNCHED();
+    } else {
+      woff = nullptr;
     }
   }
 
@@ -2546,19 +2569,6 @@ static int run_search(const ltsg_scene* sc, ltsg_result* out, ltsg_workspace* ws
   // on the device, buffers are sized from the workspace's history) and
   // checks once at the end; on any overflow the traversal re-runs in sync
   // mode, which reads each frontier size back and grows buffers as needed.
-  int64_t seed_total = 0;
-  int64_t *seed_cnt = nullptr, *seed_off = nullptr;
-  if (sc->n_pairs > 0) {
-    LTSG_TRY(ws_get(ws, "seed_cnt", (size_t)sc->n_pairs + 1, &seed_cnt));
-    LTSG_TRY(ws_get(ws, "seed_off", (size_t)sc->n_pairs + 1, &seed_off));
-    k_seed_count<<<grid_for(sc->n_pairs, 128), 128, 0, st>>>(pr.pairs, sc->n_pairs, pr.bodies,
-                                                             sc->exhaustive, seed_cnt);
-    LTSG_LAUNCHED();
-    LTSG_CUDA(cudaMemsetAsync(seed_cnt + sc->n_pairs, 0, sizeof(int64_t), st));
-    LTSG_TRY(scan_exclusive(ws, seed_cnt, seed_off, sc->n_pairs + 1, st));
-    LTSG_CUDA(cudaMemcpyAsync(&seed_total, seed_off + sc->n_pairs, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
-    LTSG_CUDA(cudaStreamSynchronize(st));
-  }
   tr.mark("poses+seedcnt");
   constexpr int kMaxGen = 2 * kMaxLevels;
   unsigned long long *gen_cnt, *x_cnt;
