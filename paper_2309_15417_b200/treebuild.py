@@ -114,26 +114,36 @@ class DeviceTreeBuild:
                                                    C.c_void_p(self.stream.cuda_stream)), "ltsg_build_trees")
 
     def fetch(self):
-        with self.torch.cuda.stream(self.stream):
-            rec_out = self.d_rec.cpu().numpy()
-            eps_out = self.d_eps.cpu().numpy()
+        """Read the build back: the coarse records and halos (the fine level
+        is the caller's input and is not copied back) and the child index."""
+        torch, lay = self.torch, self.lay
+        if not hasattr(self, "_coarse_idx"):
+            coarse = np.ones(lay.n_records, dtype=bool)
+            for p, c in enumerate(self.corners):
+                o = lay.level_off[p][0]
+                coarse[o:o + len(c)] = False
+            self._coarse_pos = np.cumsum(coarse) - 1  # record offset -> row of the coarse read-back
+            self._coarse_idx = torch.from_numpy(np.flatnonzero(coarse)).to(self.d_rec.device)
+        with torch.cuda.stream(self.stream):
+            rec_out = self.d_rec.index_select(0, self._coarse_idx).cpu().numpy()
+            eps_out = self.d_eps.index_select(0, self._coarse_idx).cpu().numpy()
             kids_out = self.d_kids.cpu().numpy().astype(np.int64)
         self.d2h_bytes = rec_out.nbytes + eps_out.nbytes + self.d_kids.numel() * 4
         return rec_out, eps_out, kids_out
 
     def trees(self) -> list:
         rec_out, eps_out, kids_out = self.fetch()
-        lay, fanout = self.lay, self.lay.fanout
+        lay, fanout, pos = self.lay, self.lay.fanout, self._coarse_pos
         trees = []
         for p, c in enumerate(self.corners):
             lv, off = lay.levels[p], lay.level_off[p]
             levels = [SurrogateLevel(corners=c, epsilon=np.full(len(c), float(self.eps[p])), children=None)]
             for l in range(1, len(lv)):
-                o, n = off[l], lv[l]
+                o, n = int(pos[off[l]]), lv[l]
                 fo, fn = off[l - 1], lv[l - 1]
                 ptr = np.minimum(np.arange(n + 1, dtype=np.int64) * fanout, fn)
-                levels.append(SurrogateLevel(corners=rec_out[o:o + n].reshape(n, 3, 3).copy(),
-                                             epsilon=eps_out[o:o + n].copy(),
+                levels.append(SurrogateLevel(corners=rec_out[o:o + n].reshape(n, 3, 3),
+                                             epsilon=eps_out[o:o + n],
                                              children=ChildIndex(ptr, kids_out[fo:fo + fn])))
             trees.append(SurrogateTree(levels=levels))
         return trees
