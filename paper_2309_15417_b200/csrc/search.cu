@@ -1239,8 +1239,9 @@ __device__ __forceinline__ void static_row_hit(bool hit, int64_t ci, const Cand*
                                                const PairInfo* __restrict__ pairs, const double* __restrict__ world,
                                                const int64_t* __restrict__ woff, const ScreenOut& out,
                                                Parent* __restrict__ par, unsigned long long* n_par, int lane) {
-  bool flagged = false;
+  bool flagged = false, rest = false;
   Parent P{};
+  RestRec R{};
   if (hit) {
     const Cand c = front[ci];
     const double* wa = world + (size_t)c.ia * kWorld;
@@ -1248,9 +1249,8 @@ __device__ __forceinline__ void static_row_hit(bool hit, int64_t ci, const Cand*
     if (c.la == 0 && c.lb == 0) {
       const PairInfo p = pairs[c.pair];
       const double h = add(__ldg(wa + 9), __ldg(wb + 9));
-      const unsigned long long slot = atomicAdd(&out.ctr->resting, 1ULL);
-      if (slot < out.rest_cap)
-        out.resting[slot] = RestRec{c.pair, (int32_t)(c.ia - woff[p.ba]), (int32_t)(c.ib - woff[p.bb]), 0, h};
+      R = RestRec{c.pair, (int32_t)(c.ia - woff[p.ba]), (int32_t)(c.ib - woff[p.bb]), 0, h};
+      rest = true;
     } else {
       int a0 = c.ia, b0c = c.ib, na = 1, nb = 1;
       if (c.la > 0) {
@@ -1268,7 +1268,15 @@ __device__ __forceinline__ void static_row_hit(bool hit, int64_t ci, const Cand*
       flagged = true;
     }
   }
-  // per-warp append: only this warp waits for the atomic
+  // per-warp appends: one atomic per warp and list
+  const unsigned mr = __ballot_sync(0xffffffffu, rest);
+  if (mr) {
+    unsigned long long rbase = 0;
+    if (lane == 0) rbase = atomicAdd(&out.ctr->resting, (unsigned long long)__popc(mr));
+    rbase = __shfl_sync(0xffffffffu, rbase, 0);
+    const unsigned long long slot = rbase + __popc(mr & ((1u << lane) - 1u));
+    if (rest && slot < out.rest_cap) out.resting[slot] = R;
+  }
   const unsigned m = __ballot_sync(0xffffffffu, flagged);
   unsigned long long base = 0;
   if (lane == 0 && m) base = atomicAdd(n_par, (unsigned long long)__popc(m));
