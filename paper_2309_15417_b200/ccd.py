@@ -199,24 +199,44 @@ class DeviceScene:
 
 
 class DeviceResult:
-    """Caller-owned output buffers of ltsg_search."""
+    """Caller-owned output buffers of ltsg_search.  Every array is a view of
+    one device allocation, laid out in three regions (per-problem arrays,
+    fused contacts, raw contacts) so that `to_host` reads a region back with
+    one copy."""
 
     def __init__(self, n_problems: int, capacity: int, device, raw: bool):
         import torch
 
         self.capacity = int(max(capacity, 1))
         self.n_problems = n_problems
-        self.f = {}
-        self.r = {}
-        self.dt = torch.empty(max(n_problems, 1), dtype=torch.float64, device=device)
-        self.first = torch.empty(max(n_problems, 1), dtype=torch.float64, device=device)
-        self.coll = torch.empty(max(n_problems, 1), dtype=torch.int32, device=device)
-        self.off = torch.empty(n_problems + 1, dtype=torch.int64, device=device)
-        tdt = {np.int32: torch.int32, np.float64: torch.float64}
+        n = max(n_problems, 1)
+        tdt = {np.int32: torch.int32, np.float64: torch.float64, np.int64: torch.int64}
+        plan = []  # (region, name, numpy dtype, shape)
+        plan += [("p", "dt", np.float64, (n,)), ("p", "first", np.float64, (n,)),
+                 ("p", "off", np.int64, (n_problems + 1,)), ("p", "coll", np.int32, (n,))]
         for name, dt, shape in _CONTACT_FIELDS:
-            self.f[name] = torch.empty((self.capacity, *shape), dtype=tdt[dt], device=device)
-            if raw:
-                self.r[name] = torch.empty((self.capacity, *shape), dtype=tdt[dt], device=device)
+            plan.append(("f", name, dt, (self.capacity, *shape)))
+        if raw:
+            for name, dt, shape in _CONTACT_FIELDS:
+                plan.append(("r", name, dt, (self.capacity, *shape)))
+        self.layout = {}
+        self.region = {}
+        off = 0
+        for reg, name, dt, shape in plan:
+            nbytes = int(np.prod(shape)) * np.dtype(dt).itemsize
+            lo = self.region.setdefault(reg, [off, off])[0]
+            self.layout[(reg, name)] = (off, nbytes, dt, shape)
+            off = (off + nbytes + 15) // 16 * 16
+            self.region[reg] = [lo, off]
+        self.blob = torch.empty(max(off, 16), dtype=torch.uint8, device=device)
+
+        def view(reg, name):
+            o, nb, dt, shape = self.layout[(reg, name)]
+            return self.blob[o:o + nb].view(tdt[dt]).view(shape)
+
+        self.dt, self.first, self.off, self.coll = (view("p", k) for k in ("dt", "first", "off", "coll"))
+        self.f = {name: view("f", name) for name, _dt, _shape in _CONTACT_FIELDS}
+        self.r = {name: view("r", name) for name, _dt, _shape in _CONTACT_FIELDS} if raw else {}
 
     def struct(self) -> _lib.Result:
         f, r = self.f, self.r
@@ -241,30 +261,51 @@ class DeviceResult:
         return res
 
     def to_host(self, st: _lib.Result) -> BatchResult:
-        """All outputs in one pass: async copies into pinned host tensors
-        (torch's caching host allocator), one stream synchronisation."""
+        """All outputs in one pass: async copies into pinned host memory
+        (torch's caching host allocator), one stream synchronisation.  A region
+        whose used rows fill at least half of its capacity is read back with
+        ONE copy (the host arrays are views of it); a sparsely filled region
+        is copied field by field, used rows only."""
         import torch
 
         n = self.n_problems
         nf, nr = int(st.n_fused), int(st.n_raw)
         stream = torch.cuda.current_stream(self.dt.device)
+        tdt = {np.int32: torch.int32, np.float64: torch.float64, np.int64: torch.int64}
 
-        def d2h(v):
-            h = torch.empty(v.shape, dtype=v.dtype, pin_memory=True)
-            h.copy_(v, non_blocking=True)
-            return h
+        def region(reg, names, rows):
+            """Host views of the first `rows` rows of the region's arrays."""
+            lo, hi = self.region[reg]
+            if rows is None or 2 * rows >= self.capacity:
+                h = torch.empty(hi - lo, dtype=torch.uint8, pin_memory=True)
+                h.copy_(self.blob[lo:hi], non_blocking=True)
+                out = {}
+                for name in names:
+                    o, nb, dt, shape = self.layout[(reg, name)]
+                    v = h[o - lo:o - lo + nb].view(tdt[dt]).view(shape)
+                    out[name] = v if rows is None else v[:rows]
+                return out
+            out = {}
+            for name in names:
+                v = (self.f if reg == "f" else self.r)[name][:rows]
+                h = torch.empty(v.shape, dtype=v.dtype, pin_memory=True)
+                h.copy_(v, non_blocking=True)
+                out[name] = h
+            return out
 
-        fused = {k: d2h(v[:nf]) for k, v in self.f.items()}
-        raw = {k: d2h(v[:nr]) for k, v in self.r.items()} if self.r else None
-        dt, coll, first, off = d2h(self.dt[:n]), d2h(self.coll[:n]), d2h(self.first[:n]), d2h(self.off)
+        names = [name for name, _dt, _shape in _CONTACT_FIELDS]
+        per = region("p", ("dt", "first", "off", "coll"), None)
+        fused = region("f", names, nf)
+        raw = region("r", names, nr) if self.r else None
         stream.synchronize()
         stats = {k: int(getattr(st, k)) for k in (
             "rows_screen", "rows_zoom", "rows_bisect", "rows_executed", "candidates",
             "generations", "n_raw", "n_fused", "launches", "rows_screen_exact", "rows_bound")}
         stats.update({k: float(getattr(st, k)) for k in ("ms_screen", "ms_refine", "ms_contacts", "ms_exact",
                                                            "ms_expand")})
-        return BatchResult(dt=dt.numpy(), collision=coll.numpy() != 0, first_contact=first.numpy(),
-                           fused_offset=off.numpy(), contacts={k: v.numpy() for k, v in fused.items()},
+        return BatchResult(dt=per["dt"][:n].numpy(), collision=per["coll"][:n].numpy() != 0,
+                           first_contact=per["first"][:n].numpy(), fused_offset=per["off"].numpy(),
+                           contacts={k: v.numpy() for k, v in fused.items()},
                            raw={k: v.numpy() for k, v in raw.items()} if raw is not None else None, stats=stats)
 
 
