@@ -1296,7 +1296,13 @@ __device__ __forceinline__ void static_row_hit(bool hit, int64_t ci, const Cand*
 #ifndef LTSG_GUIDE_MINB
 #define LTSG_GUIDE_MINB 5
 #endif
-constexpr int kGuideThreads = 128;
+#ifndef LTSG_GUIDE_THREADS
+#define LTSG_GUIDE_THREADS 128
+#endif
+#ifndef LTSG_GUIDE_GRID
+#define LTSG_GUIDE_GRID 2  // persistent grid: blocks per resident block slot
+#endif
+constexpr int kGuideThreads = LTSG_GUIDE_THREADS;
 
 // One exact feature of ccd._feature_distances (ccd.py:135-153), squared,
 // from the world records: feature k as numbered by Guide.  The operands are
@@ -2625,8 +2631,8 @@ static int run_search(const ltsg_scene* sc, ltsg_result* out, ltsg_workspace* ws
       if (use_guide) {
         // guided pre-decision: decided rows act at once, the rest are compacted into gbuf
         unsigned long long* gcnt = xcnt + (kMaxGen + 1);
-        const int64_t gb = n_in ? 148LL * LTSG_GUIDE_MINB * 2 : (n + kGuideThreads - 1) / kGuideThreads;
-        k_guide_static<<<(int)std::max<int64_t>(1, std::min<int64_t>(gb, 148LL * LTSG_GUIDE_MINB * 2)), kGuideThreads, 0,
+        const int64_t gb = n_in ? 148LL * LTSG_GUIDE_MINB * LTSG_GUIDE_GRID : (n + kGuideThreads - 1) / kGuideThreads;
+        k_guide_static<<<(int)std::max<int64_t>(1, std::min<int64_t>(gb, 148LL * LTSG_GUIDE_MINB * LTSG_GUIDE_GRID)), kGuideThreads, 0,
                          st>>>(in, n, pr.pairs, world, woff, so, reinterpret_cast<Parent*>(xbuf), xcnt, gbuf, gcnt);
         LTSG_LAUNCHED();
         exact_in = gbuf;
